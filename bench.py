@@ -1,0 +1,338 @@
+"""Benchmark of the NGF + curvature objective/gradient hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--workload c3]
+
+One step = one objective+gradient evaluation (LevelObjective.__call__) of the
+config-3 finest level: synthetic 256^3 CT-shaped pair, 64^3 deformation grid,
+NGF tau = rho = 10, alpha = 1, fp32.  `value` is whole-job evaluations/s with
+the inputs resident in HBM; `e2e` is the same metric through the numpy-facing
+LevelObjective call (H2D of y, D2H of J and the gradient inside the timed
+region).  The line also carries the full 4-level 256^3 registration time (the
+paper's headline), the fused kernel's roofline against MEASURED_PEAKS.json, the
+CPU baseline (the oracle port on this host) and the SM clocks seen.
+
+For N > 1 (torchrun), every rank registers its own pair (config 4: independent
+pairs, one per GPU, no data-path collective); timings are max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "256^3 full-registration time (s); obj+grad evals/s; HBM GB/s vs peak"
+
+WORKLOADS = {
+    # name: (image n, grid ratio, levels for the full registration)
+    "c1": (64, 4, 1),
+    "c2": (128, 4, 3),
+    "c3": (256, 4, 4),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-register", action="store_true", help="skip the full-registration leg")
+    ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU baseline work")
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.stop = threading.Event()
+        self.th = threading.Thread(target=self.run, daemon=True)
+
+    def run(self):
+        while not self.stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self.stop.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop.set()
+        self.th.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def make_inputs(n: int, ratio: int, seed: int):
+    import paper_1812_06765_b200 as ngf
+    R, T, _ = ngf.ct_pair(n, seed=seed, dtype=np.float32)
+    gd = ngf.deformation_grid_for(R.grid, ratio)
+    y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=2.0).field.astype(np.float32)
+    return R, T, gd, y
+
+
+def cpu_baseline(R, T, gd, y, budget_s: float):
+    """The oracle port (numpy restatement of the reference, oracle/) on this host's cores."""
+    from oracle import ngf_oracle as O
+    cores = os.cpu_count() or 1
+    og = O.grid(R.grid.dims, R.grid.spacing, R.grid.origin)
+    ogd = O.grid(gd.dims, gd.spacing, gd.origin)
+    obj = O.Objective(T.values, R.values, ogd, og, workers=cores)
+    t0 = time.perf_counter()
+    obj(y.ravel())  # warm (thread pools, page faults)
+    first = time.perf_counter() - t0
+    reps = max(1, min(5, int(budget_s / max(first, 1e-3)) - 1))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        obj(y.ravel())
+    dt = (time.perf_counter() - t0) / reps
+    return {"value": 1.0 / dt, "unit": "evals/s", "cores": cores, "kind": "port",
+            "sample": f"{reps} full evaluations of the same {R.grid.dims[0]}^3/{gd.dims[0]}^3 workload "
+                      f"(oracle/ngf_oracle.py, workers={cores}, f32) after 1 warm-up; {dt:.2f} s/eval"}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    n, ratio, _ = WORKLOADS[args.workload]
+    R, T, gd, y = make_inputs(n, ratio, 0)
+    from oracle import ngf_oracle as O
+    cores = os.cpu_count() or 1
+    og = O.grid(R.grid.dims, R.grid.spacing, R.grid.origin)
+    ogd = O.grid(gd.dims, gd.spacing, gd.origin)
+    obj = O.Objective(T.values, R.values, ogd, og, workers=cores)
+    t0 = time.perf_counter()
+    obj(y.ravel())
+    one = time.perf_counter() - t0
+    budget = 150.0
+    warm = max(0, min(args.warmup - 1, int(budget / 3 / max(one, 1e-3))))
+    steps = max(1, min(args.steps, int(budget / max(one, 1e-3)) - warm))
+    for _ in range(warm):
+        obj(y.ravel())
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        obj(y.ravel())
+    dt = time.perf_counter() - t0
+    value = steps / dt
+    line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": warm + 1, "ms_per_step": 1000 * dt / steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "impl": "reference",
+            "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair, {gd.dims[0]}^3 def grid, "
+                                   "one LevelObjective evaluation per step"},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
+                             "sample": f"{steps} timed of {args.steps} requested full evaluations "
+                                       f"(bounded to ~{budget:.0f} s of CPU work), workers={cores}"},
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1812_06765_b200 as ngf
+    from paper_1812_06765_b200 import _lib
+    import ctypes
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev_index = torch.cuda.current_device()
+
+    n, ratio, levels = WORKLOADS[args.workload]
+    R, T, gd, y = make_inputs(n, ratio, seed=rank)
+    gi = R.grid
+    plan = ngf.build_gather_plan(gd, gi)
+    T_dev = torch.from_numpy(T.values).cuda()
+    R_dev = torch.from_numpy(R.values).cuda()
+    obj = ngf.LevelObjective.from_device(T_dev, R_dev, plan, ngf.NgfParams(10.0, 10.0), 1.0)
+    level = obj.level
+    x = torch.from_numpy(y.ravel().copy()).cuda()
+    g = torch.empty_like(x)
+    sc = torch.zeros(3, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(v: float) -> float:
+        if ws == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---------------- device-resident leg (value) ----------------
+    for _ in range(max(3, args.warmup)):
+        obj.eval_device(x, g, sc)
+    barrier()
+    launches0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev_index) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            obj.eval_device(x, g, sc)
+        e1.record(stream)
+        barrier()
+    launches = _lib.launch_count() - launches0
+    t_ms = max_over_ranks(e0.elapsed_time(e1))
+    value = ws * args.steps / (t_ms / 1000.0)
+
+    # ---------------- fused kernel alone, CUDA events on the launching stream --------------
+    _lib.check(_lib.lib().ngf_level_set_timing(level.handle, 1), "timing")
+    kms = []
+    for _ in range(max(5, min(args.steps, 50))):
+        obj.eval_device(x, g, sc)
+        ms = ctypes.c_float()
+        _lib.check(_lib.lib().ngf_level_kernel_ms(level.handle, ctypes.byref(ms)), "kernel_ms")
+        kms.append(ms.value)
+    _lib.check(_lib.lib().ngf_level_set_timing(level.handle, 0), "timing")
+    k_ms = float(np.mean(kms))
+    info = (ctypes.c_int64 * 9)()
+    _lib.check(_lib.lib().ngf_level_info(level.handle, info), "info")
+    N, M = gi.num_points, gd.num_points
+    bytes_kernel = 20 * N + 12 * M          # T + packed reference terms + y
+    bytes_eval = 20 * N + 24 * M            # + grad J written (B_eval)
+    peak, peak_kind = peaks()
+    achieved = bytes_kernel / (k_ms / 1000.0) / 1e9
+    eval_ms = t_ms / args.steps
+
+    # ---------------- end to end through the numpy-facing LevelObjective -------------------
+    y_host = y.ravel().copy()
+    for _ in range(2):
+        obj(y_host)
+    barrier()
+    t0 = time.perf_counter()
+    ee0 = torch.cuda.Event(enable_timing=True)
+    ee1 = torch.cuda.Event(enable_timing=True)
+    ee0.record(stream)
+    for _ in range(args.steps):
+        J, gh = obj(y_host)
+    ee1.record(stream)
+    barrier()
+    e2e_s = max_over_ranks(max(time.perf_counter() - t0, ee0.elapsed_time(ee1) / 1000.0))
+    e2e = {"value": ws * args.steps / e2e_s, "unit": "evals/s",
+           "h2d_bytes_per_step": int(y_host.nbytes), "d2h_bytes_per_step": int(gh.nbytes + 24)}
+
+    # ---------------- full coarse-to-fine registration (the paper's headline) -------------
+    reg = None
+    if not args.no_register:
+        cfg = ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision="f32")
+        ngf.register(R, T, cfg)  # warm-up (allocations, first-touch)
+        barrier()
+        t0 = time.perf_counter()
+        yr, rep = ngf.register(R, T, cfg)
+        barrier()
+        reg_s = max_over_ranks(time.perf_counter() - t0)
+        reg = {"seconds": reg_s, "levels": levels,
+               "per_level": [{"image": lv.image_dims[0], "def": lv.def_dims[0],
+                              "iterations": lv.iterations, "evals": lv.evaluations,
+                              "stop": lv.stop_reason, "optimize_s": round(lv.seconds_optimize, 4)}
+                             for lv in rep.levels],
+               "paper_gtx1080ti_s": 1.99,
+               "pairs_per_s": ws / reg_s}
+
+    cpu = None
+    if rank == 0 and ws == 1:
+        cpu = cpu_baseline(R, T, gd, y, args.cpu_budget)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": eval_ms,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair (1 mm), "
+                                   f"{gd.dims[0]}^3 def grid, NGF tau=rho=10, alpha=1; one "
+                                   "LevelObjective evaluation per step",
+                       "l2": "inputs larger than L2 (T 4N + reference terms 16N = "
+                             f"{(20 * N) / 1e6:.0f} MB > 126 MB)",
+                       "parallelism": f"replicas x{ws} (one independent pair per GPU)"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_eval_fused", "kernel_ms": k_ms,
+                         "bytes_per_launch": bytes_kernel, "peak_kind": peak_kind,
+                         "eval_frac": bytes_eval / (eval_ms / 1000.0) / 1e9 / peak,
+                         "launch": {"ctas": info[0], "smem_bytes": info[1], "z_chunk": info[2]}},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "full_registration": reg,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,85 @@
+"""Device plumbing: torch is used only for CUDA memory and streams.
+
+Every compute call goes through libngfb200.so; these helpers just move numpy
+arrays to/from CUDA tensors and hand raw pointers and the current stream to
+the C-ABI.  A missing CUDA device is an error, never a silent CPU path.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+_torch = None
+
+
+def torch():
+    global _torch
+    if _torch is None:
+        import torch as _t
+        _torch = _t
+    return _torch
+
+
+def require_cuda():
+    t = torch()
+    if not t.cuda.is_available():
+        raise RuntimeError("paper_1812_06765_b200 needs a CUDA device (B200, sm_100a); "
+                           "there is no CPU fallback")
+    return t
+
+
+def torch_dtype(dtype):
+    t = torch()
+    if isinstance(dtype, t.dtype):
+        return dtype
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return t.float32
+    if dt == np.float64:
+        return t.float64
+    raise ValueError(f"unsupported dtype {dt}")
+
+
+def np_dtype(tdtype):
+    t = torch()
+    return np.float32 if tdtype == t.float32 else np.float64
+
+
+def is_tensor(v) -> bool:
+    return type(v).__module__.startswith("torch")
+
+
+def to_device(a, dtype=None):
+    """numpy array or tensor -> contiguous CUDA tensor (dtype preserved unless given)."""
+    t = require_cuda()
+    if is_tensor(a):
+        out = a
+        if dtype is not None:
+            out = out.to(torch_dtype(dtype))
+        if not out.is_cuda:
+            out = out.cuda()
+        return out.contiguous()
+    arr = np.ascontiguousarray(a if dtype is None else np.asarray(a).astype(dtype, copy=False))
+    return t.from_numpy(arr).cuda()
+
+
+def empty(shape, dtype):
+    t = require_cuda()
+    return t.empty(tuple(shape), dtype=torch_dtype(dtype), device="cuda")
+
+
+def zeros(shape, dtype):
+    t = require_cuda()
+    return t.zeros(tuple(shape), dtype=torch_dtype(dtype), device="cuda")
+
+
+def ptr(x) -> int:
+    return int(x.data_ptr()) if x is not None else 0
+
+
+def stream() -> int:
+    return int(torch().cuda.current_stream().cuda_stream)
+
+
+def to_host(x) -> np.ndarray:
+    return x.detach().cpu().numpy()

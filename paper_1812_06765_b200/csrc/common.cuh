@@ -1,0 +1,142 @@
+// Shared definitions for libngfb200 (sm_100a).  See include/ngf_b200.h for the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+
+#include "../../include/ngf_b200.h"
+
+namespace ngf {
+
+extern std::atomic<int64_t> g_launches;
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Count every kernel launch issued by the library (bench.py reports them).
+#define NGF_LAUNCH(kernel, grid, block, smem, stream, ...)                         \
+    do {                                                                            \
+        ::ngf::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                 \
+    } while (0)
+
+#define NGF_CHECK_LAUNCH()                                                          \
+    do {                                                                            \
+        cudaError_t e_ = cudaGetLastError();                                        \
+        if (e_ != cudaSuccess) return (int)e_;                                      \
+    } while (0)
+
+#define NGF_CUDA(call)                                                              \
+    do {                                                                            \
+        cudaError_t e_ = (call);                                                    \
+        if (e_ != cudaSuccess) return (int)e_;                                      \
+    } while (0)
+
+// Number of SMs on a B200; grids of grid-stride kernels are multiples of this.
+constexpr int kSMs = 148;
+
+// Kernel-side view of a grid in the working dtype T.
+template <typename T>
+struct GridK {
+    int nx, ny, nz;
+    T hx, hy, hz;       // spacing cast to the working dtype (numpy dtype.type(h))
+    T ox, oy, oz;       // origin cast to the working dtype (NEP 50 weak python float)
+    double dhx, dhy, dhz, dox, doy, doz;  // exact f64 metadata
+    __host__ __device__ int64_t n() const { return (int64_t)nx * ny * nz; }
+};
+
+template <typename T>
+inline GridK<T> make_gridk(const ngf_grid_t& g) {
+    GridK<T> k;
+    k.nx = (int)g.dims[0];
+    k.ny = (int)g.dims[1];
+    k.nz = (int)g.dims[2];
+    k.hx = (T)g.spacing[0];
+    k.hy = (T)g.spacing[1];
+    k.hz = (T)g.spacing[2];
+    k.ox = (T)g.origin[0];
+    k.oy = (T)g.origin[1];
+    k.oz = (T)g.origin[2];
+    k.dhx = g.spacing[0];
+    k.dhy = g.spacing[1];
+    k.dhz = g.spacing[2];
+    k.dox = g.origin[0];
+    k.doy = g.origin[1];
+    k.doz = g.origin[2];
+    return k;
+}
+
+inline bool grid_ok(const ngf_grid_t* g) {
+    if (!g) return false;
+    for (int a = 0; a < 3; ++a) {
+        if (g->dims[a] < 1 || g->dims[a] > (1 << 20)) return false;
+        if (!(g->spacing[a] > 0)) return false;
+    }
+    return true;
+}
+
+inline int64_t grid_n(const ngf_grid_t& g) { return g.dims[0] * g.dims[1] * g.dims[2]; }
+
+inline unsigned blocks_for(int64_t n, int threads) {
+    int64_t b = (n + threads - 1) / threads;
+    if (b < 1) b = 1;
+    if (b > (int64_t)kSMs * 64) b = (int64_t)kSMs * 64;  // grid-stride beyond this
+    return (unsigned)b;
+}
+
+// Device-side plan for one axis: image index -> (i0, w1) and gather rows.
+struct AxisDev {
+    int ni, nd, width;
+    const int32_t* i0;     // [ni]
+    const float* w1f;      // [ni]  f32(w1)
+    const double* w1d;     // [ni]
+    const int32_t* start;  // [nd]
+    const float* wf;       // [nd*width] f32(weights)
+    const double* wd;      // [nd*width]
+};
+
+template <typename T> __device__ __forceinline__ const T* w1_of(const AxisDev& a);
+template <> __device__ __forceinline__ const float* w1_of<float>(const AxisDev& a) { return a.w1f; }
+template <> __device__ __forceinline__ const double* w1_of<double>(const AxisDev& a) { return a.w1d; }
+template <typename T> __device__ __forceinline__ const T* wts_of(const AxisDev& a);
+template <> __device__ __forceinline__ const float* wts_of<float>(const AxisDev& a) { return a.wf; }
+template <> __device__ __forceinline__ const double* wts_of<double>(const AxisDev& a) { return a.wd; }
+
+// correctly rounded single operations (no contraction), dtype-generic
+__device__ __forceinline__ float __fadd_rn_t(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double __fadd_rn_t(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float __fsub_rn_t(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double __fsub_rn_t(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float __fmul_rn_t(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double __fmul_rn_t(double a, double b) { return __dmul_rn(a, b); }
+
+template <typename T> inline const T* w1_host_sel(const AxisDev& a);
+template <> inline const float* w1_host_sel<float>(const AxisDev& a) { return a.w1f; }
+template <> inline const double* w1_host_sel<double>(const AxisDev& a) { return a.w1d; }
+
+}  // namespace ngf
+
+struct ngf_plan;
+namespace ngf {
+int plan_upload(ngf_plan* p);  // lazily create the plan's device arrays (plan.cu)
+}
+
+// Opaque handle layouts (host side).
+struct ngf_plan {
+    ngf_grid_t def_grid, img_grid;
+    int width[3];
+    int n_img[3], n_def[3];
+    // host copies
+    int32_t* h_i0[3];
+    double* h_w1[3];
+    int32_t* h_start[3];
+    int32_t* h_counts[3];
+    double* h_w[3];
+    // device blob holding all device arrays
+    void* d_blob;
+    ngf::AxisDev axes[3];
+    // workspace for P^T (x/y stage result, 3 * nz_img * ny_def * nx_def doubles)
+    void* d_tmp;
+    size_t tmp_bytes;
+};

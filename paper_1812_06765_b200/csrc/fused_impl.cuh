@@ -1,0 +1,148 @@
+// Device helpers of the fused evaluation kernel.
+#pragma once
+#include "common.cuh"
+#include "eval_fused.cuh"
+
+namespace ngf {
+
+struct __align__(16) dbl4 {
+    double x, y, z, w;
+};
+template <typename T> struct V4Sel;
+template <> struct V4Sel<float> { using type = float4; };
+template <> struct V4Sel<double> { using type = dbl4; };
+template <typename T> using V4T = typename V4Sel<T>::type;
+
+template <typename T>
+struct FusedArgs {
+    int nx, ny, nz, ndx, ndy, ndz;
+    T ox, oy, oz;     // template (= image) grid origin, working dtype
+    T hx, hy, hz;     // spacing, working dtype
+    T ihx, ihy, ihz;  // 1 / spacing (derivative scale)
+    int pow2x, pow2y, pow2z;  // spacing is a power of two: division == multiply by exact reciprocal
+    const int32_t *i0x, *i0y, *i0z;  // image -> def lower index (transfer.py:54-63)
+    const T *w1x, *w1y, *w1z;        // dtype(w1)
+    const T* Tv;                     // template values
+    const V4T<T>* RT;                // packed (gR/nR, 1/nR)
+    const T* y;                      // deformation (3, M)
+    T* partial;                      // [n_cta][3][wz][wy][wx]
+    double* dpart;                   // [n_cta]
+    T tau2, taurho, neg_hbar;
+    double half_hbar;
+    FusedPlan fp;
+};
+
+__device__ __forceinline__ float lerp_exact(float a0, float a1, float w) {
+    // a0 * (1 - w) + a1 * w, each op correctly rounded, no contraction (transfer.py:126)
+    return __fadd_rn(__fmul_rn(a0, __fsub_rn(1.0f, w)), __fmul_rn(a1, w));
+}
+__device__ __forceinline__ double lerp_exact(double a0, double a1, double w) {
+    return __dadd_rn(__dmul_rn(a0, __dsub_rn(1.0, w)), __dmul_rn(a1, w));
+}
+__device__ __forceinline__ float sub_rn(float a, float b) { return __fsub_rn(a, b); }
+__device__ __forceinline__ double sub_rn(double a, double b) { return __dsub_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
+__device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float fmaf_t(float a, float b, float c) { return fmaf(a, b, c); }
+__device__ __forceinline__ double fmaf_t(double a, double b, double c) { return fma(a, b, c); }
+__device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
+__device__ __forceinline__ double rsqrt_t(double x) { return rsqrt(x); }
+
+__device__ __forceinline__ float4 ld_rt(const float4* p) { return __ldcs(p); }
+__device__ __forceinline__ dbl4 ld_rt(const dbl4* p) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+    double2 a = __ldcs(q), b = __ldcs(q + 1);
+    dbl4 r;
+    r.x = a.x;
+    r.y = a.y;
+    r.z = b.x;
+    r.w = b.y;
+    return r;
+}
+
+// Continuous template index along one axis: (p - o) / h with the reference's rounding
+// (warp.py:38).  Bit-exact, so inside/floor decisions match the reference.
+template <typename T>
+__device__ __forceinline__ T tcoord(T p, T o, T h, T ih, int pow2) {
+    const T d = sub_rn(p, o);
+    return pow2 ? mul_rn(d, ih) : div_rn(d, h);
+}
+
+template <typename T>
+__device__ __forceinline__ void axis_cell(T t, int n, bool& inside, int& lo, T& f) {
+    inside = inside && (t >= (T)0) && (t <= (T)(n - 1));
+    const T fl = floor(t);
+    const int hi = n - 2 > 0 ? n - 2 : 0;
+    if (!(fl >= (T)0))
+        lo = 0;
+    else if (fl > (T)hi)
+        lo = hi;
+    else
+        lo = (int)fl;
+    f = t - (T)lo;  // exact for inside samples (Sterbenz); outside samples are masked
+}
+
+// W = T(yhat) and the interpolant's spatial derivative / h (zero outside the hull)
+template <typename T>
+__device__ __forceinline__ void warp_point(const FusedArgs<T>& a, const T (&yh)[3], T& W, T& d0,
+                                           T& d1, T& d2) {
+    bool inside = true;
+    int ix, iy, iz;
+    T fx, fy, fz;
+    axis_cell(tcoord(yh[0], a.ox, a.hx, a.ihx, a.pow2x), a.nx, inside, ix, fx);
+    axis_cell(tcoord(yh[1], a.oy, a.hy, a.ihy, a.pow2y), a.ny, inside, iy, fy);
+    axis_cell(tcoord(yh[2], a.oz, a.hz, a.ihz, a.pow2z), a.nz, inside, iz, fz);
+    if (!inside) {
+        W = d0 = d1 = d2 = (T)0;
+        return;
+    }
+    const int64_t sx = a.nx > 1 ? 1 : 0;
+    const int64_t sy = a.ny > 1 ? a.nx : 0;
+    const int64_t sz = a.nz > 1 ? (int64_t)a.nx * a.ny : 0;
+    const T* b = a.Tv + ((int64_t)iz * a.ny + iy) * a.nx + ix;
+    const T c000 = __ldg(b), c100 = __ldg(b + sx);
+    const T c010 = __ldg(b + sy), c110 = __ldg(b + sy + sx);
+    const T c001 = __ldg(b + sz), c101 = __ldg(b + sz + sx);
+    const T c011 = __ldg(b + sz + sy), c111 = __ldg(b + sz + sy + sx);
+    // x differences and x-lerps on the four (y, z) edges
+    const T e00 = c100 - c000, e10 = c110 - c010, e01 = c101 - c001, e11 = c111 - c011;
+    const T a00 = fmaf_t(fx, e00, c000), a10 = fmaf_t(fx, e10, c010);
+    const T a01 = fmaf_t(fx, e01, c001), a11 = fmaf_t(fx, e11, c011);
+    const T dy0 = a10 - a00, dy1 = a11 - a01;
+    const T b0 = fmaf_t(fy, dy0, a00), b1 = fmaf_t(fy, dy1, a01);
+    const T dz = b1 - b0;
+    W = fmaf_t(fz, dz, b0);
+    const T ex0 = fmaf_t(fy, e10 - e00, e00), ex1 = fmaf_t(fy, e11 - e01, e01);
+    d0 = fmaf_t(fz, ex1 - ex0, ex0) * a.ihx;
+    d1 = fmaf_t(fz, dy1 - dy0, dy0) * a.ihy;
+    d2 = dz * a.ihz;
+}
+
+// NGF ratio, the distance term and q = dD/d(grad W) (ngf.py:70-112), with the
+// reference terms packed as (gR/nR, 1/nR)
+template <typename T>
+__device__ __forceinline__ void ngf_q(const FusedArgs<T>& a, T gx, T gy, T gz, const V4T<T>& rt,
+                                      T& qx, T& qy, T& qz, double& dacc) {
+    const T dot = fmaf_t(gx, rt.x, fmaf_t(gy, rt.y, gz * rt.z));
+    const T sq = fmaf_t(gx, gx, fmaf_t(gy, gy, fmaf_t(gz, gz, a.tau2)));
+    const T inv_nt = rsqrt_t(sq);
+    const T r = fmaf_t(a.taurho, rt.w, dot) * inv_nt;
+    dacc += (double)fmaf_t(-r, r, (T)1);
+    const T cf = a.neg_hbar * r * inv_nt;
+    const T t1 = r * inv_nt;
+    qx = cf * fmaf_t(-t1, gx, rt.x);
+    qy = cf * fmaf_t(-t1, gy, rt.y);
+    qz = cf * fmaf_t(-t1, gz, rt.z);
+}
+
+template <typename T>
+int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, T* L, double* spart,
+                      int ns, int* flag, T* grad, double* scalars, cudaStream_t s,
+                      cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
+template <typename T> int fused_prepare(size_t smem);
+template <typename T> size_t fused_smem(int wx, int wy, int wz);
+template <typename T> int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s);
+
+}  // namespace ngf

@@ -1,0 +1,407 @@
+// L-BFGS vector algebra on the device (lbfgs.py:68-181).
+//
+// The Python driver keeps the reference control flow; every vector operation and
+// every reduction it branches on runs here.  Reductions are deterministic: a fixed
+// grid of kRedBlocks blocks writes per-block partials, and the last block to finish
+// sums them in block order.  Scalars the reference holds as Python floats are kept
+// as doubles; vector updates reproduce the reference's dtype rounding
+// (python float -> dtype cast, then one dtype multiply and one dtype add).
+
+#include <cooperative_groups.h>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace ngf {
+
+constexpr int kRedBlocks = kSMs;  // one block per SM: also co-resident for the cooperative kernel
+constexpr int kRedThreads = 256;
+constexpr int kNStat = 5;
+
+struct Scratch {
+    double* parts = nullptr;         // [2][kRedBlocks][kNStat]
+    unsigned int* counter = nullptr;  // last-block counter
+};
+
+static std::mutex g_scr_mu;
+static Scratch g_scr[64];
+
+static Scratch* scratch() {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(g_scr_mu);
+    Scratch& s = g_scr[dev & 63];
+    if (!s.parts) {
+        if (cudaMalloc(&s.parts, 2 * kRedBlocks * kNStat * sizeof(double)) != cudaSuccess) return nullptr;
+        if (cudaMalloc(&s.counter, 64) != cudaSuccess) return nullptr;
+        cudaMemset(s.counter, 0, 64);
+        cudaDeviceSynchronize();
+    }
+    return &s;
+}
+
+template <int K>
+__device__ __forceinline__ void block_sum(double (&v)[K], double (&red)[K][kRedThreads / 32]) {
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if ((threadIdx.x & 31) == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) red[k][threadIdx.x >> 5] = v[k];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            double s = 0.0;
+            for (int w = 0; w < kRedThreads / 32; ++w) s += red[k][w];
+            v[k] = s;
+        }
+    }
+}
+
+// stats: [0] g.d  [1] s.y  [2] s.s  [3] y.y  [4] max|g|
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_stats(const T* __restrict__ g, const T* __restrict__ d,
+                                                       const T* __restrict__ s, const T* __restrict__ y,
+                                                       int64_t n, double* parts, unsigned int* counter,
+                                                       double* out) {
+    __shared__ double red[4][kRedThreads / 32];
+    __shared__ bool last;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    double mx = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        if (g) {
+            const double gv = (double)g[i];
+            if (d) v[0] += gv * (double)d[i];
+            mx = fmax(mx, fabs(gv));
+        }
+        if (s) {
+            const double sv = (double)s[i];
+            v[2] += sv * sv;
+            if (y) v[1] += sv * (double)y[i];
+        }
+        if (y) {
+            const double yv = (double)y[i];
+            v[3] += yv * yv;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ double redm[kRedThreads / 32];
+    if ((threadIdx.x & 31) == 0) redm[threadIdx.x >> 5] = mx;
+    block_sum<4>(v, red);
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) m = fmax(m, redm[w]);
+        for (int k = 0; k < 4; ++k) parts[blockIdx.x * kNStat + k] = v[k];
+        parts[blockIdx.x * kNStat + 4] = m;
+        __threadfence();
+        const unsigned int t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double acc[kNStat] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int b = 0; b < (int)gridDim.x; ++b) {
+            for (int k = 0; k < 4; ++k) acc[k] += ((volatile double*)parts)[b * kNStat + k];
+            acc[4] = fmax(acc[4], ((volatile double*)parts)[b * kNStat + 4]);
+        }
+        for (int k = 0; k < kNStat; ++k) out[k] = acc[k];
+        *counter = 0u;
+    }
+}
+
+// x_new = x + dtype(t) * d  (lbfgs.py:122, :137)
+template <typename T>
+__global__ void k_axpy_step(const T* __restrict__ x, T t, const T* __restrict__ d, T* __restrict__ out,
+                            int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __fadd_rn_t(x[i], __fmul_rn_t(t, d[i]));
+}
+
+template <typename T>
+__global__ void k_sub(const T* __restrict__ a, const T* __restrict__ b, T* __restrict__ out, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = a[i] - b[i];
+}
+
+// s = x_new - x, y = g_new - g and their stats in one pass (lbfgs.py:145-148, :161-164)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_pair(const T* __restrict__ xn, const T* __restrict__ x,
+                                                      const T* __restrict__ gn, const T* __restrict__ g,
+                                                      T* __restrict__ s_out, T* __restrict__ y_out,
+                                                      int64_t n, double* parts, unsigned int* counter,
+                                                      double* out) {
+    __shared__ double red[4][kRedThreads / 32];
+    __shared__ double redm[kRedThreads / 32];
+    __shared__ bool last;
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    double mx = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const T sv = xn[i] - x[i];
+        const T gv = gn[i];
+        const T yv = gv - g[i];
+        s_out[i] = sv;
+        y_out[i] = yv;
+        v[0] += (double)sv * (double)yv;
+        v[1] += (double)sv * (double)sv;
+        v[2] += (double)yv * (double)yv;
+        mx = fmax(mx, fabs((double)gv));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    if ((threadIdx.x & 31) == 0) redm[threadIdx.x >> 5] = mx;
+    block_sum<4>(v, red);
+    if (threadIdx.x == 0) {
+        double m = 0.0;
+        for (int w = 0; w < kRedThreads / 32; ++w) m = fmax(m, redm[w]);
+        for (int k = 0; k < 3; ++k) parts[blockIdx.x * kNStat + k] = v[k];
+        parts[blockIdx.x * kNStat + 3] = m;
+        __threadfence();
+        const unsigned int t = atomicAdd(counter, 1u);
+        last = (t == gridDim.x - 1);
+    }
+    __syncthreads();
+    if (last && threadIdx.x == 0) {
+        __threadfence();
+        double acc[4] = {0.0, 0.0, 0.0, 0.0};
+        for (int b = 0; b < (int)gridDim.x; ++b) {
+            for (int k = 0; k < 3; ++k) acc[k] += ((volatile double*)parts)[b * kNStat + k];
+            acc[3] = fmax(acc[3], ((volatile double*)parts)[b * kNStat + 3]);
+        }
+        for (int k = 0; k < 4; ++k) out[k] = acc[k];
+        *counter = 0u;
+    }
+}
+
+constexpr int kMaxMem = 32;
+
+template <typename T>
+struct TwoLoopArgs {
+    const T* S[kMaxMem];
+    const T* Y[kMaxMem];
+    double rho[kMaxMem];
+    double gamma;
+    int m;
+    const T* g;
+    T* d;  // holds q during the recursion, -q at the end
+    int64_t n;
+    double* parts;  // [2][kRedBlocks]
+    double* slope;
+};
+
+// grid-wide deterministic sum of one value per thread: block partial -> parts[buf][b],
+// grid sync, every block sums the partials in block order (identical result everywhere)
+__device__ __forceinline__ double grid_dot(cg::grid_group& grid, double v, double* parts, int buf,
+                                           double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double s = 0.0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
+        parts[buf * kRedBlocks + blockIdx.x] = s;
+    }
+    grid.sync();
+    double tot = 0.0;
+    for (int b = 0; b < (int)gridDim.x; ++b) tot += ((volatile double*)parts)[buf * kRedBlocks + b];
+    __syncthreads();  // red reused by the next call
+    return tot;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_two_loop(const TwoLoopArgs<T> a) {
+    cg::grid_group grid = cg::this_grid();
+    __shared__ double red[kRedThreads / 32];
+    const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t st = (int64_t)gridDim.x * blockDim.x;
+    int buf = 0;
+    double alpha[kMaxMem];
+    // q = g; partial of s_{m-1} . q
+    double v = 0.0;
+    for (int64_t i = i0; i < a.n; i += st) {
+        const T q = a.g[i];
+        a.d[i] = q;
+        if (a.m > 0) v += (double)a.S[a.m - 1][i] * (double)q;
+    }
+    // first loop, newest pair first: alpha = rho * (s . q); q -= dtype(alpha) * y
+    for (int k = a.m - 1; k >= 0; --k) {
+        const double dot = grid_dot(grid, v, a.parts, buf, red);
+        buf ^= 1;
+        alpha[k] = a.rho[k] * dot;
+        const T al = (T)alpha[k];
+        v = 0.0;
+        const bool last = (k == 0);
+        const T tg = (T)a.gamma;
+        for (int64_t i = i0; i < a.n; i += st) {
+            T q = __fsub_rn_t(a.d[i], __fmul_rn_t(al, a.Y[k][i]));
+            if (last) {
+                q = __fmul_rn_t(q, tg);  // q *= dtype(gamma)
+                v += (double)a.Y[0][i] * (double)q;
+            } else {
+                v += (double)a.S[k - 1][i] * (double)q;
+            }
+            a.d[i] = q;
+        }
+    }
+    // second loop, oldest pair first: beta = rho * (y . q); q += dtype(alpha - beta) * s
+    for (int k = 0; k < a.m; ++k) {
+        const double dot = grid_dot(grid, v, a.parts, buf, red);
+        buf ^= 1;
+        const double beta = a.rho[k] * dot;
+        const T c = (T)(alpha[k] - beta);
+        v = 0.0;
+        const bool last = (k == a.m - 1);
+        for (int64_t i = i0; i < a.n; i += st) {
+            T q = __fadd_rn_t(a.d[i], __fmul_rn_t(c, a.S[k][i]));
+            if (last) {
+                q = -q;
+                v += (double)a.g[i] * (double)q;
+            } else {
+                v += (double)a.Y[k + 1][i] * (double)q;
+            }
+            a.d[i] = q;
+        }
+    }
+    if (a.m == 0) {
+        // d = -g
+        v = 0.0;
+        for (int64_t i = i0; i < a.n; i += st) {
+            const T q = -a.g[i];
+            a.d[i] = q;
+            v += (double)a.g[i] * (double)q;
+        }
+    }
+    const double slope = grid_dot(grid, v, a.parts, buf, red);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.slope = slope;
+}
+
+template <typename T>
+int two_loop_impl(const void* const* S, const void* const* Y, const double* rho, double gamma, int m,
+                  const void* g, void* d, int64_t n, double* slope, cudaStream_t s) {
+    if (m < 0 || m > kMaxMem) return NGF_EARG;
+    Scratch* sc = scratch();
+    if (!sc) return NGF_ENOMEM;
+    TwoLoopArgs<T> a;
+    for (int k = 0; k < m; ++k) {
+        a.S[k] = (const T*)S[k];
+        a.Y[k] = (const T*)Y[k];
+        a.rho[k] = rho[k];
+    }
+    a.gamma = gamma;
+    a.m = m;
+    a.g = (const T*)g;
+    a.d = (T*)d;
+    a.n = n;
+    a.parts = sc->parts;
+    a.slope = slope;
+    void* args[] = {&a};
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    NGF_CUDA(cudaLaunchCooperativeKernel((const void*)k_two_loop<T>, dim3(kRedBlocks), dim3(kRedThreads),
+                                         args, 0, s));
+    return 0;
+}
+
+}  // namespace ngf
+
+using namespace ngf;
+
+extern "C" {
+
+int ngf_vec_dot(int dtype, const void* a, const void* b, int64_t n, double* out_dev, void* stream) {
+    // out_dev[0..4] receives the stats layout; [0] = a . b
+    return ngf_vec_stats(dtype, a, b, nullptr, nullptr, n, out_dev, stream);
+}
+
+int ngf_vec_stats(int dtype, const void* g, const void* d, const void* s, const void* y, int64_t n,
+                  double* out_dev, void* stream) {
+    if (!out_dev || n < 0) return NGF_EARG;
+    Scratch* sc = scratch();
+    if (!sc) return NGF_ENOMEM;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == NGF_F32)
+        NGF_LAUNCH(k_stats<float>, kRedBlocks, kRedThreads, 0, st, (const float*)g, (const float*)d,
+                   (const float*)s, (const float*)y, n, sc->parts, sc->counter, out_dev);
+    else if (dtype == NGF_F64)
+        NGF_LAUNCH(k_stats<double>, kRedBlocks, kRedThreads, 0, st, (const double*)g, (const double*)d,
+                   (const double*)s, (const double*)y, n, sc->parts, sc->counter, out_dev);
+    else
+        return NGF_EARG;
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+int ngf_vec_axpy_step(int dtype, const void* x, double t, const void* d, void* out, int64_t n,
+                      void* stream) {
+    if (!x || !d || !out || n < 0) return NGF_EARG;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == NGF_F32)
+        NGF_LAUNCH(k_axpy_step<float>, blocks_for(n, 256), 256, 0, st, (const float*)x, (float)t,
+                   (const float*)d, (float*)out, n);
+    else if (dtype == NGF_F64)
+        NGF_LAUNCH(k_axpy_step<double>, blocks_for(n, 256), 256, 0, st, (const double*)x, t,
+                   (const double*)d, (double*)out, n);
+    else
+        return NGF_EARG;
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+int ngf_vec_sub(int dtype, const void* a, const void* b, void* out, int64_t n, void* stream) {
+    if (!a || !b || !out || n < 0) return NGF_EARG;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == NGF_F32)
+        NGF_LAUNCH(k_sub<float>, blocks_for(n, 256), 256, 0, st, (const float*)a, (const float*)b,
+                   (float*)out, n);
+    else if (dtype == NGF_F64)
+        NGF_LAUNCH(k_sub<double>, blocks_for(n, 256), 256, 0, st, (const double*)a, (const double*)b,
+                   (double*)out, n);
+    else
+        return NGF_EARG;
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+int ngf_lbfgs_pair(int dtype, const void* x_new, const void* x, const void* g_new, const void* g,
+                   void* s_out, void* y_out, int64_t n, double* out_dev, void* stream) {
+    if (!x_new || !x || !g_new || !g || !s_out || !y_out || !out_dev || n < 0) return NGF_EARG;
+    Scratch* sc = scratch();
+    if (!sc) return NGF_ENOMEM;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == NGF_F32)
+        NGF_LAUNCH(k_pair<float>, kRedBlocks, kRedThreads, 0, st, (const float*)x_new, (const float*)x,
+                   (const float*)g_new, (const float*)g, (float*)s_out, (float*)y_out, n, sc->parts,
+                   sc->counter, out_dev);
+    else if (dtype == NGF_F64)
+        NGF_LAUNCH(k_pair<double>, kRedBlocks, kRedThreads, 0, st, (const double*)x_new,
+                   (const double*)x, (const double*)g_new, (const double*)g, (double*)s_out,
+                   (double*)y_out, n, sc->parts, sc->counter, out_dev);
+    else
+        return NGF_EARG;
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+int ngf_lbfgs_two_loop(int dtype, const void* const* S, const void* const* Y, const double* host_rho,
+                       double gamma, int m, const void* g, void* d, int64_t n, double* slope_dev,
+                       void* stream) {
+    if (!g || !d || !slope_dev || n < 0 || m < 0 || (m > 0 && (!S || !Y || !host_rho)))
+        return NGF_EARG;
+    cudaStream_t st = as_stream(stream);
+    if (dtype == NGF_F32) return two_loop_impl<float>(S, Y, host_rho, gamma, m, g, d, n, slope_dev, st);
+    if (dtype == NGF_F64) return two_loop_impl<double>(S, Y, host_rho, gamma, m, g, d, n, slope_dev, st);
+    return NGF_EARG;
+}
+
+}  // extern "C"

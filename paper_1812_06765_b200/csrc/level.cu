@@ -1,0 +1,410 @@
+// Level objective: reference terms, fused/exact evaluation (objective.py:22-60).
+
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "eval_fused.cuh"
+#include "fused_impl.cuh"
+#include "ops_exact.cuh"
+
+namespace ngf {
+
+constexpr int kCurvBlocks = 2 * kSMs;  // fixed grid of the curvature reduction (determinism)
+
+struct LevelWork {
+    void* yhat = nullptr;   // 3N
+    void* W = nullptr;      // N
+    void* terms = nullptr;  // N
+    void* q = nullptr;      // 3N
+    void* s = nullptr;      // N
+    void* ghat = nullptr;   // 3N
+    void* gD = nullptr;     // 3M
+    void* cws = nullptr;    // 6M
+    double* dws = nullptr;  // 8
+};
+
+}  // namespace ngf
+
+struct ngf_level {
+    int dtype;
+    ngf_grid_t img, def;
+    ngf_plan_t* plan;
+    const void* T;
+    void* gR;   // 3N exact reference terms
+    void* nR;   // N
+    void* RT;   // packed N x 4
+    double tau, rho, alpha;
+    // fused plan
+    ngf::FusedPlan fp;
+    void* fp_blob;   // device: windows + covers
+    void* partial;   // n_cta x 3 x wz x wy x wx
+    double* dpart;   // n_cta
+    double* spart;   // kCurvBlocks
+    void* L;         // 3M
+    int* flag;       // non-finite y seen in this evaluation
+    int timing;      // record events around the fused kernel
+    cudaEvent_t ev[2];
+    ngf::LevelWork ex;
+};
+
+namespace ngf {
+
+static bool is_pow2(double h) {
+    int e;
+    double m = std::frexp(h, &e);
+    return m == 0.5;
+}
+
+static int tile_windows(const int32_t* i0, int n, int nd, int tile, int ring_lo, std::vector<int>& lo,
+                        std::vector<int>& hi) {
+    const int nt = (n + tile - 1) / tile;
+    lo.resize(nt);
+    hi.resize(nt);
+    int wmax = 1;
+    for (int t = 0; t < nt; ++t) {
+        int a = t * tile - ring_lo;
+        if (a < 0) a = 0;
+        int b = t * tile + tile;  // ring voxel after the tile
+        if (b > n - 1) b = n - 1;
+        int l = i0[a];
+        int h = nd > 1 ? i0[b] + 1 : 0;
+        if (h > nd - 1) h = nd - 1;
+        lo[t] = l;
+        hi[t] = h;
+        if (h - l + 1 > wmax) wmax = h - l + 1;
+    }
+    return wmax;
+}
+
+static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, int nd,
+                        std::vector<int32_t>& cov) {
+    cov.assign((size_t)nd * kCover * 2, -1);
+    for (int d = 0; d < nd; ++d) {
+        int k = 0;
+        for (int t = 0; t < (int)lo.size(); ++t) {
+            if (d >= lo[t] && d <= hi[t]) {
+                if (k >= kCover) return false;
+                cov[((size_t)d * kCover + k) * 2] = t;
+                cov[((size_t)d * kCover + k) * 2 + 1] = d - lo[t];
+                ++k;
+            }
+        }
+    }
+    return true;
+}
+
+template <typename T>
+static int fused_setup(ngf_level* L) {
+    const ngf_plan_t* p = L->plan;
+    const int nx = (int)L->img.dims[0], ny = (int)L->img.dims[1], nz = (int)L->img.dims[2];
+    const int ndx = (int)L->def.dims[0], ndy = (int)L->def.dims[1], ndz = (int)L->def.dims[2];
+    std::vector<int> xl, xh, yl, yh, zl, zh;
+    FusedPlan& fp = L->fp;
+    fp.wx = tile_windows(p->h_i0[0], nx, ndx, kTX, 1, xl, xh);
+    fp.wy = tile_windows(p->h_i0[1], ny, ndy, kTY, 1, yl, yh);
+    fp.ntx = (int)xl.size();
+    fp.nty = (int)yl.size();
+    // z chunk: as long as possible (less z-ring recompute) while keeping >= 2 CTAs per SM
+    // busy and the window accumulator within shared memory
+    int cz = 64;
+    auto fits = [&](int c) {
+        std::vector<int> a, b;
+        int wz = tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b);
+        return fused_smem<T>(fp.wx, fp.wy, wz) <= 100 * 1024;
+    };
+    while (cz > 4 && ((int64_t)fp.ntx * fp.nty * ((nz + cz - 1) / cz) < 2 * kSMs || !fits(cz)))
+        cz /= 2;
+    if (cz < 4) cz = 4;
+    while (cz > 1 && !fits(cz)) cz /= 2;
+    if (!fits(cz)) return NGF_EARG;
+    fp.cz = cz;
+    fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh);
+    fp.ntz = (int)zl.size();
+    fp.n_cta = fp.ntx * fp.nty * fp.ntz;
+    fp.smem_bytes = fused_smem<T>(fp.wx, fp.wy, fp.wz);
+    std::vector<int32_t> cx, cy, cz_;
+    if (!build_cover(xl, xh, ndx, cx) || !build_cover(yl, yh, ndy, cy) ||
+        !build_cover(zl, zh, ndz, cz_))
+        return NGF_EARG;
+    std::vector<int32_t> blob;
+    auto app = [&](const std::vector<int32_t>& v) {
+        size_t off = blob.size();
+        blob.insert(blob.end(), v.begin(), v.end());
+        while (blob.size() % 64) blob.push_back(0);
+        return off;
+    };
+    std::vector<int32_t> wxv(xl.begin(), xl.end()), wyv(yl.begin(), yl.end()), wzv(zl.begin(), zl.end());
+    size_t o_wx = app(wxv), o_wy = app(wyv), o_wz = app(wzv), o_cx = app(cx), o_cy = app(cy),
+           o_cz = app(cz_);
+    NGF_CUDA(cudaMalloc(&L->fp_blob, blob.size() * 4));
+    NGF_CUDA(cudaMemcpy(L->fp_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice));
+    const int32_t* b = (const int32_t*)L->fp_blob;
+    fp.win_x = b + o_wx;
+    fp.win_y = b + o_wy;
+    fp.win_z = b + o_wz;
+    fp.cov_x = b + o_cx;
+    fp.cov_y = b + o_cy;
+    fp.cov_z = b + o_cz;
+    const size_t win = (size_t)fp.wz * fp.wy * fp.wx;
+    NGF_CUDA(cudaMalloc(&L->partial, (size_t)fp.n_cta * 3 * win * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&L->dpart, (size_t)fp.n_cta * sizeof(double)));
+    NGF_CUDA(cudaMalloc(&L->spart, (size_t)kCurvBlocks * sizeof(double)));
+    NGF_CUDA(cudaMalloc(&L->L, (size_t)3 * grid_n(L->def) * sizeof(T)));
+    return fused_prepare<T>(fp.smem_bytes);
+}
+
+template <typename T>
+static FusedArgs<T> fused_args(const ngf_level* L, const void* y) {
+    FusedArgs<T> a;
+    std::memset(&a, 0, sizeof(a));
+    a.nx = (int)L->img.dims[0];
+    a.ny = (int)L->img.dims[1];
+    a.nz = (int)L->img.dims[2];
+    a.ndx = (int)L->def.dims[0];
+    a.ndy = (int)L->def.dims[1];
+    a.ndz = (int)L->def.dims[2];
+    a.ox = (T)L->img.origin[0];
+    a.oy = (T)L->img.origin[1];
+    a.oz = (T)L->img.origin[2];
+    a.hx = (T)L->img.spacing[0];
+    a.hy = (T)L->img.spacing[1];
+    a.hz = (T)L->img.spacing[2];
+    a.ihx = (T)1 / a.hx;
+    a.ihy = (T)1 / a.hy;
+    a.ihz = (T)1 / a.hz;
+    a.pow2x = is_pow2((double)a.hx);
+    a.pow2y = is_pow2((double)a.hy);
+    a.pow2z = is_pow2((double)a.hz);
+    const ngf_plan_t* p = L->plan;
+    a.i0x = p->axes[0].i0;
+    a.i0y = p->axes[1].i0;
+    a.i0z = p->axes[2].i0;
+    a.w1x = w1_host_sel<T>(p->axes[0]);
+    a.w1y = w1_host_sel<T>(p->axes[1]);
+    a.w1z = w1_host_sel<T>(p->axes[2]);
+    a.Tv = (const T*)L->T;
+    a.RT = (const V4T<T>*)L->RT;
+    a.y = (const T*)y;
+    a.partial = (T*)L->partial;
+    a.dpart = L->dpart;
+    const T tau = (T)L->tau;
+    a.tau2 = tau * tau;
+    a.taurho = (T)(L->tau * L->rho);
+    const double hbar = L->img.spacing[0] * L->img.spacing[1] * L->img.spacing[2];
+    a.neg_hbar = (T)(-hbar);
+    a.half_hbar = hbar / 2;
+    a.fp = L->fp;
+    return a;
+}
+
+template <typename T>
+static int exact_alloc(ngf_level* L) {
+    LevelWork& w = L->ex;
+    if (w.yhat) return 0;
+    const int64_t n = grid_n(L->img), m = grid_n(L->def);
+    NGF_CUDA(cudaMalloc(&w.yhat, 3 * n * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.W, n * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.terms, n * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.q, 3 * n * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.s, n * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.ghat, 3 * n * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.gD, 3 * m * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.cws, 6 * m * sizeof(T)));
+    NGF_CUDA(cudaMalloc(&w.dws, 8 * sizeof(double)));
+    return 0;
+}
+
+template <typename T>
+__global__ void k_nonfinite(const T* __restrict__ y, int64_t n, int* flag) {
+    bool bad = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= !isfinite(y[i]);
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+__global__ void k_finish_exact(const double* D, const double* S, double alpha, int* flag, double* out) {
+    // J = D + alpha * S in python floats (objective.py:50-52); a non-finite trial point
+    // gives J = inf to force a backtrack (objective.py:55-57)
+    out[0] = *flag ? INFINITY : *D + alpha * *S;
+    *flag = 0;
+    out[1] = *D;
+    out[2] = *S;
+}
+
+template <typename T>
+static int eval_exact(ngf_level* L, const void* y, void* grad, double* scal, cudaStream_t s) {
+    int rc = exact_alloc<T>(L);
+    if (rc) return rc;
+    LevelWork& w = L->ex;
+    const int64_t n = grid_n(L->img);
+    const double hbar = L->img.spacing[0] * L->img.spacing[1] * L->img.spacing[2];
+    if ((rc = apply_P_impl<T>(L->plan, (const T*)y, (T*)w.yhat, s))) return rc;
+    if ((rc = warp_impl<T>(&L->img, (const T*)L->T, (const T*)w.yhat, n, (T*)w.W, nullptr, s)))
+        return rc;
+    if ((rc = ngf_terms_impl<T>(&L->img, (const T*)w.W, (const T*)L->gR, (const T*)L->nR, L->tau,
+                                L->rho, (T*)w.terms, (T*)w.q, s)))
+        return rc;
+    if ((rc = pairwise_sum_impl<T>((const T*)w.terms, n, w.dws + 4, 1, hbar / 2, s))) return rc;
+    if ((rc = gradient_t_impl<T>(&L->img, (const T*)w.q, (T*)w.s, s))) return rc;
+    if ((rc = warp_jt_impl<T>(&L->img, (const T*)L->T, (const T*)w.yhat, (const T*)w.s, n,
+                              (T*)w.ghat, s)))
+        return rc;
+    if ((rc = apply_Pt_impl<T>(L->plan, (const T*)w.ghat, (T*)w.gD, s))) return rc;
+    if ((rc = curvature_impl<T>(&L->def, (const T*)y, w.dws + 5, (T*)grad, (const T*)w.gD, L->alpha,
+                                (T*)w.cws, w.dws, s)))
+        return rc;
+    NGF_LAUNCH(k_nonfinite<T>, blocks_for(3 * grid_n(L->def), 256), 256, 0, s, (const T*)y,
+               3 * grid_n(L->def), L->flag);
+    NGF_LAUNCH(k_finish_exact, 1, 1, 0, s, w.dws + 4, w.dws + 5, L->alpha, L->flag, scal);
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+}  // namespace ngf
+
+using namespace ngf;
+
+extern "C" {
+
+static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
+                             const void* T, const void* R, const void* gR, const void* nR,
+                             double tau, double rho, double alpha, void* stream, ngf_level_t** out) {
+    if (!out || !T || (!R && (!gR || !nR)) || (dtype != NGF_F32 && dtype != NGF_F64)) return NGF_EARG;
+    if (!grid_ok(img_grid) || !grid_ok(def_grid)) return NGF_EARG;
+    if (!(tau > 0) || !(rho > 0)) return NGF_EARG;
+    *out = nullptr;
+    ngf_level* L = (ngf_level*)std::calloc(1, sizeof(ngf_level));
+    if (!L) return NGF_ENOMEM;
+    L->dtype = dtype;
+    L->img = *img_grid;
+    L->def = *def_grid;
+    L->T = T;
+    L->tau = tau;
+    L->rho = rho;
+    L->alpha = alpha;
+    int rc = ngf_plan_create(def_grid, img_grid, &L->plan);
+    if (!rc) {
+        rc = plan_upload(L->plan);
+        if (rc) ngf_plan_destroy(L->plan);
+    }
+    if (rc) {
+        std::free(L);
+        return rc;
+    }
+    cudaStream_t s = as_stream(stream);
+    const int64_t n = grid_n(L->img);
+    const size_t es = dtype == NGF_F32 ? 4 : 8;
+    if (cudaMalloc(&L->gR, 3 * n * es) || cudaMalloc(&L->nR, n * es) ||
+        cudaMalloc(&L->RT, n * 4 * es) || cudaMalloc(&L->flag, 16)) {
+        ngf_level_destroy(L);
+        return NGF_ENOMEM;
+    }
+    cudaMemsetAsync(L->flag, 0, 16, s);
+    if (R) {
+        rc = dtype == NGF_F32
+                 ? ref_terms_impl<float>(&L->img, (const float*)R, rho, (float*)L->gR, (float*)L->nR, s)
+                 : ref_terms_impl<double>(&L->img, (const double*)R, rho, (double*)L->gR,
+                                          (double*)L->nR, s);
+    } else {
+        rc = (int)cudaMemcpyAsync(L->gR, gR, 3 * n * es, cudaMemcpyDeviceToDevice, s);
+        if (!rc) rc = (int)cudaMemcpyAsync(L->nR, nR, n * es, cudaMemcpyDeviceToDevice, s);
+    }
+    if (!rc) {
+        if (dtype == NGF_F32) {
+            rc = pack_rt<float>((const float*)L->gR, (const float*)L->nR, n, L->RT, s);
+            if (!rc) rc = fused_setup<float>(L);
+        } else {
+            rc = pack_rt<double>((const double*)L->gR, (const double*)L->nR, n, L->RT, s);
+            if (!rc) rc = fused_setup<double>(L);
+        }
+    }
+    if (rc) {
+        ngf_level_destroy(L);
+        return rc;
+    }
+    *out = L;
+    return NGF_OK;
+}
+
+int ngf_level_create(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
+                     const void* T, const void* R, double tau, double rho, double alpha,
+                     void* stream, ngf_level_t** out) {
+    if (!R) return NGF_EARG;
+    return level_create_impl(img_grid, def_grid, dtype, T, R, nullptr, nullptr, tau, rho, alpha,
+                             stream, out);
+}
+
+int ngf_level_create_terms(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
+                           const void* T, const void* gR, const void* nR, double tau, double rho,
+                           double alpha, void* stream, ngf_level_t** out) {
+    return level_create_impl(img_grid, def_grid, dtype, T, nullptr, gR, nR, tau, rho, alpha,
+                             stream, out);
+}
+
+void ngf_level_destroy(ngf_level_t* L) {
+    if (!L) return;
+    if (L->plan) ngf_plan_destroy(L->plan);
+    void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart, L->L,
+                    L->ex.yhat, L->ex.W, L->ex.terms, L->ex.q, L->ex.s, L->ex.ghat, L->ex.gD,
+                    L->ex.cws, L->ex.dws};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    for (int k = 0; k < 2; ++k)
+        if (L->ev[k]) cudaEventDestroy(L->ev[k]);
+    std::free(L);
+}
+
+int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_dev, int mode,
+                   void* stream) {
+    if (!L || !y || !grad || !scalars_dev) return NGF_EARG;
+    cudaStream_t s = as_stream(stream);
+    if (mode == 1) {
+        return L->dtype == NGF_F32 ? eval_exact<float>(L, y, grad, scalars_dev, s)
+                                   : eval_exact<double>(L, y, grad, scalars_dev, s);
+    }
+    if (mode != 0) return NGF_EARG;
+    cudaEvent_t e0 = L->timing ? L->ev[0] : nullptr, e1 = L->timing ? L->ev[1] : nullptr;
+    if (L->dtype == NGF_F32) {
+        FusedArgs<float> a = fused_args<float>(L, y);
+        return fused_eval_launch<float>(a, L->def, L->alpha, (float*)L->L, L->spart, kCurvBlocks,
+                                        L->flag, (float*)grad, scalars_dev, s, e0, e1);
+    }
+    FusedArgs<double> a = fused_args<double>(L, y);
+    return fused_eval_launch<double>(a, L->def, L->alpha, (double*)L->L, L->spart, kCurvBlocks,
+                                     L->flag, (double*)grad, scalars_dev, s, e0, e1);
+}
+
+int ngf_level_set_timing(ngf_level_t* L, int on) {
+    if (!L) return NGF_EARG;
+    if (on && !L->ev[0]) {
+        NGF_CUDA(cudaEventCreate(&L->ev[0]));
+        NGF_CUDA(cudaEventCreate(&L->ev[1]));
+    }
+    L->timing = on ? 1 : 0;
+    return 0;
+}
+
+int ngf_level_kernel_ms(ngf_level_t* L, float* ms) {
+    if (!L || !ms || !L->ev[0]) return NGF_ESTATE;
+    NGF_CUDA(cudaEventSynchronize(L->ev[1]));
+    NGF_CUDA(cudaEventElapsedTime(ms, L->ev[0], L->ev[1]));
+    return 0;
+}
+
+int ngf_level_info(const ngf_level_t* L, int64_t* info) {
+    // [0] CTAs of the fused kernel, [1] smem bytes, [2] z chunk, [3..5] window wx, wy, wz,
+    // [6..8] tiles ntx, nty, ntz
+    if (!L || !info) return NGF_EARG;
+    const FusedPlan& fp = L->fp;
+    int64_t v[9] = {fp.n_cta, (int64_t)fp.smem_bytes, fp.cz, fp.wx, fp.wy, fp.wz, fp.ntx, fp.nty, fp.ntz};
+    for (int k = 0; k < 9; ++k) info[k] = v[k];
+    return 0;
+}
+
+const void* ngf_level_ref_terms(const ngf_level_t* L) { return L ? L->RT : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,113 @@
+"""Full multilevel registration on the device vs the reference (multilevel.py:179-247).
+
+Parity protocol: report max-abs displacement difference over
+all deformation nodes and over the interior (>= 2 def cells from every face),
+plus per-level iteration counts; the bar is 0.05 voxel on the interior.  The
+exact pipeline must also reproduce the reference's accepted iterates."""
+
+import numpy as np
+import pytest
+
+from conftest import load_golden
+
+pytestmark = pytest.mark.gpu
+
+import paper_1812_06765_b200 as ngf  # noqa: E402
+from oracle import ngf_oracle as O  # noqa: E402
+
+BAR_VOXEL = 0.05
+
+
+def _g(arr):
+    a = np.asarray(arr, dtype=np.float64)
+    return ngf.Grid3(tuple(int(v) for v in a[:3]), tuple(a[3:6]), tuple(a[6:9]))
+
+
+def _field_stats(y, y_ref, gd, voxel):
+    d = np.sqrt(np.sum((y.astype(np.float64) - y_ref.astype(np.float64)) ** 2, axis=0)) / voxel
+    inner = d[2:-2, 2:-2, 2:-2] if min(gd.shape) > 4 else d
+    return float(d.max()), float(inner.max()), float(d.mean())
+
+
+@pytest.mark.parametrize("p", ["f32", "f64"])
+def test_register_matches_reference_fixture(p):
+    z = load_golden("register")
+    g = _g(z["g"])
+    cfg = ngf.MultilevelConfig(coarsest_min_dim=8, precision=p,
+                               lbfgs=ngf.LbfgsConfig(max_iterations=30))
+    R, T = ngf.Image3(g, z["R"]), ngf.Image3(g, z["T"])
+    y, rep = ngf.register(R, T, cfg)
+    gd = _g(z[f"gd_{p}"])
+    assert y.grid == gd and y.field.dtype == np.dtype(p.replace("f", "float"))
+    mx, inner, mean = _field_stats(y.field, z[f"y_{p}"], gd, g.spacing[0])
+    iters = [lv.iterations for lv in rep.levels]
+    print(f"{p}: iterations {iters} vs ref {list(z[f'iters_{p}'])}; max {mx:.4f} "
+          f"interior {inner:.4f} mean {mean:.5f} voxel")
+    assert inner <= BAR_VOXEL
+    # exact pipeline: identical decisions -> identical iteration counts
+    y2, rep2 = ngf.register(R, T, ngf.MultilevelConfig(coarsest_min_dim=8, precision=p, exact=True,
+                                                        lbfgs=ngf.LbfgsConfig(max_iterations=30)))
+    assert [lv.iterations for lv in rep2.levels] == list(z[f"iters_{p}"])
+    assert _field_stats(y2.field, z[f"y_{p}"], gd, g.spacing[0])[1] <= BAR_VOXEL
+
+
+def test_register_c1_vs_oracle():
+    """Config 1: 64^3 Gaussian-bump pair, single level, f32."""
+    g = ngf.Grid3((64, 64, 64), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    center = tuple(o + e / 2 for o, e in zip(g.origin, g.extent))
+    mapping = ngf.gaussian_bump_mapping(center, 18.0, (3.0, -2.0, 1.5))
+    R, T = ngf.make_registration_pair(g, mapping)
+    y, rep = ngf.register(R, T, ngf.MultilevelConfig(num_levels=1, precision="f32"))
+    y_ref, gd, info = O.register(R.values, T.values, O.grid(g.dims), num_levels=1, precision="f32",
+                                 workers=8)
+    mx, inner, mean = _field_stats(y.field, y_ref, y.grid, 1.0)
+    print(f"C1: iterations {rep.levels[0].iterations} vs oracle {info[0]['iterations']}; "
+          f"max {mx:.4f} interior {inner:.4f} mean {mean:.5f} voxel")
+    assert inner <= BAR_VOXEL
+    # recovery against the known mapping (tests/test_acceptance.py:303-316)
+    pts = ngf.probe_lattice(g, n_per_axis=5, margin=0.25)
+    truth = np.stack(mapping(pts[:, 0], pts[:, 1], pts[:, 2]), axis=1)
+    from paper_1812_06765_b200.geometry import DeformationField
+    mapped = O_sample(y.field.astype(np.float64), y.grid, pts)
+    err = np.linalg.norm(mapped - truth, axis=1).mean()
+    assert err < 0.5
+
+
+def O_sample(field, grid, pts):
+    """Trilinear clamp-to-edge evaluation of a deformation at world points
+    (evaluation.py:39-65 of the reference; host-side scoring only)."""
+    out = np.zeros((len(pts), 3))
+    idx, fr = [], []
+    for a in range(3):
+        t = (pts[:, a] - grid.origin[a]) / grid.spacing[a]
+        n = grid.dims[a]
+        i0 = np.clip(np.floor(t).astype(int), 0, max(n - 2, 0))
+        idx.append(i0)
+        fr.append(np.clip(t - i0, 0, 1) if n > 1 else np.zeros(len(pts)))
+    for dz in (0, 1):
+        for dy in (0, 1):
+            for dx in (0, 1):
+                w = ((fr[0] if dx else 1 - fr[0]) * (fr[1] if dy else 1 - fr[1])
+                     * (fr[2] if dz else 1 - fr[2]))
+                ix = np.minimum(idx[0] + dx, grid.dims[0] - 1)
+                iy = np.minimum(idx[1] + dy, grid.dims[1] - 1)
+                iz = np.minimum(idx[2] + dz, grid.dims[2] - 1)
+                out += w[:, None] * field[:, iz, iy, ix].T
+    return out
+
+
+def test_register_identical_images_stays_near_identity():
+    g = ngf.Grid3((16, 16, 16), (2.0, 2.0, 2.0), (0.0, 0.0, 0.0))
+    T = ngf.smooth_random_volume(g, seed=8)
+    y, _ = ngf.register(T, T, ngf.MultilevelConfig(coarsest_min_dim=8,
+                                                   lbfgs=ngf.LbfgsConfig(max_iterations=10)))
+    pts = ngf.probe_lattice(g, n_per_axis=5, margin=0.25)
+    drift = np.linalg.norm(O_sample(y.field, y.grid, pts) - pts, axis=1)
+    assert drift.mean() < 1.0 and drift.max() < 2.0
+
+
+def test_register_rejects_mismatched_grids():
+    R = ngf.smooth_random_volume(ngf.Grid3((8, 8, 8), (1, 1, 1), (0, 0, 0)), seed=1)
+    T = ngf.smooth_random_volume(ngf.Grid3((9, 8, 8), (1, 1, 1), (0, 0, 0)), seed=2)
+    with pytest.raises(ngf.GridError):
+        ngf.register(R, T)
