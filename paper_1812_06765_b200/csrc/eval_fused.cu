@@ -1,18 +1,22 @@
 // Fused NGF objective/gradient evaluation for sm_100a (the performance path).
 //
-// One CTA owns a kTX x kTY column of image voxels and marches CZ z-planes.  Per
-// plane p it (A) interpolates yhat = P y on the fly (bit-exact with transfer.py:
-// 117-148), warps the template (warp.py:64-90) and the interpolant derivative
-// (warp.py:93-127) on the tile plus a one-voxel ring, (B) forms grad W, the NGF
-// ratio and q (ngf.py:70-112) for the previous plane on the tile interior, and
-// (C) applies G^T (warp.py:159-184), the warp Jacobian transpose and a
-// tile-local, fixed-order P^T (transfer.py:151-192) two planes behind.  yhat, W,
-// grad W, q, s and ghat never leave the SM: per evaluation HBM sees the template,
-// the packed reference terms, y and the small per-tile P^T partials only.
-//
-// Because G^T and P^T are linear, the ring voxels carry only this tile's
-// contributions; neighbouring tiles add theirs to the same def nodes in
-// ngf_reduce_kernel, in a fixed order (deterministic, no atomics).
+// One CTA owns a kTX x kTY column of image voxels plus a one-voxel ring
+// (E1 = (kTX+2) x (kTY+2) positions, kSlots per thread) and marches a chunk of
+// z-planes.  Step p of the march
+//   (A) interpolates yhat = P y on the fly for plane p (bit-exact with transfer.py:
+//       117-148, so the inside/floor decisions of warp.py:32-53 match the
+//       reference), gathers the 8 template corners of every slot at once and forms
+//       W (warp.py:64-90) and the interpolant derivative / h (warp.py:93-127);
+//   (B) forms grad W (warp.py:130-143), the NGF ratio, the distance term and
+//       q = dD/d(grad W) (ngf.py:70-112) on the tile interior for plane p-1, with
+//       the packed reference terms prefetched one step ahead;
+//   (C) applies G^T (warp.py:159-184) and the warp Jacobian transpose for plane p-2
+//       and accumulates P^T along z in registers (transfer.py:151-192 with the
+//       axes reordered z-first); when a deformation plane is complete, the CTA
+//       reduces it in x then y in a fixed order and writes its window partial.
+// yhat, W, grad W, q, s and ghat never leave the SM.  G^T and P^T are linear, so
+// ring voxels carry only this tile's contributions; k_reduce adds the tiles that
+// share a deformation node in a fixed order (deterministic, no atomics).
 
 #include <vector>
 
@@ -54,130 +58,120 @@ __device__ __forceinline__ void fdt_coef(int i, int n, T ih, T& gm, T& g0, T& gp
 }
 
 template <typename T>
-struct Slot {
-    T ylo[3], yhi[3];  // P_xy y on the current def-plane pair
-    T W[3];            // own W per plane ring
-    T dT[3][3];        // own interpolant derivative (already / h) per plane ring
-    T qz[3];           // own q_z per plane ring
-};
-
-template <typename T>
 struct Smem {
     T* colG;    // [kE1X][3]  G coefficients (cm, c0, cp)
     T* colGt;   // [kE1X][3]  G^T coefficients
     T* rowG;    // [kE1Y][3]
     T* rowGt;   // [kE1Y][3]
-    T* colW;    // [kE1X][2]  P^T weights to dlo (1-w1) and dlo+1 (w1)
-    T* rowW;    // [kE1Y][2]
-    T* colPw;   // [kE1X]     P weight wx (T)
+    T* colPw;   // [kE1X]     P weight wx (dtype)
     T* rowPw;   // [kE1Y]
-    T* Wsm;     // [3][kE1]
-    T* qx;      // [3][kE2]
+    T* Wsm;     // [3][kE1]   W ring (planes p-2, p-1, p)
+    T* qx;      // [3][kE2]   q_x ring, zero-padded
     T* qy;      // [3][kE2]
-    T* gh;      // [3][kE1]
-    T* Xr;      // [3][kE1Y][wx]
-    T* acc;     // [wz][wy][wx][3]
-    int* colDlo;  // [kE1X] P^T local def col (-1000 if outside)
-    int* rowDlo;  // [kE1Y]
-    int* colP0;   // [kE1X] P: def x0, x1
+    T* buf;     // [3][kE1]   completed deformation plane (z-reduced ghat)
+    T* Xr;      // [3][kE1Y][wx] x-reduced
+    T* xw;      // [2*kE1X]   CSR weights, window column d <- E1 columns
+    T* yw;      // [2*kE1Y]
+    int* colP0;  // [kE1X] P: def x0, x1
     int* colP1;
     int* rowP0;
     int* rowP1;
-    int* cs;  // [wx] x ranges
-    int* ce;
-    int* rs;  // [wy]
-    int* re;
+    int* xoff;  // [wx+1]
+    int* xcol;  // [2*kE1X]
+    int* yoff;  // [wy+1]
+    int* yrow;  // [2*kE1Y]
     double* red;  // [kThreads/32]
 };
 
 template <typename T>
-__device__ __forceinline__ size_t carve(unsigned char*& p, size_t count) {
+__device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
     size_t bytes = (count * sizeof(T) + 15) & ~size_t(15);
-    unsigned char* q = p;
+    T* q = reinterpret_cast<T*>(p);
     p += bytes;
-    return (size_t)q;
+    return q;
 }
 
 template <typename T>
 __host__ __device__ inline size_t fused_smem_bytes(int wx, int wy, int wz) {
     auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
+    (void)wz;
     size_t s = 0;
     s += al(kE1X * 3 * sizeof(T)) * 2 + al(kE1Y * 3 * sizeof(T)) * 2;
-    s += al(kE1X * 2 * sizeof(T)) + al(kE1Y * 2 * sizeof(T));
     s += al(kE1X * sizeof(T)) + al(kE1Y * sizeof(T));
     s += al(3 * kE1 * sizeof(T));
     s += al(3 * kE2 * sizeof(T)) * 2;
     s += al(3 * kE1 * sizeof(T));
     s += al((size_t)3 * kE1Y * wx * sizeof(T));
-    s += al((size_t)wz * wy * wx * 3 * sizeof(T));
-    s += al(kE1X * 4) * 3 + al(kE1Y * 4) * 3;
-    s += al(wx * 4) * 2 + al(wy * 4) * 2;
+    s += al(2 * kE1X * sizeof(T)) + al(2 * kE1Y * sizeof(T));
+    s += al(kE1X * 4) * 2 + al(kE1Y * 4) * 2;
+    s += al((wx + 1) * 4) + al(2 * kE1X * 4) + al((wy + 1) * 4) + al(2 * kE1Y * 4);
     s += al((kThreads / 32) * 8);
     return s;
 }
 
 template <typename T>
-__device__ __forceinline__ Smem<T> carve_smem(unsigned char* base, int wx, int wy, int wz) {
+__device__ __forceinline__ Smem<T> carve_smem(unsigned char* base, int wx, int wy) {
     Smem<T> s;
     unsigned char* p = base;
-    s.colG = (T*)carve<T>(p, kE1X * 3);
-    s.colGt = (T*)carve<T>(p, kE1X * 3);
-    s.rowG = (T*)carve<T>(p, kE1Y * 3);
-    s.rowGt = (T*)carve<T>(p, kE1Y * 3);
-    s.colW = (T*)carve<T>(p, kE1X * 2);
-    s.rowW = (T*)carve<T>(p, kE1Y * 2);
-    s.colPw = (T*)carve<T>(p, kE1X);
-    s.rowPw = (T*)carve<T>(p, kE1Y);
-    s.Wsm = (T*)carve<T>(p, 3 * kE1);
-    s.qx = (T*)carve<T>(p, 3 * kE2);
-    s.qy = (T*)carve<T>(p, 3 * kE2);
-    s.gh = (T*)carve<T>(p, 3 * kE1);
-    s.Xr = (T*)carve<T>(p, (size_t)3 * kE1Y * wx);
-    s.acc = (T*)carve<T>(p, (size_t)wz * wy * wx * 3);
-    s.colDlo = (int*)carve<int>(p, kE1X);
-    s.rowDlo = (int*)carve<int>(p, kE1Y);
-    s.colP0 = (int*)carve<int>(p, kE1X);
-    s.colP1 = (int*)carve<int>(p, kE1X);
-    s.rowP0 = (int*)carve<int>(p, kE1Y);
-    s.rowP1 = (int*)carve<int>(p, kE1Y);
-    s.cs = (int*)carve<int>(p, wx);
-    s.ce = (int*)carve<int>(p, wx);
-    s.rs = (int*)carve<int>(p, wy);
-    s.re = (int*)carve<int>(p, wy);
-    s.red = (double*)carve<double>(p, kThreads / 32);
+    s.colG = carve<T>(p, kE1X * 3);
+    s.colGt = carve<T>(p, kE1X * 3);
+    s.rowG = carve<T>(p, kE1Y * 3);
+    s.rowGt = carve<T>(p, kE1Y * 3);
+    s.colPw = carve<T>(p, kE1X);
+    s.rowPw = carve<T>(p, kE1Y);
+    s.Wsm = carve<T>(p, 3 * kE1);
+    s.qx = carve<T>(p, 3 * kE2);
+    s.qy = carve<T>(p, 3 * kE2);
+    s.buf = carve<T>(p, 3 * kE1);
+    s.Xr = carve<T>(p, (size_t)3 * kE1Y * wx);
+    s.xw = carve<T>(p, 2 * kE1X);
+    s.yw = carve<T>(p, 2 * kE1Y);
+    s.colP0 = carve<int>(p, kE1X);
+    s.colP1 = carve<int>(p, kE1X);
+    s.rowP0 = carve<int>(p, kE1Y);
+    s.rowP1 = carve<int>(p, kE1Y);
+    s.xoff = carve<int>(p, wx + 1);
+    s.xcol = carve<int>(p, 2 * kE1X);
+    s.yoff = carve<int>(p, wy + 1);
+    s.yrow = carve<int>(p, 2 * kE1Y);
+    s.red = carve<double>(p, kThreads / 32);
     return s;
 }
 
+// Per-thread march state.  Slot s owns E1 position P = tid + s * kThreads for all planes.
 template <typename T>
-struct Ctx {
-    const FusedArgs<T>* a;
-    Smem<T> sm;
-    int x0, y0, z0, z1;
-    int wxlo, wylo, wzlo;
-    int cur_zd;
+struct March {
+    int P[kSlots];     // flat E1 index (-1: no position)
+    int P2[kSlots];    // index in the zero-padded q layout
+    int ij[kSlots];    // j * nx + i of the image column (RT / volume offset in a plane)
+    int exy[kSlots];   // ex | ey << 8
+    unsigned flags;    // bit s: inside the image in x/y; bit 8+s: tile interior
+    T ylo[kSlots][3], yhi[kSlots][3];   // P_xy y on the current def-plane pair
+    T dT[kSlots][3][3];                 // interpolant derivative / h, plane ring
+    T qz[kSlots][3];                    // q_z, plane ring
+    T A0[kSlots][3], A1[kSlots][3];     // z-accumulated ghat for def planes zd, zd+1
+    V4T<T> rt[kSlots];                  // prefetched reference terms (next B plane)
+    int z0, z1, jfirst, jlast, wxlo, wylo, wzlo, cur_zd, cta;
     double dacc;
 };
 
-// per-slot static position info
-struct SlotPos {
-    int P;      // flat E1 index or -1
-    int ex, ey;
-    int i, j;   // image column / row
-    bool vol;   // inside the image in x/y
-    bool e0;    // tile interior
-};
+template <typename T>
+__device__ __forceinline__ bool slot_vol(const March<T>& m, int s) { return (m.flags >> s) & 1u; }
+template <typename T>
+__device__ __forceinline__ bool slot_e0(const March<T>& m, int s) { return (m.flags >> (8 + s)) & 1u; }
 
 template <typename T>
-__device__ __forceinline__ void load_yplane(const Ctx<T>& c, const SlotPos& sp, int zd, T out[3]) {
+__device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const Smem<T>& sm, int exy, int zd,
+                                            T (&out)[3]) {
     // P_xy y on def plane zd at the slot's image (i, j): x then y (transfer.py:136-142)
-    const FusedArgs<T>& a = *c.a;
-    const int x0 = c.sm.colP0[sp.ex], x1 = c.sm.colP1[sp.ex];
-    const int y0 = c.sm.rowP0[sp.ey], y1 = c.sm.rowP1[sp.ey];
-    const T wx = c.sm.colPw[sp.ex], wy = c.sm.rowPw[sp.ey];
-    const int64_t m = (int64_t)a.ndx * a.ndy * a.ndz;
+    const int ex = exy & 0xff, ey = exy >> 8;
+    const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
+    const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
+    const T wx = sm.colPw[ex], wy = sm.rowPw[ey];
+    const int64_t mm = (int64_t)a.ndx * a.ndy * a.ndz;
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const T* yc = a.y + k * m + (int64_t)zd * a.ndx * a.ndy;
+        const T* yc = a.y + k * mm + (int64_t)zd * a.ndx * a.ndy;
         const T* r0 = yc + (int64_t)y0 * a.ndx;
         const T* r1 = yc + (int64_t)y1 * a.ndx;
         const T X0 = lerp_exact(__ldg(r0 + x0), __ldg(r0 + x1), wx);
@@ -186,56 +180,132 @@ __device__ __forceinline__ void load_yplane(const Ctx<T>& c, const SlotPos& sp, 
     }
 }
 
+// Reduce a completed deformation plane (z-accumulated ghat in `acc`) in x then y over
+// the tile's window and write it to the CTA's partial slot zs.
+template <typename T>
+__device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>& sm, March<T>& m,
+                                            T (&acc)[kSlots][3], int zs) {
+    const int wx = a.fp.wx, wy = a.fp.wy;
+#pragma unroll
+    for (int s = 0; s < kSlots; ++s) {
+        if (m.P[s] < 0) continue;
+#pragma unroll
+        for (int c = 0; c < 3; ++c) sm.buf[c * kE1 + m.P[s]] = acc[s][c];
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < kE1Y * wx; t += kThreads) {
+        const int row = t / wx;
+        const int d = t - row * wx;
+        const int k0 = sm.xoff[d], k1 = sm.xoff[d + 1];
+        T r0 = (T)0, r1 = (T)0, r2 = (T)0;
+        const T* b = sm.buf + row * kE1X;
+        for (int k = k0; k < k1; ++k) {
+            const int e = sm.xcol[k];
+            const T w = sm.xw[k];
+            r0 = fmaf_t(b[e], w, r0);
+            r1 = fmaf_t(b[kE1 + e], w, r1);
+            r2 = fmaf_t(b[2 * kE1 + e], w, r2);
+        }
+        sm.Xr[(0 * kE1Y + row) * wx + d] = r0;
+        sm.Xr[(1 * kE1Y + row) * wx + d] = r1;
+        sm.Xr[(2 * kE1Y + row) * wx + d] = r2;
+    }
+    __syncthreads();
+    const size_t win = (size_t)a.fp.wz * wy * wx;
+    T* out = a.partial + (size_t)m.cta * 3 * win + (size_t)zs * wy * wx;
+    for (int t = threadIdx.x; t < wy * wx; t += kThreads) {
+        const int dr = t / wx;
+        const int d = t - dr * wx;
+        const int k0 = sm.yoff[dr], k1 = sm.yoff[dr + 1];
+        T r0 = (T)0, r1 = (T)0, r2 = (T)0;
+        for (int k = k0; k < k1; ++k) {
+            const int row = sm.yrow[k];
+            const T w = sm.yw[k];
+            r0 = fmaf_t(sm.Xr[(0 * kE1Y + row) * wx + d], w, r0);
+            r1 = fmaf_t(sm.Xr[(1 * kE1Y + row) * wx + d], w, r1);
+            r2 = fmaf_t(sm.Xr[(2 * kE1Y + row) * wx + d], w, r2);
+        }
+        out[t] = r0;
+        out[win + t] = r1;
+        out[2 * win + t] = r2;
+    }
+}
+
 template <int R, typename T>
-__device__ __forceinline__ void fused_step(Ctx<T>& c, Slot<T> (&st)[kSlots],
-                                           const SlotPos (&sp)[kSlots], int p) {
-    const FusedArgs<T>& a = *c.a;
-    Smem<T>& sm = c.sm;
+__device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>& sm, March<T>& m,
+                                           int p) {
     constexpr int RB = (R + 2) % 3;  // plane p-1
     constexpr int RC = (R + 1) % 3;  // plane p-2
 
     // ---------------------------------------------------------------- (A) plane p
-    const bool pv = (p >= 0) && (p < a.nz) && (p <= c.z1);
-    if (pv) {
+    if (p >= 0 && p < a.nz && p <= m.z1) {
         const int zd = a.i0z[p];
-        if (zd != c.cur_zd) {
+        if (zd != m.cur_zd) {
             const int zd1 = min(zd + 1, a.ndz - 1);
-            const bool shift = (zd == c.cur_zd + 1);
+            const bool shift = (zd == m.cur_zd + 1);
 #pragma unroll
             for (int s = 0; s < kSlots; ++s) {
-                if (sp[s].P < 0 || !sp[s].vol) continue;
+                if (!slot_vol(m, s)) continue;
                 if (shift) {
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) st[s].ylo[k] = st[s].yhi[k];
+                    for (int k = 0; k < 3; ++k) m.ylo[s][k] = m.yhi[s][k];
                 } else {
-                    load_yplane(c, sp[s], zd, st[s].ylo);
+                    load_yplane(a, sm, m.exy[s], zd, m.ylo[s]);
                 }
-                load_yplane(c, sp[s], zd1, st[s].yhi);
+                load_yplane(a, sm, m.exy[s], zd1, m.yhi[s]);
             }
-            c.cur_zd = zd;
+            m.cur_zd = zd;
         }
         const T wz = a.w1z[p];
+        // coordinates and corner addresses of all slots first, so the 8 * kSlots
+        // gathers are in flight together
+        const T* base[kSlots];
+        T fx[kSlots], fy[kSlots], fz[kSlots];
+        bool in[kSlots];
 #pragma unroll
         for (int s = 0; s < kSlots; ++s) {
-            T W = (T)0, d0 = (T)0, d1 = (T)0, d2 = (T)0;
-            if (sp[s].P >= 0 && sp[s].vol) {
-                T yh[3];
+            T yh0 = lerp_exact(m.ylo[s][0], m.yhi[s][0], wz);
+            T yh1 = lerp_exact(m.ylo[s][1], m.yhi[s][1], wz);
+            T yh2 = lerp_exact(m.ylo[s][2], m.yhi[s][2], wz);
+            bool inside = slot_vol(m, s);
+            int ix, iy, iz;
+            axis_cell(tcoord(yh0, a.ox, a.hx, a.ihx, a.pow2x), a.nx, inside, ix, fx[s]);
+            axis_cell(tcoord(yh1, a.oy, a.hy, a.ihy, a.pow2y), a.ny, inside, iy, fy[s]);
+            axis_cell(tcoord(yh2, a.oz, a.hz, a.ihz, a.pow2z), a.nz, inside, iz, fz[s]);
+            in[s] = inside;
+            base[s] = a.Tv + ((int64_t)iz * a.ny + iy) * a.nx + ix;
+        }
+        const int64_t sx = a.nx > 1 ? 1 : 0;
+        const int64_t sy = a.ny > 1 ? a.nx : 0;
+        const int64_t sz = a.nz > 1 ? (int64_t)a.nx * a.ny : 0;
+        T cv[kSlots][8];
 #pragma unroll
-                for (int k = 0; k < 3; ++k) yh[k] = lerp_exact(st[s].ylo[k], st[s].yhi[k], wz);
-                warp_point(a, yh, W, d0, d1, d2);
-            }
-            st[s].W[R] = W;
-            st[s].dT[R][0] = d0;
-            st[s].dT[R][1] = d1;
-            st[s].dT[R][2] = d2;
-            if (sp[s].P >= 0) sm.Wsm[R * kE1 + sp[s].P] = W;
+        for (int s = 0; s < kSlots; ++s) {
+            const T* b = base[s];
+            cv[s][0] = __ldg(b);
+            cv[s][1] = __ldg(b + sx);
+            cv[s][2] = __ldg(b + sy);
+            cv[s][3] = __ldg(b + sy + sx);
+            cv[s][4] = __ldg(b + sz);
+            cv[s][5] = __ldg(b + sz + sx);
+            cv[s][6] = __ldg(b + sz + sy);
+            cv[s][7] = __ldg(b + sz + sy + sx);
+        }
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s) {
+            T W, d0, d1, d2;
+            trilinear(a, cv[s], fx[s], fy[s], fz[s], W, d0, d1, d2);
+            if (!in[s]) W = d0 = d1 = d2 = (T)0;
+            m.dT[s][R][0] = d0;
+            m.dT[s][R][1] = d1;
+            m.dT[s][R][2] = d2;
+            if (m.P[s] >= 0) sm.Wsm[R * kE1 + m.P[s]] = W;
         }
     } else {
 #pragma unroll
         for (int s = 0; s < kSlots; ++s) {
-            st[s].W[R] = (T)0;
-            st[s].dT[R][0] = st[s].dT[R][1] = st[s].dT[R][2] = (T)0;
-            if (sp[s].P >= 0) sm.Wsm[R * kE1 + sp[s].P] = (T)0;
+            m.dT[s][R][0] = m.dT[s][R][1] = m.dT[s][R][2] = (T)0;
+            if (m.P[s] >= 0) sm.Wsm[R * kE1 + m.P[s]] = (T)0;
         }
     }
     __syncthreads();
@@ -243,131 +313,121 @@ __device__ __forceinline__ void fused_step(Ctx<T>& c, Slot<T> (&st)[kSlots],
     // ---------------------------------------------------------------- (B) q on plane k = p-1
     {
         const int k = p - 1;
-        const bool kv = (k >= c.z0) && (k < c.z1);
+        const bool kv = (k >= m.z0) && (k < m.z1);
         T cmz, c0z, cpz;
         fd_coef<T>(k, a.nz, a.ihz, cmz, c0z, cpz);
         const T* Wk = sm.Wsm + RB * kE1;
+        const T* Wm = sm.Wsm + RC * kE1;
+        const T* Wp = sm.Wsm + R * kE1;
 #pragma unroll
         for (int s = 0; s < kSlots; ++s) {
             T qxv = (T)0, qyv = (T)0, qzv = (T)0;
-            if (kv && sp[s].e0) {
-                const int P = sp[s].P;
-                const T* cg = sm.colG + 3 * sp[s].ex;
-                const T* rg = sm.rowG + 3 * sp[s].ey;
-                const T gx = cg[0] * Wk[P - 1] + cg[1] * Wk[P] + cg[2] * Wk[P + 1];
-                const T gy = rg[0] * Wk[P - kE1X] + rg[1] * Wk[P] + rg[2] * Wk[P + kE1X];
-                const T gz = cmz * st[s].W[RC] + c0z * st[s].W[RB] + cpz * st[s].W[R];
-                const V4T<T> rt = ld_rt(a.RT + ((int64_t)k * a.ny + sp[s].j) * a.nx + sp[s].i);
-                ngf_q(a, gx, gy, gz, rt, qxv, qyv, qzv, c.dacc);
+            if (kv && slot_e0(m, s)) {
+                const int P = m.P[s];
+                const int ex = m.exy[s] & 0xff, ey = m.exy[s] >> 8;
+                const T* cg = sm.colG + 3 * ex;
+                const T* rg = sm.rowG + 3 * ey;
+                const T gx = fmaf_t(cg[0], Wk[P - 1], fmaf_t(cg[1], Wk[P], cg[2] * Wk[P + 1]));
+                const T gy = fmaf_t(rg[0], Wk[P - kE1X], fmaf_t(rg[1], Wk[P], rg[2] * Wk[P + kE1X]));
+                const T gz = fmaf_t(cmz, Wm[P], fmaf_t(c0z, Wk[P], cpz * Wp[P]));
+                ngf_q(a, gx, gy, gz, m.rt[s], qxv, qyv, qzv, m.dacc);
             }
-            if (sp[s].P >= 0) {
-                const int P2 = (sp[s].ey + 1) * kE2X + sp[s].ex + 1;
-                sm.qx[RB * kE2 + P2] = qxv;
-                sm.qy[RB * kE2 + P2] = qyv;
+            if (m.P[s] >= 0) {
+                sm.qx[RB * kE2 + m.P2[s]] = qxv;
+                sm.qy[RB * kE2 + m.P2[s]] = qyv;
             }
-            st[s].qz[RB] = qzv;
+            m.qz[s][RB] = qzv;
+        }
+        // prefetch the reference terms of plane p for the next step's (B)
+        if (p >= m.z0 && p < m.z1) {
+            const V4T<T>* rp = a.RT + (int64_t)p * a.nx * a.ny;
+#pragma unroll
+            for (int s = 0; s < kSlots; ++s)
+                if (slot_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
         }
     }
     __syncthreads();
 
-    // ---------------------------------------------------------------- (C) s, ghat, P^T on j = p-2
+    // ---------------------------------------------------------------- (C) s, ghat, z-P^T on j = p-2
     const int j = p - 2;
-    const bool jv = (j >= c.z0 - 1) && (j <= c.z1) && (j >= 0) && (j < a.nz);
-    if (!jv) return;  // uniform
-    {
-        T gtm, gt0, gtp;
-        fdt_coef<T>(j, a.nz, a.ihz, gtm, gt0, gtp);
-        const T* qxj = sm.qx + RC * kE2;
-        const T* qyj = sm.qy + RC * kE2;
+    if (j < m.jfirst || j > m.jlast) return;  // uniform
+    T gtm, gt0, gtp;
+    fdt_coef<T>(j, a.nz, a.ihz, gtm, gt0, gtp);
+    const T* qxj = sm.qx + RC * kE2;
+    const T* qyj = sm.qy + RC * kE2;
+    const int zdj = a.i0z[j];
+    const T w1 = a.w1z[j];
+    const T w0 = (T)1 - w1;
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
-            if (sp[s].P < 0) continue;
-            T g0 = (T)0, g1 = (T)0, g2 = (T)0;
-            if (sp[s].vol) {
-                const int P2 = (sp[s].ey + 1) * kE2X + sp[s].ex + 1;
-                const T* ct = sm.colGt + 3 * sp[s].ex;
-                const T* rt = sm.rowGt + 3 * sp[s].ey;
-                T sv = ct[0] * qxj[P2 - 1] + ct[1] * qxj[P2] + ct[2] * qxj[P2 + 1];
-                sv += rt[0] * qyj[P2 - kE2X] + rt[1] * qyj[P2] + rt[2] * qyj[P2 + kE2X];
-                sv += gtm * st[s].qz[R] + gt0 * st[s].qz[RC] + gtp * st[s].qz[RB];
-                g0 = sv * st[s].dT[RC][0];
-                g1 = sv * st[s].dT[RC][1];
-                g2 = sv * st[s].dT[RC][2];
-            }
-            sm.gh[sp[s].P] = g0;
-            sm.gh[kE1 + sp[s].P] = g1;
-            sm.gh[2 * kE1 + sp[s].P] = g2;
+    for (int s = 0; s < kSlots; ++s) {
+        if (!slot_vol(m, s)) continue;
+        const int P2 = m.P2[s];
+        const int ex = m.exy[s] & 0xff, ey = m.exy[s] >> 8;
+        const T* ct = sm.colGt + 3 * ex;
+        const T* rt = sm.rowGt + 3 * ey;
+        T sv = fmaf_t(ct[0], qxj[P2 - 1], fmaf_t(ct[1], qxj[P2], ct[2] * qxj[P2 + 1]));
+        sv = fmaf_t(rt[0], qyj[P2 - kE2X], fmaf_t(rt[1], qyj[P2], fmaf_t(rt[2], qyj[P2 + kE2X], sv)));
+        sv = fmaf_t(gtm, m.qz[s][R], fmaf_t(gt0, m.qz[s][RC], fmaf_t(gtp, m.qz[s][RB], sv)));
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            const T g = sv * m.dT[s][RC][c];
+            m.A0[s][c] = fmaf_t(w0, g, m.A0[s][c]);
+            m.A1[s][c] = fmaf_t(w1, g, m.A1[s][c]);
         }
     }
-    __syncthreads();
-    // x-reduce: Xr[c][row][d] = sum over E1 columns feeding window column d
-    {
-        const int wx = a.fp.wx;
-        const int ntask = 3 * kE1Y * wx;
-        for (int t = threadIdx.x; t < ntask; t += kThreads) {
-            const int d = t % wx;
-            const int row = (t / wx) % kE1Y;
-            const int comp = t / (wx * kE1Y);
-            const T* g = sm.gh + comp * kE1 + row * kE1X;
-            T acc = (T)0;
-            for (int e = sm.cs[d]; e < sm.ce[d]; ++e) {
-                const T w = (sm.colDlo[e] == d) ? sm.colW[2 * e] : sm.colW[2 * e + 1];
-                acc += g[e] * w;
+    // def plane zdj is complete when the next image plane maps to a later pair.  The map
+    // can advance by 2 (w1 rounds to just below 1 when the grids nearly coincide), in
+    // which case zdj + 1 is complete as well.
+    const bool last = (j == m.jlast);
+    const int step = last ? 2 : a.i0z[j + 1] - zdj;
+    if (step >= 1) {
+        flush_plane(a, sm, m, m.A0, zdj - m.wzlo);
+        if (step >= 2) {
+            if (zdj + 1 <= a.ndz - 1) {
+                __syncthreads();
+                flush_plane(a, sm, m, m.A1, zdj + 1 - m.wzlo);
             }
-            sm.Xr[(comp * kE1Y + row) * wx + d] = acc;
-        }
-    }
-    __syncthreads();
-    // y-reduce and z-accumulate into the tile's def-node window
-    {
-        const int wx = a.fp.wx, wy = a.fp.wy;
-        const int ntask = 3 * wy * wx;
-        const int zd = a.i0z[j] - c.wzlo;
-        const T w1 = a.w1z[j];
-        const T w0 = (T)1 - w1;
-        const bool two = a.ndz > 1;
-        for (int t = threadIdx.x; t < ntask; t += kThreads) {
-            const int d = t % wx;
-            const int dr = (t / wx) % wy;
-            const int comp = t / (wx * wy);
-            T acc = (T)0;
-            for (int e = sm.rs[dr]; e < sm.re[dr]; ++e) {
-                const T w = (sm.rowDlo[e] == dr) ? sm.rowW[2 * e] : sm.rowW[2 * e + 1];
-                acc += sm.Xr[(comp * kE1Y + e) * wx + d] * w;
-            }
-            T* A = sm.acc + ((size_t)(zd * wy + dr) * wx + d) * 3 + comp;
-            A[0] += w0 * acc;
-            if (two) A[(size_t)wy * wx * 3] += w1 * acc;
+#pragma unroll
+            for (int s = 0; s < kSlots; ++s)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) m.A0[s][c] = m.A1[s][c] = (T)0;
+        } else {
+#pragma unroll
+            for (int s = 0; s < kSlots; ++s)
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    m.A0[s][c] = m.A1[s][c];
+                    m.A1[s][c] = (T)0;
+                }
         }
     }
 }
 
 template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const FusedArgs<T> a) {
+__global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    Ctx<T> c;
-    c.a = &a;
     const FusedPlan& fp = a.fp;
-    c.sm = carve_smem<T>(smem_raw, fp.wx, fp.wy, fp.wz);
-    Smem<T>& sm = c.sm;
+    const Smem<T> sm = carve_smem<T>(smem_raw, fp.wx, fp.wy);
     const int tid = threadIdx.x;
-    const int cta = blockIdx.x;
-    const int tx = cta % fp.ntx;
-    const int ty = (cta / fp.ntx) % fp.nty;
-    const int tz = cta / (fp.ntx * fp.nty);
-    c.x0 = tx * kTX;
-    c.y0 = ty * kTY;
-    c.z0 = tz * fp.cz;
-    c.z1 = min(c.z0 + fp.cz, a.nz);
-    c.wxlo = fp.win_x[tx];
-    c.wylo = fp.win_y[ty];
-    c.wzlo = fp.win_z[tz];
-    c.cur_zd = -1000;
-    c.dacc = 0.0;
+    March<T> m;
+    m.cta = blockIdx.x;
+    const int tx = m.cta % fp.ntx;
+    const int ty = (m.cta / fp.ntx) % fp.nty;
+    const int tz = m.cta / (fp.ntx * fp.nty);
+    const int x0 = tx * kTX, y0 = ty * kTY;
+    m.z0 = tz * fp.cz;
+    m.z1 = min(m.z0 + fp.cz, a.nz);
+    m.jfirst = max(m.z0 - 1, 0);
+    m.jlast = min(m.z1, a.nz - 1);
+    m.wxlo = fp.win_x[tx];
+    m.wylo = fp.win_y[ty];
+    m.wzlo = fp.win_z[tz];
+    m.cur_zd = -1000;
+    m.dacc = 0.0;
 
     // ---- per-CTA tables
     for (int e = tid; e < kE1X; e += kThreads) {
-        const int i = c.x0 - 1 + e;
+        const int i = x0 - 1 + e;
         T cm, c0, cp;
         fd_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
         sm.colG[3 * e] = cm;
@@ -379,16 +439,12 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const FusedArgs<T> a
         sm.colGt[3 * e + 2] = cp;
         const bool in = i >= 0 && i < a.nx;
         const int i0 = in ? a.i0x[i] : 0;
-        const T w1 = in ? a.w1x[i] : (T)0;
-        sm.colDlo[e] = in ? i0 - c.wxlo : -1000;
-        sm.colW[2 * e] = (T)1 - w1;
-        sm.colW[2 * e + 1] = w1;
         sm.colP0[e] = i0;
         sm.colP1[e] = min(i0 + 1, a.ndx - 1);
-        sm.colPw[e] = w1;
+        sm.colPw[e] = in ? a.w1x[i] : (T)0;
     }
     for (int e = tid; e < kE1Y; e += kThreads) {
-        const int jj = c.y0 - 1 + e;
+        const int jj = y0 - 1 + e;
         T cm, c0, cp;
         fd_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
         sm.rowG[3 * e] = cm;
@@ -400,105 +456,93 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const FusedArgs<T> a
         sm.rowGt[3 * e + 2] = cp;
         const bool in = jj >= 0 && jj < a.ny;
         const int i0 = in ? a.i0y[jj] : 0;
-        const T w1 = in ? a.w1y[jj] : (T)0;
-        sm.rowDlo[e] = in ? i0 - c.wylo : -1000;
-        sm.rowW[2 * e] = (T)1 - w1;
-        sm.rowW[2 * e + 1] = w1;
         sm.rowP0[e] = i0;
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
-        sm.rowPw[e] = w1;
+        sm.rowPw[e] = in ? a.w1y[jj] : (T)0;
     }
     for (int t = tid; t < 3 * kE2; t += kThreads) {
         sm.qx[t] = (T)0;
         sm.qy[t] = (T)0;
     }
-    const int nacc = fp.wz * fp.wy * fp.wx * 3;
-    for (int t = tid; t < nacc; t += kThreads) sm.acc[t] = (T)0;
-    __syncthreads();
-    if (tid == 0) {
-        // x ranges: window column d <- E1 columns with dlo in {d-1, d} (contiguous)
-        for (int d = 0; d < fp.wx; ++d) {
-            int s0 = kE1X, s1 = 0;
-            for (int e = 0; e < kE1X; ++e) {
-                const int dl = sm.colDlo[e];
-                const bool hit = (dl == d) || (dl == d - 1 && a.ndx > 1);
-                if (hit) {
-                    s0 = min(s0, e);
-                    s1 = max(s1, e + 1);
+    if (tid == 0 || tid == 32) {
+        // CSR of the transposed 1-D interpolation over the tile window, ascending
+        // E1 index per window entry (the reference's gather order, transfer.py:89-96)
+        const bool isx = tid == 0;
+        const int ne = isx ? kE1X : kE1Y, w = isx ? fp.wx : fp.wy, org = isx ? x0 : y0;
+        const int n = isx ? a.nx : a.ny, nd = isx ? a.ndx : a.ndy, lo = isx ? m.wxlo : m.wylo;
+        const int32_t* i0a = isx ? a.i0x : a.i0y;
+        const T* w1a = isx ? a.w1x : a.w1y;
+        int* off = isx ? sm.xoff : sm.yoff;
+        int* idx = isx ? sm.xcol : sm.yrow;
+        T* wt = isx ? sm.xw : sm.yw;
+        int cnt = 0;
+        for (int d = 0; d < w; ++d) {
+            off[d] = cnt;
+            for (int e = 0; e < ne; ++e) {
+                const int i = org - 1 + e;
+                if (i < 0 || i >= n) continue;
+                const int dl = i0a[i] - lo;
+                const T w1 = w1a[i];
+                if (dl == d) {
+                    idx[cnt] = e;
+                    wt[cnt++] = (T)1 - w1;
+                } else if (dl == d - 1 && nd > 1) {
+                    idx[cnt] = e;
+                    wt[cnt++] = w1;
                 }
             }
-            sm.cs[d] = s0 < s1 ? s0 : 0;
-            sm.ce[d] = s0 < s1 ? s1 : 0;
         }
-    } else if (tid == 32) {
-        for (int d = 0; d < fp.wy; ++d) {
-            int s0 = kE1Y, s1 = 0;
-            for (int e = 0; e < kE1Y; ++e) {
-                const int dl = sm.rowDlo[e];
-                const bool hit = (dl == d) || (dl == d - 1 && a.ndy > 1);
-                if (hit) {
-                    s0 = min(s0, e);
-                    s1 = max(s1, e + 1);
-                }
-            }
-            sm.rs[d] = s0 < s1 ? s0 : 0;
-            sm.re[d] = s0 < s1 ? s1 : 0;
-        }
+        off[w] = cnt;
     }
 
     // ---- slot positions (fixed for all planes)
-    SlotPos sp[kSlots];
+    m.flags = 0u;
 #pragma unroll
     for (int s = 0; s < kSlots; ++s) {
         const int P = tid + s * kThreads;
-        SlotPos q;
-        q.P = P < kE1 ? P : -1;
-        q.ex = P % kE1X;
-        q.ey = P / kE1X;
-        if (q.P < 0) {
-            q.ex = 0;
-            q.ey = 0;
-        }
-        q.i = c.x0 - 1 + q.ex;
-        q.j = c.y0 - 1 + q.ey;
-        q.vol = q.P >= 0 && q.i >= 0 && q.i < a.nx && q.j >= 0 && q.j < a.ny;
-        q.e0 = q.vol && q.ex >= 1 && q.ex <= kTX && q.ey >= 1 && q.ey <= kTY;
-        sp[s] = q;
-    }
-    __syncthreads();
-
-    Slot<T> st[kSlots];
-#pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
+        const bool ok = P < kE1;
+        const int ex = ok ? P % kE1X : 0, ey = ok ? P / kE1X : 0;
+        const int i = x0 - 1 + ex, jj = y0 - 1 + ey;
+        const bool vol = ok && i >= 0 && i < a.nx && jj >= 0 && jj < a.ny;
+        const bool e0 = vol && ex >= 1 && ex <= kTX && ey >= 1 && ey <= kTY;
+        m.P[s] = ok ? P : -1;
+        m.P2[s] = (ey + 1) * kE2X + ex + 1;
+        m.ij[s] = vol ? jj * a.nx + i : 0;
+        m.exy[s] = ex | (ey << 8);
+        m.flags |= (vol ? 1u : 0u) << s;
+        m.flags |= (e0 ? 1u : 0u) << (8 + s);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
-            st[s].W[r] = (T)0;
-            st[s].qz[r] = (T)0;
-            st[s].dT[r][0] = st[s].dT[r][1] = st[s].dT[r][2] = (T)0;
+            m.qz[s][r] = (T)0;
+            m.dT[s][r][0] = m.dT[s][r][1] = m.dT[s][r][2] = (T)0;
         }
 #pragma unroll
-        for (int k = 0; k < 3; ++k) st[s].ylo[k] = st[s].yhi[k] = (T)0;
-    }
-
-    // planes p = z0-1 .. z1+2: A on p, B on p-1, C on p-2
-    const int pstart = c.z0 - 1;
-    const int nsteps = (c.z1 + 2) - pstart + 1;
-    for (int b = 0; b < nsteps; b += 3) {
-        fused_step<0>(c, st, sp, pstart + b);
-        if (b + 1 < nsteps) fused_step<1>(c, st, sp, pstart + b + 1);
-        if (b + 2 < nsteps) fused_step<2>(c, st, sp, pstart + b + 2);
+        for (int c = 0; c < 3; ++c) {
+            m.ylo[s][c] = m.yhi[s][c] = (T)0;
+            m.A0[s][c] = m.A1[s][c] = (T)0;
+        }
+        m.rt[s] = V4T<T>{};
     }
     __syncthreads();
-
-    // ---- write the window partials and the D partial
-    T* out = a.partial + (size_t)cta * nacc;
-    for (int t = tid; t < nacc; t += kThreads) {
-        // acc layout [wz][wy][wx][3] -> partial layout [3][wz][wy][wx]
-        const int comp = t % 3;
-        const int rest = t / 3;
-        out[(size_t)comp * (nacc / 3) + rest] = sm.acc[t];
+    // reference terms of the first interior plane
+    if (m.z0 < m.z1) {
+        const V4T<T>* rp = a.RT + (int64_t)m.z0 * a.nx * a.ny;
+#pragma unroll
+        for (int s = 0; s < kSlots; ++s)
+            if (slot_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
     }
-    double v = c.dacc;
+
+    // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2
+    const int pstart = m.z0 - 1;
+    const int nsteps = (m.z1 + 2) - pstart + 1;
+    for (int b = 0; b < nsteps; b += 3) {
+        fused_step<0>(a, sm, m, pstart + b);
+        if (b + 1 < nsteps) fused_step<1>(a, sm, m, pstart + b + 1);
+        if (b + 2 < nsteps) fused_step<2>(a, sm, m, pstart + b + 2);
+    }
+
+    // ---- the CTA's D partial
+    double v = m.dacc;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
     if ((tid & 31) == 0) sm.red[tid >> 5] = v;
@@ -506,7 +550,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const FusedArgs<T> a
     if (tid == 0) {
         double sacc = 0.0;
         for (int w = 0; w < kThreads / 32; ++w) sacc += sm.red[w];
-        a.dpart[cta] = sacc;
+        a.dpart[m.cta] = sacc;
     }
 }
 

@@ -32,7 +32,7 @@ struct FusedPlan {
     int n_cta;
     size_t smem_bytes;
 };
-constexpr int kCover = 4;
+constexpr int kCover = 8;
 
 struct LevelDev;  // defined in level.cu
 

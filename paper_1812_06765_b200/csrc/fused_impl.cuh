@@ -120,6 +120,24 @@ __device__ __forceinline__ void warp_point(const FusedArgs<T>& a, const T (&yh)[
     d2 = dz * a.ihz;
 }
 
+// Trilinear value and derivative / h from the 8 corners c[dx + 2 dy + 4 dz] (lerp form
+// of warp.py:79-85 and :111-120)
+template <typename T>
+__device__ __forceinline__ void trilinear(const FusedArgs<T>& a, const T (&c)[8], T fx, T fy, T fz,
+                                          T& W, T& d0, T& d1, T& d2) {
+    const T e00 = c[1] - c[0], e10 = c[3] - c[2], e01 = c[5] - c[4], e11 = c[7] - c[6];
+    const T a00 = fmaf_t(fx, e00, c[0]), a10 = fmaf_t(fx, e10, c[2]);
+    const T a01 = fmaf_t(fx, e01, c[4]), a11 = fmaf_t(fx, e11, c[6]);
+    const T dy0 = a10 - a00, dy1 = a11 - a01;
+    const T b0 = fmaf_t(fy, dy0, a00), b1 = fmaf_t(fy, dy1, a01);
+    const T dz = b1 - b0;
+    W = fmaf_t(fz, dz, b0);
+    const T ex0 = fmaf_t(fy, e10 - e00, e00), ex1 = fmaf_t(fy, e11 - e01, e01);
+    d0 = fmaf_t(fz, ex1 - ex0, ex0) * a.ihx;
+    d1 = fmaf_t(fz, dy1 - dy0, dy0) * a.ihy;
+    d2 = dz * a.ihz;
+}
+
 // NGF ratio, the distance term and q = dD/d(grad W) (ngf.py:70-112), with the
 // reference terms packed as (gR/nR, 1/nR)
 template <typename T>

@@ -108,18 +108,31 @@ static int fused_setup(ngf_level* L) {
     fp.ntx = (int)xl.size();
     fp.nty = (int)yl.size();
     // z chunk: as long as possible (less z-ring recompute) while keeping >= 2 CTAs per SM
-    // busy and the window accumulator within shared memory
-    int cz = 64;
-    auto fits = [&](int c) {
+    // busy; every candidate must fit shared memory and keep each def node covered by at
+    // most kCover chunks (the reduce kernel's fixed-order sum)
+    auto valid = [&](int c, size_t limit) {
         std::vector<int> a, b;
         int wz = tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b);
-        return fused_smem<T>(fp.wx, fp.wy, wz) <= 100 * 1024;
+        if (fused_smem<T>(fp.wx, fp.wy, wz) > limit) return false;
+        std::vector<int32_t> cov;
+        return build_cover(a, b, ndz, cov);
     };
-    while (cz > 4 && ((int64_t)fp.ntx * fp.nty * ((nz + cz - 1) / cz) < 2 * kSMs || !fits(cz)))
-        cz /= 2;
-    if (cz < 4) cz = 4;
-    while (cz > 1 && !fits(cz)) cz /= 2;
-    if (!fits(cz)) return NGF_EARG;
+    int cz = 0;
+    for (size_t limit : {size_t(100) * 1024, size_t(220) * 1024}) {
+        int best_par = 0, best_any = 0;
+        for (int c = 64; c >= 1; c /= 2) {
+            if (!valid(c, limit)) continue;
+            if (!best_par && (int64_t)fp.ntx * fp.nty * ((nz + c - 1) / c) >= 2 * kSMs) best_par = c;
+            best_any = c;  // smallest valid chunk = most CTAs
+        }
+        cz = best_par ? best_par : best_any;
+        if (cz) break;
+    }
+    if (!cz) return NGF_EARG;
+    if (const char* env = std::getenv("NGF_FUSED_CZ")) {  // tuning / debugging override
+        const int forced = std::atoi(env);
+        if (forced > 0 && valid(forced, size_t(220) * 1024)) cz = forced;
+    }
     fp.cz = cz;
     fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh);
     fp.ntz = (int)zl.size();
