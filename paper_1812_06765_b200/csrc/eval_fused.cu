@@ -1,7 +1,7 @@
 // Fused NGF objective/gradient evaluation for sm_100a (the performance path).
 //
-// One CTA owns a kTX x kTY column of image voxels plus a one-voxel ring
-// (E1 = (kTX+2) x (kTY+2) positions, kSlots per thread) and marches a chunk of
+// One CTA owns a 32 x TY column of image voxels plus a one-voxel ring
+// (E1 = 34 x (TY+2) positions, S slots per thread) and marches a chunk of
 // z-planes.  Step p of the march
 //   (A) interpolates yhat = P y on the fly for plane p (bit-exact with transfer.py:
 //       117-148, so the inside/floor decisions of warp.py:32-53 match the
@@ -18,6 +18,7 @@
 // ring voxels carry only this tile's contributions; k_reduce adds the tiles that
 // share a deformation node in a fixed order (deterministic, no atomics).
 
+#include <cstdlib>
 #include <vector>
 
 #include "common.cuh"
@@ -25,6 +26,15 @@
 #include "fused_impl.cuh"
 
 namespace ngf {
+
+// Tile / launch configuration of one kernel variant.
+template <int TY_, int NT_, int MINB_>
+struct Cfg {
+    static constexpr int TX = 32, TY = TY_, NT = NT_, MINB = MINB_;
+    static constexpr int E1X = TX + 2, E1Y = TY + 2, E1 = E1X * E1Y;
+    static constexpr int S = (E1 + NT - 1) / NT;
+    static constexpr int E2X = TX + 4, E2Y = TY + 4, E2 = E2X * E2Y;
+};
 
 template <typename T>
 __device__ __forceinline__ void fd_coef(int i, int n, T ih, T& cm, T& c0, T& cp) {
@@ -59,28 +69,28 @@ __device__ __forceinline__ void fdt_coef(int i, int n, T ih, T& gm, T& g0, T& gp
 
 template <typename T>
 struct Smem {
-    T* colG;    // [kE1X][3]  G coefficients (cm, c0, cp)
-    T* colGt;   // [kE1X][3]  G^T coefficients
-    T* rowG;    // [kE1Y][3]
-    T* rowGt;   // [kE1Y][3]
-    T* colPw;   // [kE1X]     P weight wx (dtype)
-    T* rowPw;   // [kE1Y]
-    T* Wsm;     // [3][kE1]   W ring (planes p-2, p-1, p)
-    T* qx;      // [3][kE2]   q_x ring, zero-padded
-    T* qy;      // [3][kE2]
-    T* buf;     // [3][kE1]   completed deformation plane (z-reduced ghat)
-    T* Xr;      // [3][kE1Y][wx] x-reduced
-    T* xw;      // [2*kE1X]   CSR weights, window column d <- E1 columns
-    T* yw;      // [2*kE1Y]
-    int* colP0;  // [kE1X] P: def x0, x1
+    T* colG;    // [E1X][3]  G coefficients (cm, c0, cp)
+    T* colGt;   // [E1X][3]  G^T coefficients
+    T* rowG;    // [E1Y][3]
+    T* rowGt;   // [E1Y][3]
+    T* colPw;   // [E1X]     P weight wx (dtype)
+    T* rowPw;   // [E1Y]
+    T* Wsm;     // [3][E1]   W ring (planes p-2, p-1, p)
+    T* qx;      // [2][E2]   q_x of planes p-1 (written) and p-2 (read), zero-padded
+    T* qy;      // [2][E2]
+    T* buf;     // [3][E1]   completed deformation plane (z-reduced ghat)
+    T* Xr;      // [3][E1Y][wx] x-reduced
+    T* xw;      // [2*E1X]   CSR weights, window column d <- E1 columns
+    T* yw;      // [2*E1Y]
+    int* colP0;  // [E1X] P: def x0, x1
     int* colP1;
     int* rowP0;
     int* rowP1;
     int* xoff;  // [wx+1]
-    int* xcol;  // [2*kE1X]
+    int* xcol;  // [2*E1X]
     int* yoff;  // [wy+1]
-    int* yrow;  // [2*kE1Y]
-    double* red;  // [kThreads/32]
+    int* yrow;  // [2*E1Y]
+    double* red;  // [NT/32]
 };
 
 template <typename T>
@@ -91,74 +101,73 @@ __device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
     return q;
 }
 
-template <typename T>
-__host__ __device__ inline size_t fused_smem_bytes(int wx, int wy, int wz) {
+template <typename T, typename C>
+__host__ __device__ inline size_t smem_bytes_cfg(int wx, int wy) {
     auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
-    (void)wz;
     size_t s = 0;
-    s += al(kE1X * 3 * sizeof(T)) * 2 + al(kE1Y * 3 * sizeof(T)) * 2;
-    s += al(kE1X * sizeof(T)) + al(kE1Y * sizeof(T));
-    s += al(3 * kE1 * sizeof(T));
-    s += al(3 * kE2 * sizeof(T)) * 2;
-    s += al(3 * kE1 * sizeof(T));
-    s += al((size_t)3 * kE1Y * wx * sizeof(T));
-    s += al(2 * kE1X * sizeof(T)) + al(2 * kE1Y * sizeof(T));
-    s += al(kE1X * 4) * 2 + al(kE1Y * 4) * 2;
-    s += al((wx + 1) * 4) + al(2 * kE1X * 4) + al((wy + 1) * 4) + al(2 * kE1Y * 4);
-    s += al((kThreads / 32) * 8);
+    s += al(C::E1X * 3 * sizeof(T)) * 2 + al(C::E1Y * 3 * sizeof(T)) * 2;
+    s += al(C::E1X * sizeof(T)) + al(C::E1Y * sizeof(T));
+    s += al(3 * C::E1 * sizeof(T));
+    s += al(2 * C::E2 * sizeof(T)) * 2;
+    s += al(3 * C::E1 * sizeof(T));
+    s += al((size_t)3 * C::E1Y * wx * sizeof(T));
+    s += al(2 * C::E1X * sizeof(T)) + al(2 * C::E1Y * sizeof(T));
+    s += al(C::E1X * 4) * 2 + al(C::E1Y * 4) * 2;
+    s += al((wx + 1) * 4) + al(2 * C::E1X * 4) + al((wy + 1) * 4) + al(2 * C::E1Y * 4);
+    s += al((C::NT / 32) * 8);
     return s;
 }
 
-template <typename T>
+template <typename T, typename C>
 __device__ __forceinline__ Smem<T> carve_smem(unsigned char* base, int wx, int wy) {
     Smem<T> s;
     unsigned char* p = base;
-    s.colG = carve<T>(p, kE1X * 3);
-    s.colGt = carve<T>(p, kE1X * 3);
-    s.rowG = carve<T>(p, kE1Y * 3);
-    s.rowGt = carve<T>(p, kE1Y * 3);
-    s.colPw = carve<T>(p, kE1X);
-    s.rowPw = carve<T>(p, kE1Y);
-    s.Wsm = carve<T>(p, 3 * kE1);
-    s.qx = carve<T>(p, 3 * kE2);
-    s.qy = carve<T>(p, 3 * kE2);
-    s.buf = carve<T>(p, 3 * kE1);
-    s.Xr = carve<T>(p, (size_t)3 * kE1Y * wx);
-    s.xw = carve<T>(p, 2 * kE1X);
-    s.yw = carve<T>(p, 2 * kE1Y);
-    s.colP0 = carve<int>(p, kE1X);
-    s.colP1 = carve<int>(p, kE1X);
-    s.rowP0 = carve<int>(p, kE1Y);
-    s.rowP1 = carve<int>(p, kE1Y);
+    s.colG = carve<T>(p, C::E1X * 3);
+    s.colGt = carve<T>(p, C::E1X * 3);
+    s.rowG = carve<T>(p, C::E1Y * 3);
+    s.rowGt = carve<T>(p, C::E1Y * 3);
+    s.colPw = carve<T>(p, C::E1X);
+    s.rowPw = carve<T>(p, C::E1Y);
+    s.Wsm = carve<T>(p, 3 * C::E1);
+    s.qx = carve<T>(p, 2 * C::E2);
+    s.qy = carve<T>(p, 2 * C::E2);
+    s.buf = carve<T>(p, 3 * C::E1);
+    s.Xr = carve<T>(p, (size_t)3 * C::E1Y * wx);
+    s.xw = carve<T>(p, 2 * C::E1X);
+    s.yw = carve<T>(p, 2 * C::E1Y);
+    s.colP0 = carve<int>(p, C::E1X);
+    s.colP1 = carve<int>(p, C::E1X);
+    s.rowP0 = carve<int>(p, C::E1Y);
+    s.rowP1 = carve<int>(p, C::E1Y);
     s.xoff = carve<int>(p, wx + 1);
-    s.xcol = carve<int>(p, 2 * kE1X);
+    s.xcol = carve<int>(p, 2 * C::E1X);
     s.yoff = carve<int>(p, wy + 1);
-    s.yrow = carve<int>(p, 2 * kE1Y);
-    s.red = carve<double>(p, kThreads / 32);
+    s.yrow = carve<int>(p, 2 * C::E1Y);
+    s.red = carve<double>(p, C::NT / 32);
     return s;
 }
 
-// Per-thread march state.  Slot s owns E1 position P = tid + s * kThreads for all planes.
-template <typename T>
+// Per-thread march state.  Slot s owns E1 position P = tid + s * NT for all planes.
+template <typename T, typename C>
 struct March {
-    int P[kSlots];     // flat E1 index (-1: no position)
-    int P2[kSlots];    // index in the zero-padded q layout
-    int ij[kSlots];    // j * nx + i of the image column (RT / volume offset in a plane)
-    int exy[kSlots];   // ex | ey << 8
-    unsigned flags;    // bit s: inside the image in x/y; bit 8+s: tile interior
-    T ylo[kSlots][3], yhi[kSlots][3];   // P_xy y on the current def-plane pair
-    T dT[kSlots][3][3];                 // interpolant derivative / h, plane ring
-    T qz[kSlots][3];                    // q_z, plane ring
-    T A0[kSlots][3], A1[kSlots][3];     // z-accumulated ghat for def planes zd, zd+1
-    V4T<T> rt[kSlots];                  // prefetched reference terms (next B plane)
+    int P[C::S];     // flat E1 index (-1: no position)
+    int P2[C::S];    // index in the zero-padded q layout
+    unsigned ij[C::S];  // j * nx + i of the image column (offset inside a plane)
+    int exy[C::S];   // ex | ey << 8
+    unsigned flags;  // bit s: inside the image in x/y; bit 8+s: tile interior
+    T ylo[C::S][3], yhi[C::S][3];  // P_xy y on the current def-plane pair
+    T dT[C::S][3][3];              // interpolant derivative / h, plane ring
+    T qz[C::S][3];                 // q_z, plane ring
+    T A0[C::S][3], A1[C::S][3];    // z-accumulated ghat for def planes zd, zd+1
+    V4T<T> rt[C::S];               // prefetched reference terms (next B plane)
     int z0, z1, jfirst, jlast, wxlo, wylo, wzlo, cur_zd, cta;
     double dacc;
 };
 
-template <typename T>
-__device__ __forceinline__ bool slot_vol(const March<T>& m, int s) { return (m.flags >> s) & 1u; }
-template <typename T>
-__device__ __forceinline__ bool slot_e0(const March<T>& m, int s) { return (m.flags >> (8 + s)) & 1u; }
+template <typename T, typename C>
+__device__ __forceinline__ bool slot_vol(const March<T, C>& m, int s) { return (m.flags >> s) & 1u; }
+template <typename T, typename C>
+__device__ __forceinline__ bool slot_e0(const March<T, C>& m, int s) { return (m.flags >> (8 + s)) & 1u; }
 
 template <typename T>
 __device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const Smem<T>& sm, int exy, int zd,
@@ -168,12 +177,13 @@ __device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const Smem<T>
     const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
     const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
     const T wx = sm.colPw[ex], wy = sm.rowPw[ey];
-    const int64_t mm = (int64_t)a.ndx * a.ndy * a.ndz;
+    const unsigned mm = (unsigned)(a.ndx * a.ndy * a.ndz);
+    const unsigned plane = (unsigned)zd * (unsigned)(a.ndx * a.ndy);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const T* yc = a.y + k * mm + (int64_t)zd * a.ndx * a.ndy;
-        const T* r0 = yc + (int64_t)y0 * a.ndx;
-        const T* r1 = yc + (int64_t)y1 * a.ndx;
+        const T* yc = a.y + (k * mm + plane);
+        const T* r0 = yc + y0 * a.ndx;
+        const T* r1 = yc + y1 * a.ndx;
         const T X0 = lerp_exact(__ldg(r0 + x0), __ldg(r0 + x1), wx);
         const T X1 = lerp_exact(__ldg(r1 + x0), __ldg(r1 + x1), wx);
         out[k] = lerp_exact(X0, X1, wy);
@@ -182,38 +192,38 @@ __device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const Smem<T>
 
 // Reduce a completed deformation plane (z-accumulated ghat in `acc`) in x then y over
 // the tile's window and write it to the CTA's partial slot zs.
-template <typename T>
-__device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>& sm, March<T>& m,
-                                            T (&acc)[kSlots][3], int zs) {
+template <typename T, typename C>
+__device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>& sm, March<T, C>& m,
+                                            T (&acc)[C::S][3], int zs) {
     const int wx = a.fp.wx, wy = a.fp.wy;
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < C::S; ++s) {
         if (m.P[s] < 0) continue;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) sm.buf[c * kE1 + m.P[s]] = acc[s][c];
+        for (int c = 0; c < 3; ++c) sm.buf[c * C::E1 + m.P[s]] = acc[s][c];
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < kE1Y * wx; t += kThreads) {
+    for (int t = threadIdx.x; t < C::E1Y * wx; t += C::NT) {
         const int row = t / wx;
         const int d = t - row * wx;
         const int k0 = sm.xoff[d], k1 = sm.xoff[d + 1];
         T r0 = (T)0, r1 = (T)0, r2 = (T)0;
-        const T* b = sm.buf + row * kE1X;
+        const T* b = sm.buf + row * C::E1X;
         for (int k = k0; k < k1; ++k) {
             const int e = sm.xcol[k];
             const T w = sm.xw[k];
             r0 = fmaf_t(b[e], w, r0);
-            r1 = fmaf_t(b[kE1 + e], w, r1);
-            r2 = fmaf_t(b[2 * kE1 + e], w, r2);
+            r1 = fmaf_t(b[C::E1 + e], w, r1);
+            r2 = fmaf_t(b[2 * C::E1 + e], w, r2);
         }
-        sm.Xr[(0 * kE1Y + row) * wx + d] = r0;
-        sm.Xr[(1 * kE1Y + row) * wx + d] = r1;
-        sm.Xr[(2 * kE1Y + row) * wx + d] = r2;
+        sm.Xr[(0 * C::E1Y + row) * wx + d] = r0;
+        sm.Xr[(1 * C::E1Y + row) * wx + d] = r1;
+        sm.Xr[(2 * C::E1Y + row) * wx + d] = r2;
     }
     __syncthreads();
     const size_t win = (size_t)a.fp.wz * wy * wx;
     T* out = a.partial + (size_t)m.cta * 3 * win + (size_t)zs * wy * wx;
-    for (int t = threadIdx.x; t < wy * wx; t += kThreads) {
+    for (int t = threadIdx.x; t < wy * wx; t += C::NT) {
         const int dr = t / wx;
         const int d = t - dr * wx;
         const int k0 = sm.yoff[dr], k1 = sm.yoff[dr + 1];
@@ -221,9 +231,9 @@ __device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>
         for (int k = k0; k < k1; ++k) {
             const int row = sm.yrow[k];
             const T w = sm.yw[k];
-            r0 = fmaf_t(sm.Xr[(0 * kE1Y + row) * wx + d], w, r0);
-            r1 = fmaf_t(sm.Xr[(1 * kE1Y + row) * wx + d], w, r1);
-            r2 = fmaf_t(sm.Xr[(2 * kE1Y + row) * wx + d], w, r2);
+            r0 = fmaf_t(sm.Xr[(0 * C::E1Y + row) * wx + d], w, r0);
+            r1 = fmaf_t(sm.Xr[(1 * C::E1Y + row) * wx + d], w, r1);
+            r2 = fmaf_t(sm.Xr[(2 * C::E1Y + row) * wx + d], w, r2);
         }
         out[t] = r0;
         out[win + t] = r1;
@@ -231,11 +241,26 @@ __device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>
     }
 }
 
-template <int R, typename T>
-__device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>& sm, March<T>& m,
+// One axis of the template cell lookup (warp.py:38-53): t = (p - o) / h with the
+// reference's rounding, the hull test, the clamped lower corner and the fraction.
+template <typename T, bool POW2>
+__device__ __forceinline__ int cell_axis(T p, T o, T h, T ih, int n, bool& inside, T& f) {
+    const T d = sub_rn(p, o);
+    const T t = POW2 ? mul_rn(d, ih) : div_rn(d, h);
+    inside = inside && (t >= (T)0) && (t <= (T)(n - 1));
+    const T hi = (T)(n > 2 ? n - 2 : 0);
+    const T fl = fmin_t(fmax_t(floor(t), (T)0), hi);  // NaN -> 0
+    f = t - fl;  // exact for inside samples (Sterbenz); outside samples are masked
+    return (int)fl;
+}
+
+template <int R, typename T, typename C, bool POW2>
+__device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>& sm, March<T, C>& m,
                                            int p) {
     constexpr int RB = (R + 2) % 3;  // plane p-1
     constexpr int RC = (R + 1) % 3;  // plane p-2
+    constexpr int S = C::S;
+    const unsigned nxy = (unsigned)a.nx * (unsigned)a.ny;
 
     // ---------------------------------------------------------------- (A) plane p
     if (p >= 0 && p < a.nz && p <= m.z1) {
@@ -244,7 +269,7 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
             const int zd1 = min(zd + 1, a.ndz - 1);
             const bool shift = (zd == m.cur_zd + 1);
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s) {
+            for (int s = 0; s < S; ++s) {
                 if (!slot_vol(m, s)) continue;
                 if (shift) {
 #pragma unroll
@@ -257,70 +282,73 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
             m.cur_zd = zd;
         }
         const T wz = a.w1z[p];
-        // coordinates and corner addresses of all slots first, so the 8 * kSlots
-        // gathers are in flight together
-        const T* base[kSlots];
-        T fx[kSlots], fy[kSlots], fz[kSlots];
-        bool in[kSlots];
+        const T wz0 = sub_rn((T)1, wz);
+        // coordinates and corner offsets of all slots first, so the 8 * S gathers are
+        // in flight together
+        unsigned off[S];
+        T fx[S], fy[S], fz[S];
+        bool in[S];
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
-            T yh0 = lerp_exact(m.ylo[s][0], m.yhi[s][0], wz);
-            T yh1 = lerp_exact(m.ylo[s][1], m.yhi[s][1], wz);
-            T yh2 = lerp_exact(m.ylo[s][2], m.yhi[s][2], wz);
+        for (int s = 0; s < S; ++s) {
+            // yhat = Ylo * (1 - w) + Yhi * w, each op rounded (transfer.py:126)
+            const T yh0 = add_rn(mul_rn(m.ylo[s][0], wz0), mul_rn(m.yhi[s][0], wz));
+            const T yh1 = add_rn(mul_rn(m.ylo[s][1], wz0), mul_rn(m.yhi[s][1], wz));
+            const T yh2 = add_rn(mul_rn(m.ylo[s][2], wz0), mul_rn(m.yhi[s][2], wz));
             bool inside = slot_vol(m, s);
-            int ix, iy, iz;
-            axis_cell(tcoord(yh0, a.ox, a.hx, a.ihx, a.pow2x), a.nx, inside, ix, fx[s]);
-            axis_cell(tcoord(yh1, a.oy, a.hy, a.ihy, a.pow2y), a.ny, inside, iy, fy[s]);
-            axis_cell(tcoord(yh2, a.oz, a.hz, a.ihz, a.pow2z), a.nz, inside, iz, fz[s]);
+            const int ix = cell_axis<T, POW2>(yh0, a.ox, a.hx, a.ihx, a.nx, inside, fx[s]);
+            const int iy = cell_axis<T, POW2>(yh1, a.oy, a.hy, a.ihy, a.ny, inside, fy[s]);
+            const int iz = cell_axis<T, POW2>(yh2, a.oz, a.hz, a.ihz, a.nz, inside, fz[s]);
             in[s] = inside;
-            base[s] = a.Tv + ((int64_t)iz * a.ny + iy) * a.nx + ix;
+            off[s] = (unsigned)iz * nxy + (unsigned)iy * (unsigned)a.nx + (unsigned)ix;
         }
-        const int64_t sx = a.nx > 1 ? 1 : 0;
-        const int64_t sy = a.ny > 1 ? a.nx : 0;
-        const int64_t sz = a.nz > 1 ? (int64_t)a.nx * a.ny : 0;
-        T cv[kSlots][8];
+        const unsigned sx = a.nx > 1 ? 1u : 0u;
+        const unsigned sy = a.ny > 1 ? (unsigned)a.nx : 0u;
+        const unsigned sz = a.nz > 1 ? nxy : 0u;
+        T cv[S][8];
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
-            const T* b = base[s];
-            cv[s][0] = __ldg(b);
-            cv[s][1] = __ldg(b + sx);
-            cv[s][2] = __ldg(b + sy);
-            cv[s][3] = __ldg(b + sy + sx);
-            cv[s][4] = __ldg(b + sz);
-            cv[s][5] = __ldg(b + sz + sx);
-            cv[s][6] = __ldg(b + sz + sy);
-            cv[s][7] = __ldg(b + sz + sy + sx);
+        for (int s = 0; s < S; ++s) {
+            const unsigned o = off[s];
+            cv[s][0] = __ldg(a.Tv + o);
+            cv[s][1] = __ldg(a.Tv + (o + sx));
+            cv[s][2] = __ldg(a.Tv + (o + sy));
+            cv[s][3] = __ldg(a.Tv + (o + sy + sx));
+            cv[s][4] = __ldg(a.Tv + (o + sz));
+            cv[s][5] = __ldg(a.Tv + (o + sz + sx));
+            cv[s][6] = __ldg(a.Tv + (o + sz + sy));
+            cv[s][7] = __ldg(a.Tv + (o + sz + sy + sx));
         }
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
+        for (int s = 0; s < S; ++s) {
             T W, d0, d1, d2;
             trilinear(a, cv[s], fx[s], fy[s], fz[s], W, d0, d1, d2);
             if (!in[s]) W = d0 = d1 = d2 = (T)0;
             m.dT[s][R][0] = d0;
             m.dT[s][R][1] = d1;
             m.dT[s][R][2] = d2;
-            if (m.P[s] >= 0) sm.Wsm[R * kE1 + m.P[s]] = W;
+            if (m.P[s] >= 0) sm.Wsm[R * C::E1 + m.P[s]] = W;
         }
     } else {
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
+        for (int s = 0; s < S; ++s) {
             m.dT[s][R][0] = m.dT[s][R][1] = m.dT[s][R][2] = (T)0;
-            if (m.P[s] >= 0) sm.Wsm[R * kE1 + m.P[s]] = (T)0;
+            if (m.P[s] >= 0) sm.Wsm[R * C::E1 + m.P[s]] = (T)0;
         }
     }
     __syncthreads();
 
     // ---------------------------------------------------------------- (B) q on plane k = p-1
+    T* qxw = sm.qx + (p & 1) * C::E2;  // plane p-1 buffer; plane p-2 sits in the other one
+    T* qyw = sm.qy + (p & 1) * C::E2;
     {
         const int k = p - 1;
         const bool kv = (k >= m.z0) && (k < m.z1);
         T cmz, c0z, cpz;
         fd_coef<T>(k, a.nz, a.ihz, cmz, c0z, cpz);
-        const T* Wk = sm.Wsm + RB * kE1;
-        const T* Wm = sm.Wsm + RC * kE1;
-        const T* Wp = sm.Wsm + R * kE1;
+        const T* Wk = sm.Wsm + RB * C::E1;
+        const T* Wm = sm.Wsm + RC * C::E1;
+        const T* Wp = sm.Wsm + R * C::E1;
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s) {
+        for (int s = 0; s < S; ++s) {
             T qxv = (T)0, qyv = (T)0, qzv = (T)0;
             if (kv && slot_e0(m, s)) {
                 const int P = m.P[s];
@@ -328,21 +356,21 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
                 const T* cg = sm.colG + 3 * ex;
                 const T* rg = sm.rowG + 3 * ey;
                 const T gx = fmaf_t(cg[0], Wk[P - 1], fmaf_t(cg[1], Wk[P], cg[2] * Wk[P + 1]));
-                const T gy = fmaf_t(rg[0], Wk[P - kE1X], fmaf_t(rg[1], Wk[P], rg[2] * Wk[P + kE1X]));
+                const T gy = fmaf_t(rg[0], Wk[P - C::E1X], fmaf_t(rg[1], Wk[P], rg[2] * Wk[P + C::E1X]));
                 const T gz = fmaf_t(cmz, Wm[P], fmaf_t(c0z, Wk[P], cpz * Wp[P]));
                 ngf_q(a, gx, gy, gz, m.rt[s], qxv, qyv, qzv, m.dacc);
             }
             if (m.P[s] >= 0) {
-                sm.qx[RB * kE2 + m.P2[s]] = qxv;
-                sm.qy[RB * kE2 + m.P2[s]] = qyv;
+                qxw[m.P2[s]] = qxv;
+                qyw[m.P2[s]] = qyv;
             }
             m.qz[s][RB] = qzv;
         }
         // prefetch the reference terms of plane p for the next step's (B)
         if (p >= m.z0 && p < m.z1) {
-            const V4T<T>* rp = a.RT + (int64_t)p * a.nx * a.ny;
+            const V4T<T>* rp = a.RT + (size_t)p * nxy;
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s)
+            for (int s = 0; s < S; ++s)
                 if (slot_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
         }
     }
@@ -353,20 +381,20 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
     if (j < m.jfirst || j > m.jlast) return;  // uniform
     T gtm, gt0, gtp;
     fdt_coef<T>(j, a.nz, a.ihz, gtm, gt0, gtp);
-    const T* qxj = sm.qx + RC * kE2;
-    const T* qyj = sm.qy + RC * kE2;
+    const T* qxj = sm.qx + ((p & 1) ^ 1) * C::E2;
+    const T* qyj = sm.qy + ((p & 1) ^ 1) * C::E2;
     const int zdj = a.i0z[j];
     const T w1 = a.w1z[j];
     const T w0 = (T)1 - w1;
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
+    for (int s = 0; s < S; ++s) {
         if (!slot_vol(m, s)) continue;
         const int P2 = m.P2[s];
         const int ex = m.exy[s] & 0xff, ey = m.exy[s] >> 8;
         const T* ct = sm.colGt + 3 * ex;
         const T* rt = sm.rowGt + 3 * ey;
         T sv = fmaf_t(ct[0], qxj[P2 - 1], fmaf_t(ct[1], qxj[P2], ct[2] * qxj[P2 + 1]));
-        sv = fmaf_t(rt[0], qyj[P2 - kE2X], fmaf_t(rt[1], qyj[P2], fmaf_t(rt[2], qyj[P2 + kE2X], sv)));
+        sv = fmaf_t(rt[0], qyj[P2 - C::E2X], fmaf_t(rt[1], qyj[P2], fmaf_t(rt[2], qyj[P2 + C::E2X], sv)));
         sv = fmaf_t(gtm, m.qz[s][R], fmaf_t(gt0, m.qz[s][RC], fmaf_t(gtp, m.qz[s][RB], sv)));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -381,19 +409,19 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
     const bool last = (j == m.jlast);
     const int step = last ? 2 : a.i0z[j + 1] - zdj;
     if (step >= 1) {
-        flush_plane(a, sm, m, m.A0, zdj - m.wzlo);
+        flush_plane<T, C>(a, sm, m, m.A0, zdj - m.wzlo);
         if (step >= 2) {
             if (zdj + 1 <= a.ndz - 1) {
                 __syncthreads();
-                flush_plane(a, sm, m, m.A1, zdj + 1 - m.wzlo);
+                flush_plane<T, C>(a, sm, m, m.A1, zdj + 1 - m.wzlo);
             }
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s)
+            for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) m.A0[s][c] = m.A1[s][c] = (T)0;
         } else {
 #pragma unroll
-            for (int s = 0; s < kSlots; ++s)
+            for (int s = 0; s < S; ++s)
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
                     m.A0[s][c] = m.A1[s][c];
@@ -403,18 +431,19 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
     }
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
+template <typename T, typename C, bool POW2>
+__global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int S = C::S;
     const FusedPlan& fp = a.fp;
-    const Smem<T> sm = carve_smem<T>(smem_raw, fp.wx, fp.wy);
+    const Smem<T> sm = carve_smem<T, C>(smem_raw, fp.wx, fp.wy);
     const int tid = threadIdx.x;
-    March<T> m;
+    March<T, C> m;
     m.cta = blockIdx.x;
     const int tx = m.cta % fp.ntx;
     const int ty = (m.cta / fp.ntx) % fp.nty;
     const int tz = m.cta / (fp.ntx * fp.nty);
-    const int x0 = tx * kTX, y0 = ty * kTY;
+    const int x0 = tx * C::TX, y0 = ty * C::TY;
     m.z0 = tz * fp.cz;
     m.z1 = min(m.z0 + fp.cz, a.nz);
     m.jfirst = max(m.z0 - 1, 0);
@@ -426,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constan
     m.dacc = 0.0;
 
     // ---- per-CTA tables
-    for (int e = tid; e < kE1X; e += kThreads) {
+    for (int e = tid; e < C::E1X; e += C::NT) {
         const int i = x0 - 1 + e;
         T cm, c0, cp;
         fd_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
@@ -443,7 +472,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constan
         sm.colP1[e] = min(i0 + 1, a.ndx - 1);
         sm.colPw[e] = in ? a.w1x[i] : (T)0;
     }
-    for (int e = tid; e < kE1Y; e += kThreads) {
+    for (int e = tid; e < C::E1Y; e += C::NT) {
         const int jj = y0 - 1 + e;
         T cm, c0, cp;
         fd_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
@@ -460,54 +489,43 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constan
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : (T)0;
     }
-    for (int t = tid; t < 3 * kE2; t += kThreads) {
+    for (int t = tid; t < 2 * C::E2; t += C::NT) {
         sm.qx[t] = (T)0;
         sm.qy[t] = (T)0;
     }
-    if (tid == 0 || tid == 32) {
-        // CSR of the transposed 1-D interpolation over the tile window, ascending
-        // E1 index per window entry (the reference's gather order, transfer.py:89-96)
-        const bool isx = tid == 0;
-        const int ne = isx ? kE1X : kE1Y, w = isx ? fp.wx : fp.wy, org = isx ? x0 : y0;
-        const int n = isx ? a.nx : a.ny, nd = isx ? a.ndx : a.ndy, lo = isx ? m.wxlo : m.wylo;
-        const int32_t* i0a = isx ? a.i0x : a.i0y;
-        const T* w1a = isx ? a.w1x : a.w1y;
-        int* off = isx ? sm.xoff : sm.yoff;
-        int* idx = isx ? sm.xcol : sm.yrow;
-        T* wt = isx ? sm.xw : sm.yw;
-        int cnt = 0;
-        for (int d = 0; d < w; ++d) {
-            off[d] = cnt;
-            for (int e = 0; e < ne; ++e) {
-                const int i = org - 1 + e;
-                if (i < 0 || i >= n) continue;
-                const int dl = i0a[i] - lo;
-                const T w1 = w1a[i];
-                if (dl == d) {
-                    idx[cnt] = e;
-                    wt[cnt++] = (T)1 - w1;
-                } else if (dl == d - 1 && nd > 1) {
-                    idx[cnt] = e;
-                    wt[cnt++] = w1;
-                }
-            }
+    {
+        // this tile's CSR of the transposed 1-D interpolation (host-built, ascending E1
+        // index per window entry: the reference's gather order, transfer.py:89-96)
+        const int sx = fp.wx + 1 + 2 * C::E1X, sy = fp.wy + 1 + 2 * C::E1Y;
+        const int32_t* gx = fp.xcsr + (size_t)tx * sx;
+        const int32_t* gy = fp.ycsr + (size_t)ty * sy;
+        const T* wxg = (const T*)fp.xcw + (size_t)tx * 2 * C::E1X;
+        const T* wyg = (const T*)fp.ycw + (size_t)ty * 2 * C::E1Y;
+        for (int t = tid; t < fp.wx + 1; t += C::NT) sm.xoff[t] = gx[t];
+        for (int t = tid; t < 2 * C::E1X; t += C::NT) {
+            sm.xcol[t] = gx[fp.wx + 1 + t];
+            sm.xw[t] = wxg[t];
         }
-        off[w] = cnt;
+        for (int t = tid; t < fp.wy + 1; t += C::NT) sm.yoff[t] = gy[t];
+        for (int t = tid; t < 2 * C::E1Y; t += C::NT) {
+            sm.yrow[t] = gy[fp.wy + 1 + t];
+            sm.yw[t] = wyg[t];
+        }
     }
 
     // ---- slot positions (fixed for all planes)
     m.flags = 0u;
 #pragma unroll
-    for (int s = 0; s < kSlots; ++s) {
-        const int P = tid + s * kThreads;
-        const bool ok = P < kE1;
-        const int ex = ok ? P % kE1X : 0, ey = ok ? P / kE1X : 0;
+    for (int s = 0; s < S; ++s) {
+        const int P = tid + s * C::NT;
+        const bool ok = P < C::E1;
+        const int ex = ok ? P % C::E1X : 0, ey = ok ? P / C::E1X : 0;
         const int i = x0 - 1 + ex, jj = y0 - 1 + ey;
         const bool vol = ok && i >= 0 && i < a.nx && jj >= 0 && jj < a.ny;
-        const bool e0 = vol && ex >= 1 && ex <= kTX && ey >= 1 && ey <= kTY;
+        const bool e0 = vol && ex >= 1 && ex <= C::TX && ey >= 1 && ey <= C::TY;
         m.P[s] = ok ? P : -1;
-        m.P2[s] = (ey + 1) * kE2X + ex + 1;
-        m.ij[s] = vol ? jj * a.nx + i : 0;
+        m.P2[s] = (ey + 1) * C::E2X + ex + 1;
+        m.ij[s] = vol ? (unsigned)(jj * a.nx + i) : 0u;
         m.exy[s] = ex | (ey << 8);
         m.flags |= (vol ? 1u : 0u) << s;
         m.flags |= (e0 ? 1u : 0u) << (8 + s);
@@ -526,9 +544,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constan
     __syncthreads();
     // reference terms of the first interior plane
     if (m.z0 < m.z1) {
-        const V4T<T>* rp = a.RT + (int64_t)m.z0 * a.nx * a.ny;
+        const V4T<T>* rp = a.RT + (size_t)m.z0 * a.nx * a.ny;
 #pragma unroll
-        for (int s = 0; s < kSlots; ++s)
+        for (int s = 0; s < S; ++s)
             if (slot_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
     }
 
@@ -536,9 +554,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constan
     const int pstart = m.z0 - 1;
     const int nsteps = (m.z1 + 2) - pstart + 1;
     for (int b = 0; b < nsteps; b += 3) {
-        fused_step<0>(a, sm, m, pstart + b);
-        if (b + 1 < nsteps) fused_step<1>(a, sm, m, pstart + b + 1);
-        if (b + 2 < nsteps) fused_step<2>(a, sm, m, pstart + b + 2);
+        fused_step<0, T, C, POW2>(a, sm, m, pstart + b);
+        if (b + 1 < nsteps) fused_step<1, T, C, POW2>(a, sm, m, pstart + b + 1);
+        if (b + 2 < nsteps) fused_step<2, T, C, POW2>(a, sm, m, pstart + b + 2);
     }
 
     // ---- the CTA's D partial
@@ -549,7 +567,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_eval_fused(const __grid_constan
     __syncthreads();
     if (tid == 0) {
         double sacc = 0.0;
-        for (int w = 0; w < kThreads / 32; ++w) sacc += sm.red[w];
+        for (int w = 0; w < C::NT / 32; ++w) sacc += sm.red[w];
         a.dpart[m.cta] = sacc;
     }
 }
@@ -685,6 +703,96 @@ __global__ void k_finalize(const double* __restrict__ dpart, int nd, const doubl
 
 // ------------------------------------------------------------------ host launchers
 
+// Kernel variants: tile rows TY, threads per CTA, minimum resident CTAs per SM.
+using V0 = Cfg<20, 256, 2>;
+using V1 = Cfg<12, 256, 2>;
+using V2 = Cfg<12, 256, 3>;
+using V3 = Cfg<28, 512, 1>;
+using V4 = Cfg<12, 512, 2>;
+using V5 = Cfg<20, 256, 1>;
+constexpr int kNumVariants = 6;
+
+void fused_variant_geom(int v, int* ty, int* nt) {
+    switch (v) {
+        case 1: *ty = V1::TY; *nt = V1::NT; return;
+        case 2: *ty = V2::TY; *nt = V2::NT; return;
+        case 3: *ty = V3::TY; *nt = V3::NT; return;
+        case 4: *ty = V4::TY; *nt = V4::NT; return;
+        case 5: *ty = V5::TY; *nt = V5::NT; return;
+        default: *ty = V0::TY; *nt = V0::NT; return;
+    }
+}
+
+int fused_variant_count() { return kNumVariants; }
+
+template <typename T>
+size_t fused_smem(int v, int wx, int wy) {
+    switch (v) {
+        case 1: return smem_bytes_cfg<T, V1>(wx, wy);
+        case 2: return smem_bytes_cfg<T, V2>(wx, wy);
+        case 3: return smem_bytes_cfg<T, V3>(wx, wy);
+        case 4: return smem_bytes_cfg<T, V4>(wx, wy);
+        case 5: return smem_bytes_cfg<T, V5>(wx, wy);
+        default: return smem_bytes_cfg<T, V0>(wx, wy);
+    }
+}
+
+template <typename T, typename C>
+static int prep(size_t smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_eval_fused<T, C, true>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_eval_fused<T, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem);
+    return (int)e;
+}
+
+template <typename T, typename C>
+static void launch(const FusedArgs<T>& a, cudaStream_t s) {
+    if (a.pow2x && a.pow2y && a.pow2z)
+        NGF_LAUNCH((k_eval_fused<T, C, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+    else
+        NGF_LAUNCH((k_eval_fused<T, C, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+}
+
+template <>
+int fused_prepare<float>(int v, size_t smem) {
+    switch (v) {
+        case 1: return prep<float, V1>(smem);
+        case 2: return prep<float, V2>(smem);
+        case 3: return prep<float, V3>(smem);
+        case 4: return prep<float, V4>(smem);
+        case 5: return prep<float, V5>(smem);
+        default: return prep<float, V0>(smem);
+    }
+}
+
+template <>
+int fused_prepare<double>(int v, size_t smem) {
+    (void)v;
+    return prep<double, V0>(smem);  // one f64 variant
+}
+
+template <typename T>
+static void launch_variant(const FusedArgs<T>& a, cudaStream_t s);
+
+template <>
+void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
+    switch (a.fp.variant) {
+        case 1: launch<float, V1>(a, s); return;
+        case 2: launch<float, V2>(a, s); return;
+        case 3: launch<float, V3>(a, s); return;
+        case 4: launch<float, V4>(a, s); return;
+        case 5: launch<float, V5>(a, s); return;
+        default: launch<float, V0>(a, s); return;
+    }
+}
+
+template <>
+void launch_variant<double>(const FusedArgs<double>& a, cudaStream_t s) {
+    launch<double, V0>(a, s);
+}
+
 template <typename T>
 int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, T* L, double* spart,
                       int ns, int* flag, T* grad, double* scalars, cudaStream_t s,
@@ -693,7 +801,7 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
     const int64_t m = grid_n(dg);
     NGF_LAUNCH(k_curv_L<T>, ns, 256, 0, s, gk, a.y, L, spart, flag);
     if (ev0) cudaEventRecord(ev0, s);
-    NGF_LAUNCH(k_eval_fused<T>, a.fp.n_cta, kThreads, a.fp.smem_bytes, s, a);
+    launch_variant<T>(a, s);
     if (ev1) cudaEventRecord(ev1, s);
     const double vol = dg.spacing[0] * dg.spacing[1] * dg.spacing[2];
     NGF_LAUNCH(k_reduce<T>, blocks_for(3 * m, 256), 256, 0, s, gk, a.fp, a.partial, L, (T)vol,
@@ -702,18 +810,6 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
                alpha, flag, scalars);
     NGF_CHECK_LAUNCH();
     return 0;
-}
-
-template <typename T>
-int fused_prepare(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_fused<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    return (int)e;
-}
-
-template <typename T>
-size_t fused_smem(int wx, int wy, int wz) {
-    return fused_smem_bytes<T>(wx, wy, wz);
 }
 
 // packed reference terms (gR / nR, 1 / nR) from the exact ones
@@ -739,14 +835,13 @@ int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s) {
     return 0;
 }
 
+
 template int fused_eval_launch<float>(const FusedArgs<float>&, const ngf_grid_t&, double, float*,
                                       double*, int, int*, float*, double*, cudaStream_t,
                                       cudaEvent_t, cudaEvent_t);
 template int fused_eval_launch<double>(const FusedArgs<double>&, const ngf_grid_t&, double, double*,
                                        double*, int, int*, double*, double*, cudaStream_t,
                                        cudaEvent_t, cudaEvent_t);
-template int fused_prepare<float>(size_t);
-template int fused_prepare<double>(size_t);
 template size_t fused_smem<float>(int, int, int);
 template size_t fused_smem<double>(int, int, int);
 template int pack_rt<float>(const float*, const float*, int64_t, void*, cudaStream_t);

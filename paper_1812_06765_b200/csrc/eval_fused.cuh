@@ -4,21 +4,13 @@
 
 namespace ngf {
 
-// Tile geometry of the fused kernel: TX x TY image voxels per CTA in x/y, a ring
-// of one voxel around it (E1 = (TX+2) x (TY+2)), marching CZ planes in z.
+// Tile geometry of the fused kernel: kTX x TY image voxels per CTA in x/y (TY per
+// kernel variant), a ring of one voxel around it, marching cz planes in z.
 constexpr int kTX = 32;
-constexpr int kTY = 20;
-constexpr int kE1X = kTX + 2;              // 34
-constexpr int kE1Y = kTY + 2;              // 22
-constexpr int kE1 = kE1X * kE1Y;           // 748
-constexpr int kThreads = 256;
-constexpr int kSlots = (kE1 + kThreads - 1) / kThreads;  // 3
-constexpr int kE2X = kTX + 4;              // padded q layout (36)
-constexpr int kE2Y = kTY + 4;              // 24
-constexpr int kE2 = kE2X * kE2Y;           // 864
 
 struct FusedPlan {
-    // tiles
+    // kernel variant (tile rows, threads per CTA, occupancy) and tiles
+    int variant, ty, nthreads;
     int ntx, nty, ntz, cz;
     // P^T windows: max sizes and per-tile lower def index (device arrays)
     int wx, wy, wz;
@@ -29,6 +21,12 @@ struct FusedPlan {
     const int32_t* cov_x;  // [ndx * kCover * 2]
     const int32_t* cov_y;
     const int32_t* cov_z;
+    // per-tile CSR of the transposed 1-D interpolation over the tile window (host-built):
+    // x tile t: offsets [wx+1] then E1 column indices [2*(kTX+2)]; weights separately
+    const int32_t* xcsr;  // [ntx][wx + 1 + 2*(kTX+2)]
+    const int32_t* ycsr;  // [nty][wy + 1 + 2*(ty+2)]
+    const void* xcw;      // [ntx][2*(kTX+2)] dtype weights
+    const void* ycw;      // [nty][2*(ty+2)]
     int n_cta;
     size_t smem_bytes;
 };

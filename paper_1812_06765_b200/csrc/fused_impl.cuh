@@ -45,6 +45,12 @@ __device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, 
 __device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
 __device__ __forceinline__ float div_rn(float a, float b) { return __fdiv_rn(a, b); }
 __device__ __forceinline__ double div_rn(double a, double b) { return __ddiv_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float fmin_t(float a, float b) { return fminf(a, b); }
+__device__ __forceinline__ double fmin_t(double a, double b) { return fmin(a, b); }
+__device__ __forceinline__ float fmax_t(float a, float b) { return fmaxf(a, b); }
+__device__ __forceinline__ double fmax_t(double a, double b) { return fmax(a, b); }
 __device__ __forceinline__ float fmaf_t(float a, float b, float c) { return fmaf(a, b, c); }
 __device__ __forceinline__ double fmaf_t(double a, double b, double c) { return fma(a, b, c); }
 __device__ __forceinline__ float rsqrt_t(float x) { return rsqrtf(x); }
@@ -159,8 +165,10 @@ template <typename T>
 int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, T* L, double* spart,
                       int ns, int* flag, T* grad, double* scalars, cudaStream_t s,
                       cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr);
-template <typename T> int fused_prepare(size_t smem);
-template <typename T> size_t fused_smem(int wx, int wy, int wz);
+template <typename T> int fused_prepare(int variant, size_t smem);
+template <typename T> size_t fused_smem(int variant, int wx, int wy);
+void fused_variant_geom(int variant, int* ty, int* nthreads);
+int fused_variant_count();
 template <typename T> int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s);
 
 }  // namespace ngf

@@ -1,5 +1,6 @@
 // Level objective: reference terms, fused/exact evaluation (objective.py:22-60).
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -103,55 +104,103 @@ static int fused_setup(ngf_level* L) {
     const int ndx = (int)L->def.dims[0], ndy = (int)L->def.dims[1], ndz = (int)L->def.dims[2];
     std::vector<int> xl, xh, yl, yh, zl, zh;
     FusedPlan& fp = L->fp;
+    // kernel variant (f32: several tile/occupancy shapes; f64: one)
+    int variant = 2;  // 32x12 tiles, 256 threads, 3 CTAs/SM: fastest at 256^3 (tools/sweep.py)
+    if (const char* env = std::getenv("NGF_FUSED_VARIANT"))
+        variant = std::atoi(env) % fused_variant_count();
+    if (sizeof(T) == 8) variant = 0;
+    static const int kMinBlocks[] = {2, 2, 3, 1, 2, 1};
+    fp.variant = variant;
+    fused_variant_geom(variant, &fp.ty, &fp.nthreads);
     fp.wx = tile_windows(p->h_i0[0], nx, ndx, kTX, 1, xl, xh);
-    fp.wy = tile_windows(p->h_i0[1], ny, ndy, kTY, 1, yl, yh);
+    fp.wy = tile_windows(p->h_i0[1], ny, ndy, fp.ty, 1, yl, yh);
     fp.ntx = (int)xl.size();
     fp.nty = (int)yl.size();
-    // z chunk: as long as possible (less z-ring recompute) while keeping >= 2 CTAs per SM
-    // busy; every candidate must fit shared memory and keep each def node covered by at
-    // most kCover chunks (the reduce kernel's fixed-order sum)
-    auto valid = [&](int c, size_t limit) {
+    fp.smem_bytes = fused_smem<T>(variant, fp.wx, fp.wy);
+    if (fp.smem_bytes > size_t(220) * 1024) return NGF_EARG;
+    // z chunk: every candidate must keep each def node covered by at most kCover chunks
+    // (the reduce kernel's fixed-order sum).  Among those, minimise the modelled time
+    // (waves of resident CTAs) x (planes marched per CTA, incl. the ring and pipeline).
+    auto valid = [&](int c) {
         std::vector<int> a, b;
-        int wz = tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b);
-        if (fused_smem<T>(fp.wx, fp.wy, wz) > limit) return false;
+        tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b);
         std::vector<int32_t> cov;
         return build_cover(a, b, ndz, cov);
     };
+    const int64_t resident = (int64_t)kSMs * kMinBlocks[variant];
     int cz = 0;
-    for (size_t limit : {size_t(100) * 1024, size_t(220) * 1024}) {
-        int best_par = 0, best_any = 0;
-        for (int c = 64; c >= 1; c /= 2) {
-            if (!valid(c, limit)) continue;
-            if (!best_par && (int64_t)fp.ntx * fp.nty * ((nz + c - 1) / c) >= 2 * kSMs) best_par = c;
-            best_any = c;  // smallest valid chunk = most CTAs
+    double best = 1e300;
+    for (int c = std::min(nz, 96); c >= 1; --c) {
+        const int64_t nct = (int64_t)fp.ntx * fp.nty * ((nz + c - 1) / c);
+        const double waves = (double)((nct + resident - 1) / resident);
+        const double cost = waves * (c + 10);  // ~10 planes of per-CTA fixed cost (measured)
+        if (cost < best * 0.999 && valid(c)) {
+            best = cost;
+            cz = c;
         }
-        cz = best_par ? best_par : best_any;
-        if (cz) break;
     }
     if (!cz) return NGF_EARG;
     if (const char* env = std::getenv("NGF_FUSED_CZ")) {  // tuning / debugging override
         const int forced = std::atoi(env);
-        if (forced > 0 && valid(forced, size_t(220) * 1024)) cz = forced;
+        if (forced > 0 && valid(forced)) cz = forced;
     }
     fp.cz = cz;
     fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh);
     fp.ntz = (int)zl.size();
     fp.n_cta = fp.ntx * fp.nty * fp.ntz;
-    fp.smem_bytes = fused_smem<T>(fp.wx, fp.wy, fp.wz);
     std::vector<int32_t> cx, cy, cz_;
     if (!build_cover(xl, xh, ndx, cx) || !build_cover(yl, yh, ndy, cy) ||
         !build_cover(zl, zh, ndz, cz_))
         return NGF_EARG;
+    // per-tile CSR of the transposed 1-D interpolation over the tile window
+    // (transfer.py:82-101 restricted to the tile's columns incl. its ring)
+    auto build_csr = [&](int axis, int tile, int ntile, int w, const std::vector<int>& lo,
+                         std::vector<int32_t>& csr, std::vector<T>& wts) {
+        const int ne = tile + 2, n = p->n_img[axis], nd = p->n_def[axis];
+        const int stride = w + 1 + 2 * ne;
+        csr.assign((size_t)ntile * stride, 0);
+        wts.assign((size_t)ntile * 2 * ne, (T)0);
+        for (int t = 0; t < ntile; ++t) {
+            int32_t* off = csr.data() + (size_t)t * stride;
+            int32_t* idx = off + w + 1;
+            T* wt = wts.data() + (size_t)t * 2 * ne;
+            int cnt = 0;
+            for (int d = 0; d < w; ++d) {
+                off[d] = cnt;
+                for (int e = 0; e < ne; ++e) {
+                    const int i = t * tile - 1 + e;
+                    if (i < 0 || i >= n) continue;
+                    const int dl = p->h_i0[axis][i] - lo[t];
+                    const double w1 = p->h_w1[axis][i];
+                    if (dl == d) {
+                        idx[cnt] = e;
+                        wt[cnt++] = (T)(1.0 - w1);
+                    } else if (dl == d - 1 && nd > 1) {
+                        idx[cnt] = e;
+                        wt[cnt++] = (T)w1;
+                    }
+                }
+            }
+            off[w] = cnt;
+        }
+    };
+    std::vector<int32_t> xcsr, ycsr;
+    std::vector<T> xcw, ycw;
+    build_csr(0, kTX, fp.ntx, fp.wx, xl, xcsr, xcw);
+    build_csr(1, fp.ty, fp.nty, fp.wy, yl, ycsr, ycw);
     std::vector<int32_t> blob;
-    auto app = [&](const std::vector<int32_t>& v) {
+    auto app = [&](const void* v, size_t bytes) {
         size_t off = blob.size();
-        blob.insert(blob.end(), v.begin(), v.end());
+        blob.resize(off + (bytes + 3) / 4);
+        std::memcpy(blob.data() + off, v, bytes);
         while (blob.size() % 64) blob.push_back(0);
         return off;
     };
     std::vector<int32_t> wxv(xl.begin(), xl.end()), wyv(yl.begin(), yl.end()), wzv(zl.begin(), zl.end());
-    size_t o_wx = app(wxv), o_wy = app(wyv), o_wz = app(wzv), o_cx = app(cx), o_cy = app(cy),
-           o_cz = app(cz_);
+    auto appv = [&](const std::vector<int32_t>& v) { return app(v.data(), v.size() * 4); };
+    size_t o_wx = appv(wxv), o_wy = appv(wyv), o_wz = appv(wzv), o_cx = appv(cx), o_cy = appv(cy),
+           o_cz = appv(cz_), o_xcsr = appv(xcsr), o_ycsr = appv(ycsr),
+           o_xcw = app(xcw.data(), xcw.size() * sizeof(T)), o_ycw = app(ycw.data(), ycw.size() * sizeof(T));
     NGF_CUDA(cudaMalloc(&L->fp_blob, blob.size() * 4));
     NGF_CUDA(cudaMemcpy(L->fp_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice));
     const int32_t* b = (const int32_t*)L->fp_blob;
@@ -161,12 +210,16 @@ static int fused_setup(ngf_level* L) {
     fp.cov_x = b + o_cx;
     fp.cov_y = b + o_cy;
     fp.cov_z = b + o_cz;
+    fp.xcsr = b + o_xcsr;
+    fp.ycsr = b + o_ycsr;
+    fp.xcw = b + o_xcw;
+    fp.ycw = b + o_ycw;
     const size_t win = (size_t)fp.wz * fp.wy * fp.wx;
     NGF_CUDA(cudaMalloc(&L->partial, (size_t)fp.n_cta * 3 * win * sizeof(T)));
     NGF_CUDA(cudaMalloc(&L->dpart, (size_t)fp.n_cta * sizeof(double)));
     NGF_CUDA(cudaMalloc(&L->spart, (size_t)kCurvBlocks * sizeof(double)));
     NGF_CUDA(cudaMalloc(&L->L, (size_t)3 * grid_n(L->def) * sizeof(T)));
-    return fused_prepare<T>(fp.smem_bytes);
+    return fused_prepare<T>(variant, fp.smem_bytes);
 }
 
 template <typename T>
