@@ -17,6 +17,11 @@
 // yhat, W, grad W, q, s and ghat never leave the SM.  G^T and P^T are linear, so
 // ring voxels carry only this tile's contributions; k_reduce adds the tiles that
 // share a deformation node in a fixed order (deterministic, no atomics).
+//
+// Shared memory has a compile-time layout (SmemL) so every access is one LDS/STS
+// with an immediate offset from a per-slot register; x/y differences are plain
+// central differences except for the few slots next to a volume face, which use
+// the exact one-sided coefficients (warp.py:139-142, :168-175).
 
 #include <cstdlib>
 #include <vector>
@@ -27,6 +32,8 @@
 
 namespace ngf {
 
+constexpr int kCzMax = 96;  // longest z chunk a CTA marches
+
 // Tile / launch configuration of one kernel variant.
 template <int TY_, int NT_, int MINB_>
 struct Cfg {
@@ -34,10 +41,11 @@ struct Cfg {
     static constexpr int E1X = TX + 2, E1Y = TY + 2, E1 = E1X * E1Y;
     static constexpr int S = (E1 + NT - 1) / NT;
     static constexpr int E2X = TX + 4, E2Y = TY + 4, E2 = E2X * E2Y;
+    static constexpr int WXMAX = E1X + 1, WYMAX = E1Y + 1;  // P^T window bounds
 };
 
 template <typename T>
-__device__ __forceinline__ void fd_coef(int i, int n, T ih, T& cm, T& c0, T& cp) {
+__host__ __device__ __forceinline__ void fd_coef(int i, int n, T ih, T& cm, T& c0, T& cp) {
     // derivative at index i as cm*v[i-1] + c0*v[i] + cp*v[i+1] (warp.py:130-143)
     cm = (T)0;
     c0 = (T)0;
@@ -57,7 +65,7 @@ __device__ __forceinline__ void fd_coef(int i, int n, T ih, T& cm, T& c0, T& cp)
 
 // transpose coefficients at index i: multiply q[i-1], q[i], q[i+1]
 template <typename T>
-__device__ __forceinline__ void fdt_coef(int i, int n, T ih, T& gm, T& g0, T& gp) {
+__host__ __device__ __forceinline__ void fdt_coef(int i, int n, T ih, T& gm, T& g0, T& gp) {
     T a, b, c;
     fd_coef<T>(i - 1, n, ih, a, b, c);
     gm = c;
@@ -67,113 +75,59 @@ __device__ __forceinline__ void fdt_coef(int i, int n, T ih, T& gm, T& g0, T& gp
     gp = a;
 }
 
-template <typename T>
-struct Smem {
-    T* colG;    // [E1X][3]  G coefficients (cm, c0, cp)
-    T* colGt;   // [E1X][3]  G^T coefficients
-    T* rowG;    // [E1Y][3]
-    T* rowGt;   // [E1Y][3]
-    T* colPw;   // [E1X]     P weight wx (dtype)
-    T* rowPw;   // [E1Y]
-    T* Wsm;     // [3][E1]   W ring (planes p-2, p-1, p)
-    T* qx;      // [2][E2]   q_x of planes p-1 (written) and p-2 (read), zero-padded
-    T* qy;      // [2][E2]
-    T* buf;     // [3][E1]   completed deformation plane (z-reduced ghat)
-    T* Xr;      // [3][E1Y][wx] x-reduced
-    T* xw;      // [2*E1X]   CSR weights, window column d <- E1 columns
-    T* yw;      // [2*E1Y]
-    int* colP0;  // [E1X] P: def x0, x1
-    int* colP1;
-    int* rowP0;
-    int* rowP1;
-    int* xoff;  // [wx+1]
-    int* xcol;  // [2*E1X]
-    int* yoff;  // [wy+1]
-    int* yrow;  // [2*E1Y]
-    double* red;  // [NT/32]
+// Compile-time shared memory layout.
+template <typename T, typename C>
+struct SmemL {
+    T Wsm[3][C::E1 + 1];        // W ring (planes p-2, p-1, p); [E1] = padding-slot sink
+    T qx[2][C::E2], qy[2][C::E2];  // q_x, q_y of planes p-1 (written) / p-2 (read), zero-padded
+    T buf[3][C::E1 + 1];        // completed deformation plane (z-reduced ghat)
+    T Xr[3][C::E1Y][C::WXMAX];  // x-reduced
+    T colG[C::E1X][3], colGt[C::E1X][3], rowG[C::E1Y][3], rowGt[C::E1Y][3];  // face coefficients
+    T colPw[C::E1X], rowPw[C::E1Y];  // P weights
+    T xw[2 * C::E1X], yw[2 * C::E1Y];  // CSR weights
+    T zt[kCzMax + 4][8];        // per plane: G (cm,c0,cp), G^T (gm,g0,gp), w1z, 1-w1z
+    int zi[kCzMax + 4][2];      // per plane: i0z, advance of i0z to the next plane
+    int colP0[C::E1X], colP1[C::E1X], rowP0[C::E1Y], rowP1[C::E1Y];
+    int xoff[C::WXMAX + 1], xcol[2 * C::E1X], yoff[C::WYMAX + 1], yrow[2 * C::E1Y];
+    double red[C::NT / 32];
 };
-
-template <typename T>
-__device__ __forceinline__ T* carve(unsigned char*& p, size_t count) {
-    size_t bytes = (count * sizeof(T) + 15) & ~size_t(15);
-    T* q = reinterpret_cast<T*>(p);
-    p += bytes;
-    return q;
-}
 
 template <typename T, typename C>
 __host__ __device__ inline size_t smem_bytes_cfg(int wx, int wy) {
-    auto al = [](size_t b) { return (b + 15) & ~size_t(15); };
-    size_t s = 0;
-    s += al(C::E1X * 3 * sizeof(T)) * 2 + al(C::E1Y * 3 * sizeof(T)) * 2;
-    s += al(C::E1X * sizeof(T)) + al(C::E1Y * sizeof(T));
-    s += al(3 * C::E1 * sizeof(T));
-    s += al(2 * C::E2 * sizeof(T)) * 2;
-    s += al(3 * C::E1 * sizeof(T));
-    s += al((size_t)3 * C::E1Y * wx * sizeof(T));
-    s += al(2 * C::E1X * sizeof(T)) + al(2 * C::E1Y * sizeof(T));
-    s += al(C::E1X * 4) * 2 + al(C::E1Y * 4) * 2;
-    s += al((wx + 1) * 4) + al(2 * C::E1X * 4) + al((wy + 1) * 4) + al(2 * C::E1Y * 4);
-    s += al((C::NT / 32) * 8);
-    return s;
-}
-
-template <typename T, typename C>
-__device__ __forceinline__ Smem<T> carve_smem(unsigned char* base, int wx, int wy) {
-    Smem<T> s;
-    unsigned char* p = base;
-    s.colG = carve<T>(p, C::E1X * 3);
-    s.colGt = carve<T>(p, C::E1X * 3);
-    s.rowG = carve<T>(p, C::E1Y * 3);
-    s.rowGt = carve<T>(p, C::E1Y * 3);
-    s.colPw = carve<T>(p, C::E1X);
-    s.rowPw = carve<T>(p, C::E1Y);
-    s.Wsm = carve<T>(p, 3 * C::E1);
-    s.qx = carve<T>(p, 2 * C::E2);
-    s.qy = carve<T>(p, 2 * C::E2);
-    s.buf = carve<T>(p, 3 * C::E1);
-    s.Xr = carve<T>(p, (size_t)3 * C::E1Y * wx);
-    s.xw = carve<T>(p, 2 * C::E1X);
-    s.yw = carve<T>(p, 2 * C::E1Y);
-    s.colP0 = carve<int>(p, C::E1X);
-    s.colP1 = carve<int>(p, C::E1X);
-    s.rowP0 = carve<int>(p, C::E1Y);
-    s.rowP1 = carve<int>(p, C::E1Y);
-    s.xoff = carve<int>(p, wx + 1);
-    s.xcol = carve<int>(p, 2 * C::E1X);
-    s.yoff = carve<int>(p, wy + 1);
-    s.yrow = carve<int>(p, 2 * C::E1Y);
-    s.red = carve<double>(p, C::NT / 32);
-    return s;
+    if (wx > C::WXMAX || wy > C::WYMAX) return size_t(1) << 30;  // cannot happen for valid plans
+    return sizeof(SmemL<T, C>);
 }
 
 // Per-thread march state.  Slot s owns E1 position P = tid + s * NT for all planes.
 template <typename T, typename C>
 struct March {
-    int P[C::S];     // flat E1 index (-1: no position)
-    int P2[C::S];    // index in the zero-padded q layout
+    int P[C::S];        // flat E1 index (E1 = sink for padding slots)
+    int P2[C::S];       // index in the zero-padded q layout
     unsigned ij[C::S];  // j * nx + i of the image column (offset inside a plane)
-    int exy[C::S];   // ex | ey << 8
-    unsigned flags;  // bit s: inside the image in x/y; bit 8+s: tile interior
+    unsigned flags;     // per slot s, bits 4s..4s+3: in volume (x/y), tile interior, x face, y face
     T ylo[C::S][3], yhi[C::S][3];  // P_xy y on the current def-plane pair
     T dT[C::S][3][3];              // interpolant derivative / h, plane ring
     T qz[C::S][3];                 // q_z, plane ring
     T A0[C::S][3], A1[C::S][3];    // z-accumulated ghat for def planes zd, zd+1
     V4T<T> rt[C::S];               // prefetched reference terms (next B plane)
-    int z0, z1, jfirst, jlast, wxlo, wylo, wzlo, cur_zd, cta;
+    int z0, z1, zb, jfirst, jlast, wzlo, cur_zd, cta;
     double dacc;
 };
 
 template <typename T, typename C>
-__device__ __forceinline__ bool slot_vol(const March<T, C>& m, int s) { return (m.flags >> s) & 1u; }
+__device__ __forceinline__ bool s_vol(const March<T, C>& m, int s) { return (m.flags >> (4 * s)) & 1u; }
 template <typename T, typename C>
-__device__ __forceinline__ bool slot_e0(const March<T, C>& m, int s) { return (m.flags >> (8 + s)) & 1u; }
+__device__ __forceinline__ bool s_e0(const March<T, C>& m, int s) { return (m.flags >> (4 * s + 1)) & 1u; }
+template <typename T, typename C>
+__device__ __forceinline__ bool s_fx(const March<T, C>& m, int s) { return (m.flags >> (4 * s + 2)) & 1u; }
+template <typename T, typename C>
+__device__ __forceinline__ bool s_fy(const March<T, C>& m, int s) { return (m.flags >> (4 * s + 3)) & 1u; }
 
-template <typename T>
-__device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const Smem<T>& sm, int exy, int zd,
+template <typename T, typename C>
+__device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const SmemL<T, C>& sm, int P, int zd,
                                             T (&out)[3]) {
     // P_xy y on def plane zd at the slot's image (i, j): x then y (transfer.py:136-142)
-    const int ex = exy & 0xff, ey = exy >> 8;
+    const int ex = P % C::E1X, ey = P / C::E1X;
     const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
     const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
     const T wx = sm.colPw[ex], wy = sm.rowPw[ey];
@@ -193,14 +147,13 @@ __device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const Smem<T>
 // Reduce a completed deformation plane (z-accumulated ghat in `acc`) in x then y over
 // the tile's window and write it to the CTA's partial slot zs.
 template <typename T, typename C>
-__device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>& sm, March<T, C>& m,
-                                            T (&acc)[C::S][3], int zs) {
+__device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, SmemL<T, C>& sm, const int (&P)[C::S],
+                                         const T (&acc)[C::S][3], int cta, int zs) {
     const int wx = a.fp.wx, wy = a.fp.wy;
 #pragma unroll
     for (int s = 0; s < C::S; ++s) {
-        if (m.P[s] < 0) continue;
 #pragma unroll
-        for (int c = 0; c < 3; ++c) sm.buf[c * C::E1 + m.P[s]] = acc[s][c];
+        for (int c = 0; c < 3; ++c) sm.buf[c][P[s]] = acc[s][c];
     }
     __syncthreads();
     for (int t = threadIdx.x; t < C::E1Y * wx; t += C::NT) {
@@ -208,21 +161,20 @@ __device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>
         const int d = t - row * wx;
         const int k0 = sm.xoff[d], k1 = sm.xoff[d + 1];
         T r0 = (T)0, r1 = (T)0, r2 = (T)0;
-        const T* b = sm.buf + row * C::E1X;
         for (int k = k0; k < k1; ++k) {
-            const int e = sm.xcol[k];
+            const int e = row * C::E1X + sm.xcol[k];
             const T w = sm.xw[k];
-            r0 = fmaf_t(b[e], w, r0);
-            r1 = fmaf_t(b[C::E1 + e], w, r1);
-            r2 = fmaf_t(b[2 * C::E1 + e], w, r2);
+            r0 = fmaf_t(sm.buf[0][e], w, r0);
+            r1 = fmaf_t(sm.buf[1][e], w, r1);
+            r2 = fmaf_t(sm.buf[2][e], w, r2);
         }
-        sm.Xr[(0 * C::E1Y + row) * wx + d] = r0;
-        sm.Xr[(1 * C::E1Y + row) * wx + d] = r1;
-        sm.Xr[(2 * C::E1Y + row) * wx + d] = r2;
+        sm.Xr[0][row][d] = r0;
+        sm.Xr[1][row][d] = r1;
+        sm.Xr[2][row][d] = r2;
     }
     __syncthreads();
     const size_t win = (size_t)a.fp.wz * wy * wx;
-    T* out = a.partial + (size_t)m.cta * 3 * win + (size_t)zs * wy * wx;
+    T* out = a.partial + (size_t)cta * 3 * win + (size_t)zs * wy * wx;
     for (int t = threadIdx.x; t < wy * wx; t += C::NT) {
         const int dr = t / wx;
         const int d = t - dr * wx;
@@ -231,9 +183,9 @@ __device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, const Smem<T>
         for (int k = k0; k < k1; ++k) {
             const int row = sm.yrow[k];
             const T w = sm.yw[k];
-            r0 = fmaf_t(sm.Xr[(0 * C::E1Y + row) * wx + d], w, r0);
-            r1 = fmaf_t(sm.Xr[(1 * C::E1Y + row) * wx + d], w, r1);
-            r2 = fmaf_t(sm.Xr[(2 * C::E1Y + row) * wx + d], w, r2);
+            r0 = fmaf_t(sm.Xr[0][row][d], w, r0);
+            r1 = fmaf_t(sm.Xr[1][row][d], w, r1);
+            r2 = fmaf_t(sm.Xr[2][row][d], w, r2);
         }
         out[t] = r0;
         out[win + t] = r1;
@@ -255,34 +207,35 @@ __device__ __forceinline__ int cell_axis(T p, T o, T h, T ih, int n, bool& insid
 }
 
 template <int R, typename T, typename C, bool POW2>
-__device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>& sm, March<T, C>& m,
+__device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& sm, March<T, C>& m,
                                            int p) {
     constexpr int RB = (R + 2) % 3;  // plane p-1
     constexpr int RC = (R + 1) % 3;  // plane p-2
     constexpr int S = C::S;
     const unsigned nxy = (unsigned)a.nx * (unsigned)a.ny;
+    const T hx2 = (T)0.5 * a.ihx, hy2 = (T)0.5 * a.ihy;
 
     // ---------------------------------------------------------------- (A) plane p
     if (p >= 0 && p < a.nz && p <= m.z1) {
-        const int zd = a.i0z[p];
+        const int zd = sm.zi[p - m.zb][0];
         if (zd != m.cur_zd) {
             const int zd1 = min(zd + 1, a.ndz - 1);
             const bool shift = (zd == m.cur_zd + 1);
 #pragma unroll
             for (int s = 0; s < S; ++s) {
-                if (!slot_vol(m, s)) continue;
+                if (!s_vol(m, s)) continue;
                 if (shift) {
 #pragma unroll
                     for (int k = 0; k < 3; ++k) m.ylo[s][k] = m.yhi[s][k];
                 } else {
-                    load_yplane(a, sm, m.exy[s], zd, m.ylo[s]);
+                    load_yplane(a, sm, m.P[s], zd, m.ylo[s]);
                 }
-                load_yplane(a, sm, m.exy[s], zd1, m.yhi[s]);
+                load_yplane(a, sm, m.P[s], zd1, m.yhi[s]);
             }
             m.cur_zd = zd;
         }
-        const T wz = a.w1z[p];
-        const T wz0 = sub_rn((T)1, wz);
+        const T wz = sm.zt[p - m.zb][6];
+        const T wz0 = sm.zt[p - m.zb][7];
         // coordinates and corner offsets of all slots first, so the 8 * S gathers are
         // in flight together
         unsigned off[S];
@@ -294,7 +247,7 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
             const T yh0 = add_rn(mul_rn(m.ylo[s][0], wz0), mul_rn(m.yhi[s][0], wz));
             const T yh1 = add_rn(mul_rn(m.ylo[s][1], wz0), mul_rn(m.yhi[s][1], wz));
             const T yh2 = add_rn(mul_rn(m.ylo[s][2], wz0), mul_rn(m.yhi[s][2], wz));
-            bool inside = slot_vol(m, s);
+            bool inside = s_vol(m, s);
             const int ix = cell_axis<T, POW2>(yh0, a.ox, a.hx, a.ihx, a.nx, inside, fx[s]);
             const int iy = cell_axis<T, POW2>(yh1, a.oy, a.hy, a.ihy, a.ny, inside, fy[s]);
             const int iz = cell_axis<T, POW2>(yh2, a.oz, a.hz, a.ihz, a.nz, inside, fz[s]);
@@ -325,45 +278,47 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
             m.dT[s][R][0] = d0;
             m.dT[s][R][1] = d1;
             m.dT[s][R][2] = d2;
-            if (m.P[s] >= 0) sm.Wsm[R * C::E1 + m.P[s]] = W;
+            sm.Wsm[R][m.P[s]] = W;
         }
     } else {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             m.dT[s][R][0] = m.dT[s][R][1] = m.dT[s][R][2] = (T)0;
-            if (m.P[s] >= 0) sm.Wsm[R * C::E1 + m.P[s]] = (T)0;
+            sm.Wsm[R][m.P[s]] = (T)0;
         }
     }
     __syncthreads();
 
     // ---------------------------------------------------------------- (B) q on plane k = p-1
-    T* qxw = sm.qx + (p & 1) * C::E2;  // plane p-1 buffer; plane p-2 sits in the other one
-    T* qyw = sm.qy + (p & 1) * C::E2;
+    T* qxw = sm.qx[p & 1];  // plane p-1 buffer; plane p-2 sits in the other one
+    T* qyw = sm.qy[p & 1];
     {
         const int k = p - 1;
         const bool kv = (k >= m.z0) && (k < m.z1);
-        T cmz, c0z, cpz;
-        fd_coef<T>(k, a.nz, a.ihz, cmz, c0z, cpz);
-        const T* Wk = sm.Wsm + RB * C::E1;
-        const T* Wm = sm.Wsm + RC * C::E1;
-        const T* Wp = sm.Wsm + R * C::E1;
+        const T* zc = sm.zt[max(k - m.zb, 0)];
+        const T cmz = zc[0], c0z = zc[1], cpz = zc[2];
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             T qxv = (T)0, qyv = (T)0, qzv = (T)0;
-            if (kv && slot_e0(m, s)) {
+            if (kv && s_e0(m, s)) {
                 const int P = m.P[s];
-                const int ex = m.exy[s] & 0xff, ey = m.exy[s] >> 8;
-                const T* cg = sm.colG + 3 * ex;
-                const T* rg = sm.rowG + 3 * ey;
-                const T gx = fmaf_t(cg[0], Wk[P - 1], fmaf_t(cg[1], Wk[P], cg[2] * Wk[P + 1]));
-                const T gy = fmaf_t(rg[0], Wk[P - C::E1X], fmaf_t(rg[1], Wk[P], rg[2] * Wk[P + C::E1X]));
-                const T gz = fmaf_t(cmz, Wm[P], fmaf_t(c0z, Wk[P], cpz * Wp[P]));
+                const T w0 = sm.Wsm[RB][P];
+                T gx = (sm.Wsm[RB][P + 1] - sm.Wsm[RB][P - 1]) * hx2;
+                T gy = (sm.Wsm[RB][P + C::E1X] - sm.Wsm[RB][P - C::E1X]) * hy2;
+                if (s_fx(m, s)) {  // one-sided difference at an x face
+                    const T* cg = sm.colG[P % C::E1X];
+                    gx = fmaf_t(cg[0], sm.Wsm[RB][P - 1], fmaf_t(cg[1], w0, cg[2] * sm.Wsm[RB][P + 1]));
+                }
+                if (s_fy(m, s)) {
+                    const T* rg = sm.rowG[P / C::E1X];
+                    gy = fmaf_t(rg[0], sm.Wsm[RB][P - C::E1X],
+                                fmaf_t(rg[1], w0, rg[2] * sm.Wsm[RB][P + C::E1X]));
+                }
+                const T gz = fmaf_t(cmz, sm.Wsm[RC][P], fmaf_t(c0z, w0, cpz * sm.Wsm[R][P]));
                 ngf_q(a, gx, gy, gz, m.rt[s], qxv, qyv, qzv, m.dacc);
             }
-            if (m.P[s] >= 0) {
-                qxw[m.P2[s]] = qxv;
-                qyw[m.P2[s]] = qyv;
-            }
+            qxw[m.P2[s]] = qxv;
+            qyw[m.P2[s]] = qyv;
             m.qz[s][RB] = qzv;
         }
         // prefetch the reference terms of plane p for the next step's (B)
@@ -371,7 +326,7 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
             const V4T<T>* rp = a.RT + (size_t)p * nxy;
 #pragma unroll
             for (int s = 0; s < S; ++s)
-                if (slot_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
+                if (s_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
         }
     }
     __syncthreads();
@@ -379,22 +334,25 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
     // ---------------------------------------------------------------- (C) s, ghat, z-P^T on j = p-2
     const int j = p - 2;
     if (j < m.jfirst || j > m.jlast) return;  // uniform
-    T gtm, gt0, gtp;
-    fdt_coef<T>(j, a.nz, a.ihz, gtm, gt0, gtp);
-    const T* qxj = sm.qx + ((p & 1) ^ 1) * C::E2;
-    const T* qyj = sm.qy + ((p & 1) ^ 1) * C::E2;
-    const int zdj = a.i0z[j];
-    const T w1 = a.w1z[j];
-    const T w0 = (T)1 - w1;
+    const T* zc = sm.zt[j - m.zb];
+    const T gtm = zc[3], gt0 = zc[4], gtp = zc[5], w1 = zc[6], w0 = zc[7];
+    const T* qxj = sm.qx[(p & 1) ^ 1];
+    const T* qyj = sm.qy[(p & 1) ^ 1];
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        if (!slot_vol(m, s)) continue;
+        if (!s_vol(m, s)) continue;
         const int P2 = m.P2[s];
-        const int ex = m.exy[s] & 0xff, ey = m.exy[s] >> 8;
-        const T* ct = sm.colGt + 3 * ex;
-        const T* rt = sm.rowGt + 3 * ey;
-        T sv = fmaf_t(ct[0], qxj[P2 - 1], fmaf_t(ct[1], qxj[P2], ct[2] * qxj[P2 + 1]));
-        sv = fmaf_t(rt[0], qyj[P2 - C::E2X], fmaf_t(rt[1], qyj[P2], fmaf_t(rt[2], qyj[P2 + C::E2X], sv)));
+        T sx = (qxj[P2 - 1] - qxj[P2 + 1]) * hx2;
+        T sy = (qyj[P2 - C::E2X] - qyj[P2 + C::E2X]) * hy2;
+        if (s_fx(m, s)) {  // exact transposed face rows (warp.py:168-175)
+            const T* ct = sm.colGt[m.P[s] % C::E1X];
+            sx = fmaf_t(ct[0], qxj[P2 - 1], fmaf_t(ct[1], qxj[P2], ct[2] * qxj[P2 + 1]));
+        }
+        if (s_fy(m, s)) {
+            const T* rt = sm.rowGt[m.P[s] / C::E1X];
+            sy = fmaf_t(rt[0], qyj[P2 - C::E2X], fmaf_t(rt[1], qyj[P2], rt[2] * qyj[P2 + C::E2X]));
+        }
+        T sv = sx + sy;
         sv = fmaf_t(gtm, m.qz[s][R], fmaf_t(gt0, m.qz[s][RC], fmaf_t(gtp, m.qz[s][RB], sv)));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -406,14 +364,14 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
     // def plane zdj is complete when the next image plane maps to a later pair.  The map
     // can advance by 2 (w1 rounds to just below 1 when the grids nearly coincide), in
     // which case zdj + 1 is complete as well.
-    const bool last = (j == m.jlast);
-    const int step = last ? 2 : a.i0z[j + 1] - zdj;
+    const int zdj = sm.zi[j - m.zb][0];
+    const int step = (j == m.jlast) ? 2 : sm.zi[j - m.zb][1];
     if (step >= 1) {
-        flush_plane<T, C>(a, sm, m, m.A0, zdj - m.wzlo);
+        flush_plane<T, C>(a, sm, m.P, m.A0, m.cta, zdj - m.wzlo);
         if (step >= 2) {
             if (zdj + 1 <= a.ndz - 1) {
                 __syncthreads();
-                flush_plane<T, C>(a, sm, m, m.A1, zdj + 1 - m.wzlo);
+                flush_plane<T, C>(a, sm, m.P, m.A1, m.cta, zdj + 1 - m.wzlo);
             }
 #pragma unroll
             for (int s = 0; s < S; ++s)
@@ -434,9 +392,9 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, const Smem<T>&
 template <typename T, typename C, bool POW2>
 __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmemL<T, C>& sm = *reinterpret_cast<SmemL<T, C>*>(smem_raw);
     constexpr int S = C::S;
     const FusedPlan& fp = a.fp;
-    const Smem<T> sm = carve_smem<T, C>(smem_raw, fp.wx, fp.wy);
     const int tid = threadIdx.x;
     March<T, C> m;
     m.cta = blockIdx.x;
@@ -446,10 +404,11 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
     const int x0 = tx * C::TX, y0 = ty * C::TY;
     m.z0 = tz * fp.cz;
     m.z1 = min(m.z0 + fp.cz, a.nz);
+    m.zb = m.z0 - 1;  // first plane of the z tables
     m.jfirst = max(m.z0 - 1, 0);
     m.jlast = min(m.z1, a.nz - 1);
-    m.wxlo = fp.win_x[tx];
-    m.wylo = fp.win_y[ty];
+    const int wxlo = fp.win_x[tx];
+    const int wylo = fp.win_y[ty];
     m.wzlo = fp.win_z[tz];
     m.cur_zd = -1000;
     m.dacc = 0.0;
@@ -457,15 +416,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
     // ---- per-CTA tables
     for (int e = tid; e < C::E1X; e += C::NT) {
         const int i = x0 - 1 + e;
-        T cm, c0, cp;
-        fd_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
-        sm.colG[3 * e] = cm;
-        sm.colG[3 * e + 1] = c0;
-        sm.colG[3 * e + 2] = cp;
-        fdt_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
-        sm.colGt[3 * e] = cm;
-        sm.colGt[3 * e + 1] = c0;
-        sm.colGt[3 * e + 2] = cp;
+        fd_coef<T>(i, a.nx, a.ihx, sm.colG[e][0], sm.colG[e][1], sm.colG[e][2]);
+        fdt_coef<T>(i, a.nx, a.ihx, sm.colGt[e][0], sm.colGt[e][1], sm.colGt[e][2]);
         const bool in = i >= 0 && i < a.nx;
         const int i0 = in ? a.i0x[i] : 0;
         sm.colP0[e] = i0;
@@ -474,31 +426,37 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
     }
     for (int e = tid; e < C::E1Y; e += C::NT) {
         const int jj = y0 - 1 + e;
-        T cm, c0, cp;
-        fd_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
-        sm.rowG[3 * e] = cm;
-        sm.rowG[3 * e + 1] = c0;
-        sm.rowG[3 * e + 2] = cp;
-        fdt_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
-        sm.rowGt[3 * e] = cm;
-        sm.rowGt[3 * e + 1] = c0;
-        sm.rowGt[3 * e + 2] = cp;
+        fd_coef<T>(jj, a.ny, a.ihy, sm.rowG[e][0], sm.rowG[e][1], sm.rowG[e][2]);
+        fdt_coef<T>(jj, a.ny, a.ihy, sm.rowGt[e][0], sm.rowGt[e][1], sm.rowGt[e][2]);
         const bool in = jj >= 0 && jj < a.ny;
         const int i0 = in ? a.i0y[jj] : 0;
         sm.rowP0[e] = i0;
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : (T)0;
     }
+    for (int t = tid; t < m.z1 + 2 - m.zb; t += C::NT) {
+        // z tables for planes zb .. z1+1 (coefficients of warp.py:130-176 along z, P's w1)
+        const int z = m.zb + t;
+        T* zc = sm.zt[t];
+        fd_coef<T>(z, a.nz, a.ihz, zc[0], zc[1], zc[2]);
+        fdt_coef<T>(z, a.nz, a.ihz, zc[3], zc[4], zc[5]);
+        const bool in = z >= 0 && z < a.nz;
+        const T w1 = in ? a.w1z[z] : (T)0;
+        zc[6] = w1;
+        zc[7] = sub_rn((T)1, w1);
+        sm.zi[t][0] = in ? a.i0z[z] : 0;
+        sm.zi[t][1] = (in && z + 1 < a.nz) ? a.i0z[z + 1] - a.i0z[z] : 2;
+    }
     for (int t = tid; t < 2 * C::E2; t += C::NT) {
-        sm.qx[t] = (T)0;
-        sm.qy[t] = (T)0;
+        (&sm.qx[0][0])[t] = (T)0;
+        (&sm.qy[0][0])[t] = (T)0;
     }
     {
         // this tile's CSR of the transposed 1-D interpolation (host-built, ascending E1
         // index per window entry: the reference's gather order, transfer.py:89-96)
-        const int sx = fp.wx + 1 + 2 * C::E1X, sy = fp.wy + 1 + 2 * C::E1Y;
-        const int32_t* gx = fp.xcsr + (size_t)tx * sx;
-        const int32_t* gy = fp.ycsr + (size_t)ty * sy;
+        const int sxs = fp.wx + 1 + 2 * C::E1X, sys = fp.wy + 1 + 2 * C::E1Y;
+        const int32_t* gx = fp.xcsr + (size_t)tx * sxs;
+        const int32_t* gy = fp.ycsr + (size_t)ty * sys;
         const T* wxg = (const T*)fp.xcw + (size_t)tx * 2 * C::E1X;
         const T* wyg = (const T*)fp.ycw + (size_t)ty * 2 * C::E1Y;
         for (int t = tid; t < fp.wx + 1; t += C::NT) sm.xoff[t] = gx[t];
@@ -512,23 +470,34 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
             sm.yw[t] = wyg[t];
         }
     }
+    (void)wxlo;
+    (void)wylo;
 
     // ---- slot positions (fixed for all planes)
     m.flags = 0u;
+    const T hx2 = (T)0.5 * a.ihx, hy2 = (T)0.5 * a.ihy;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
         const int P = tid + s * C::NT;
         const bool ok = P < C::E1;
-        const int ex = ok ? P % C::E1X : 0, ey = ok ? P / C::E1X : 0;
+        const int Pc = ok ? P : C::E1;  // padding slots write into the sink entry
+        const int ex = Pc % C::E1X, ey = Pc / C::E1X;
         const int i = x0 - 1 + ex, jj = y0 - 1 + ey;
         const bool vol = ok && i >= 0 && i < a.nx && jj >= 0 && jj < a.ny;
         const bool e0 = vol && ex >= 1 && ex <= C::TX && ey >= 1 && ey <= C::TY;
-        m.P[s] = ok ? P : -1;
-        m.P2[s] = (ey + 1) * C::E2X + ex + 1;
+        // a slot needs the exact face coefficients where G or G^T differ from central
+        T cm, c0, cp, gm, g0, gp;
+        fd_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
+        fdt_coef<T>(i, a.nx, a.ihx, gm, g0, gp);
+        const bool fx = !(cm == -hx2 && c0 == (T)0 && cp == hx2 && gm == hx2 && g0 == (T)0 && gp == -hx2);
+        fd_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
+        fdt_coef<T>(jj, a.ny, a.ihy, gm, g0, gp);
+        const bool fy = !(cm == -hy2 && c0 == (T)0 && cp == hy2 && gm == hy2 && g0 == (T)0 && gp == -hy2);
+        m.P[s] = Pc;
+        m.P2[s] = ok ? (ey + 1) * C::E2X + ex + 1 : 0;  // padding slots write 0 into the pad ring
         m.ij[s] = vol ? (unsigned)(jj * a.nx + i) : 0u;
-        m.exy[s] = ex | (ey << 8);
-        m.flags |= (vol ? 1u : 0u) << s;
-        m.flags |= (e0 ? 1u : 0u) << (8 + s);
+        m.flags |= ((vol ? 1u : 0u) | (e0 ? 2u : 0u) | (vol && fx ? 4u : 0u) | (vol && fy ? 8u : 0u))
+                   << (4 * s);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
             m.qz[s][r] = (T)0;
@@ -547,7 +516,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         const V4T<T>* rp = a.RT + (size_t)m.z0 * a.nx * a.ny;
 #pragma unroll
         for (int s = 0; s < S; ++s)
-            if (slot_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
+            if (s_e0(m, s)) m.rt[s] = ld_rt(rp + m.ij[s]);
     }
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2

@@ -105,7 +105,7 @@ static int fused_setup(ngf_level* L) {
     std::vector<int> xl, xh, yl, yh, zl, zh;
     FusedPlan& fp = L->fp;
     // kernel variant (f32: several tile/occupancy shapes; f64: one)
-    int variant = 2;  // 32x12 tiles, 256 threads, 3 CTAs/SM: fastest at 256^3 (tools/sweep.py)
+    int variant = 1;  // 32x12 tiles, 256 threads, 2 CTAs/SM: fastest at 256^3 (tools/sweep.py)
     if (const char* env = std::getenv("NGF_FUSED_VARIANT"))
         variant = std::atoi(env) % fused_variant_count();
     if (sizeof(T) == 8) variant = 0;
@@ -142,7 +142,7 @@ static int fused_setup(ngf_level* L) {
     if (!cz) return NGF_EARG;
     if (const char* env = std::getenv("NGF_FUSED_CZ")) {  // tuning / debugging override
         const int forced = std::atoi(env);
-        if (forced > 0 && valid(forced)) cz = forced;
+        if (forced > 0 && forced <= 96 && valid(forced)) cz = forced;
     }
     fp.cz = cz;
     fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh);
