@@ -285,10 +285,12 @@ def run_ours(args):
         yr, rep = ngf.register(R, T, cfg)
         barrier()
         reg_s = max_over_ranks(time.perf_counter() - t0)
-        reg = {"seconds": reg_s, "levels": levels,
+        reg = {"seconds": reg_s, "levels": levels, "inputs": "host numpy f32 (H2D inside)",
+               "seconds_pyramid": round(rep.seconds_pyramid, 4),
                "per_level": [{"image": lv.image_dims[0], "def": lv.def_dims[0],
                               "iterations": lv.iterations, "evals": lv.evaluations,
-                              "stop": lv.stop_reason, "optimize_s": round(lv.seconds_optimize, 4)}
+                              "stop": lv.stop_reason, "setup_s": round(lv.seconds_setup, 4),
+                              "optimize_s": round(lv.seconds_optimize, 4)}
                              for lv in rep.levels],
                "paper_gtx1080ti_s": 1.99,
                "pairs_per_s": ws / reg_s}

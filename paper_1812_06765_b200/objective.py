@@ -128,12 +128,37 @@ class LevelObjective:
         J, D, S = float(sc[0]), float(sc[1]), float(sc[2])
         return J, D, S, (dev.to_host(g) if np_out else g)
 
+    def _host_call(self, x: np.ndarray):
+        """numpy in / out through pinned staging buffers: one H2D of x, one evaluation,
+        one D2H of (grad, J, D, S), one stream sync."""
+        t = dev.torch()
+        n = x.size
+        st = getattr(self, "_stage", None)
+        if st is None or st[0].numel() != n or st[0].dtype != dev.torch_dtype(x.dtype):
+            tdt = dev.torch_dtype(x.dtype)
+            st = (t.empty(n, dtype=tdt, pin_memory=True), dev.empty((n,), tdt), dev.empty((n,), tdt),
+                  t.empty(n, dtype=tdt, pin_memory=True), dev.zeros((3,), "float64"),
+                  t.empty(3, dtype=t.float64, pin_memory=True))
+            self._stage = st
+        x_pin, x_dev, g_dev, g_pin, sc_dev, sc_pin = st
+        x_pin.numpy()[:] = x.reshape(-1)
+        x_dev.copy_(x_pin, non_blocking=True)
+        self.eval_device(x_dev, g_dev, sc_dev)
+        g_pin.copy_(g_dev, non_blocking=True)
+        sc_pin.copy_(sc_dev, non_blocking=True)
+        t.cuda.current_stream().synchronize()
+        J, D, S = (float(v) for v in sc_pin.numpy())
+        return J, D, S, g_pin.numpy().copy()
+
     def __call__(self, x):
-        if not dev.is_tensor(x) and not np.all(np.isfinite(x)):
-            # overflowed line-search trial point; force a backtrack (objective.py:55-57)
-            return float("inf"), np.zeros_like(x)
-        J, D, S, g = self.evaluate(self.field_from_flat(x))
+        if dev.is_tensor(x):
+            J, D, S, g = self.evaluate(self.field_from_flat(x))
+        else:
+            # non-finite trial points are detected on the device (J = inf), so the host
+            # does not re-scan x (objective.py:55-57 semantics are kept below)
+            J, D, S, g = self._host_call(np.asarray(x))
         if not np.isfinite(J):
+            # overflowed line-search trial point; force a backtrack (objective.py:55-57)
             return float("inf"), (np.zeros_like(g) if not dev.is_tensor(g) else g.zero_())
         self.last_D, self.last_S = D, S
         return J, g
