@@ -543,54 +543,67 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
 
 // ------------------------------------------------------------------ reduce + curvature
 
-// Lu (3, M) of the displacement and per-block partial sums of (Lu)^2
+// Lu (3, M) of the displacement and per-block partial sums of (Lu)^2.  Grid: x/y tiles of
+// 32 x 8 nodes, blockIdx.z = comp * nz + k (32-bit index math only).
 template <typename T>
-__global__ void k_curv_L(GridK<T> g, const T* __restrict__ y, T* __restrict__ L,
-                         double* __restrict__ spart, int* __restrict__ flag) {
-    const int64_t m = g.n();
-    const int64_t sy = g.nx, sz = (int64_t)g.nx * g.ny;
-    const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
+__device__ __forceinline__ T ident(double o, double h, int i) {
+    return (T)(o + h * (double)i);  // identity_field_array: f64 centres cast (geometry.py:148-155)
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) k_curv_L(GridK<T> g, const T* __restrict__ y, T* __restrict__ L,
+                                                double* __restrict__ spart, int* __restrict__ flag) {
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 8 + threadIdx.y;
+    const int comp = blockIdx.z / g.nz, k = blockIdx.z - comp * g.nz;
+    const unsigned m = (unsigned)g.nx * g.ny * g.nz;
+    const unsigned sy = g.nx, sz = (unsigned)g.nx * g.ny;
     double acc = 0.0;
     bool bad = false;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 3 * m;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        bad |= !isfinite(y[t]);
-        const int comp = (int)(t / m);
-        const int64_t idx = t % m;
-        const int i = (int)(idx % g.nx);
-        const int j = (int)((idx / g.nx) % g.ny);
-        const int k = (int)(idx / sz);
-        const T* yc = y + comp * m;
-        auto u = [&](int ii, int jj, int kk) -> T {
-            const T idv = comp == 0 ? (T)(g.dox + g.dhx * (double)ii)
-                                    : (comp == 1 ? (T)(g.doy + g.dhy * (double)jj)
-                                                 : (T)(g.doz + g.dhz * (double)kk));
-            return yc[((int64_t)kk * g.ny + jj) * g.nx + ii] - idv;
-        };
-        const T u0 = u(i, j, k);
+    if (i < g.nx && j < g.ny) {
+        const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
+        const unsigned idx = (unsigned)k * sz + (unsigned)j * sy + (unsigned)i;
+        const T* yc = y + (size_t)comp * m;
+        // displacement u = y - id; id varies only along the component's own axis
+        const double o = comp == 0 ? g.dox : (comp == 1 ? g.doy : g.doz);
+        const double h = comp == 0 ? g.dhx : (comp == 1 ? g.dhy : g.dhz);
+        const int own = comp == 0 ? i : (comp == 1 ? j : k);
+        const T id0 = ident<T>(o, h, own);
+        const T yv = yc[idx];
+        bad = !isfinite(yv);
+        const T u0 = yv - id0;
         T lap = (T)0;
-        if (g.nx >= 3 && i > 0 && i < g.nx - 1) lap += (u(i + 1, j, k) - (T)2 * u0 + u(i - 1, j, k)) * ihx2;
-        if (g.ny >= 3 && j > 0 && j < g.ny - 1) lap += (u(i, j + 1, k) - (T)2 * u0 + u(i, j - 1, k)) * ihy2;
-        if (g.nz >= 3 && k > 0 && k < g.nz - 1) lap += (u(i, j, k + 1) - (T)2 * u0 + u(i, j, k - 1)) * ihz2;
-        L[t] = lap;
-        acc += (double)lap * (double)lap;
-        (void)sy;
+        if (g.nx >= 3 && i > 0 && i < g.nx - 1) {
+            const T idm = comp == 0 ? ident<T>(o, h, i - 1) : id0, idp = comp == 0 ? ident<T>(o, h, i + 1) : id0;
+            lap += ((yc[idx + 1] - idp) - (T)2 * u0 + (yc[idx - 1] - idm)) * ihx2;
+        }
+        if (g.ny >= 3 && j > 0 && j < g.ny - 1) {
+            const T idm = comp == 1 ? ident<T>(o, h, j - 1) : id0, idp = comp == 1 ? ident<T>(o, h, j + 1) : id0;
+            lap += ((yc[idx + sy] - idp) - (T)2 * u0 + (yc[idx - sy] - idm)) * ihy2;
+        }
+        if (g.nz >= 3 && k > 0 && k < g.nz - 1) {
+            const T idm = comp == 2 ? ident<T>(o, h, k - 1) : id0, idp = comp == 2 ? ident<T>(o, h, k + 1) : id0;
+            lap += ((yc[idx + sz] - idp) - (T)2 * u0 + (yc[idx - sz] - idm)) * ihz2;
+        }
+        L[(size_t)comp * m + idx] = lap;
+        acc = (double)lap * (double)lap;
     }
-    __shared__ double red[32];
-    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+    __shared__ double red[8];
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (threadIdx.x == 0) red[threadIdx.y] = acc;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double s = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += red[w];
-        spart[blockIdx.x] = s;
+        for (int w = 0; w < 8; ++w) s += red[w];
+        spart[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
     }
 }
 
 template <typename T>
-__device__ __forceinline__ T d2t(const T* w, int64_t idx, int i, int n, int64_t stride, T ih2) {
+__device__ __forceinline__ T d2t(const T* w, unsigned idx, int i, int n, unsigned stride, T ih2) {
     if (n < 3) return (T)0;
     T o = (T)0;
     if (i <= n - 3) o += w[idx + stride];
@@ -599,40 +612,39 @@ __device__ __forceinline__ T d2t(const T* w, int64_t idx, int i, int n, int64_t 
     return o * ih2;
 }
 
+// grad = grad D (fixed-order sum of the covering tiles' partials) + alpha * vol * L^T L u
 template <typename T>
-__global__ void k_reduce(GridK<T> g, const FusedPlan fp, const T* __restrict__ partial,
-                         const T* __restrict__ L, T vol, T alpha, T* __restrict__ grad) {
-    const int64_t m = g.n();
-    const int64_t sz = (int64_t)g.nx * g.ny;
+__global__ void __launch_bounds__(256) k_reduce(GridK<T> g, const FusedPlan fp,
+                                                const T* __restrict__ partial, const T* __restrict__ L,
+                                                T vol, T alpha, T* __restrict__ grad) {
+    const int i = blockIdx.x * 32 + threadIdx.x;
+    const int j = blockIdx.y * 8 + threadIdx.y;
+    const int comp = blockIdx.z / g.nz, k = blockIdx.z - comp * g.nz;
+    if (i >= g.nx || j >= g.ny) return;
+    const unsigned m = (unsigned)g.nx * g.ny * g.nz;
+    const unsigned sy = g.nx, sz = (unsigned)g.nx * g.ny;
+    const unsigned idx = (unsigned)k * sz + (unsigned)j * sy + (unsigned)i;
     const int win = fp.wz * fp.wy * fp.wx;
-    const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < 3 * m;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const int comp = (int)(t / m);
-        const int64_t idx = t % m;
-        const int i = (int)(idx % g.nx);
-        const int j = (int)((idx / g.nx) % g.ny);
-        const int k = (int)(idx / sz);
-        // grad D: fixed-order sum of the covering tiles' partials
-        T gd = (T)0;
-        const int32_t* cz = fp.cov_z + (int64_t)k * kCover * 2;
-        const int32_t* cy = fp.cov_y + (int64_t)j * kCover * 2;
-        const int32_t* cx = fp.cov_x + (int64_t)i * kCover * 2;
-        for (int az = 0; az < kCover && cz[2 * az] >= 0; ++az) {
-            for (int ay = 0; ay < kCover && cy[2 * ay] >= 0; ++ay) {
-                for (int ax = 0; ax < kCover && cx[2 * ax] >= 0; ++ax) {
-                    const int cta = (cz[2 * az] * fp.nty + cy[2 * ay]) * fp.ntx + cx[2 * ax];
-                    const int off = (cz[2 * az + 1] * fp.wy + cy[2 * ay + 1]) * fp.wx + cx[2 * ax + 1];
-                    gd += __ldg(partial + ((size_t)cta * 3 + comp) * win + off);
-                }
+    T gd = (T)0;
+    const int32_t* cz = fp.cov_z + k * kCover * 2;
+    const int32_t* cy = fp.cov_y + j * kCover * 2;
+    const int32_t* cx = fp.cov_x + i * kCover * 2;
+    for (int az = 0; az < kCover && cz[2 * az] >= 0; ++az) {
+        for (int ay = 0; ay < kCover && cy[2 * ay] >= 0; ++ay) {
+            const int rowc = (cz[2 * az] * fp.nty + cy[2 * ay]) * fp.ntx;
+            const int rowo = (cz[2 * az + 1] * fp.wy + cy[2 * ay + 1]) * fp.wx;
+            for (int ax = 0; ax < kCover && cx[2 * ax] >= 0; ++ax) {
+                const int cta = rowc + cx[2 * ax];
+                gd += __ldg(partial + ((size_t)cta * 3 + comp) * win + rowo + cx[2 * ax + 1]);
             }
         }
-        // grad S = vol * L^T L u (curvature.py:74-81)
-        const T* Lc = L + comp * m;
-        T lt = d2t(Lc, idx, i, g.nx, 1, ihx2) + d2t(Lc, idx, j, g.ny, (int64_t)g.nx, ihy2) +
-               d2t(Lc, idx, k, g.nz, sz, ihz2);
-        grad[t] = gd + alpha * (vol * lt);
     }
+    // grad S = vol * L^T L u (curvature.py:74-81)
+    const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
+    const T* Lc = L + (size_t)comp * m;
+    const T lt = d2t(Lc, idx, i, g.nx, 1u, ihx2) + d2t(Lc, idx, j, g.ny, sy, ihy2) +
+                 d2t(Lc, idx, k, g.nz, sz, ihz2);
+    grad[(size_t)comp * m + idx] = gd + alpha * (vol * lt);
 }
 
 template <typename T>
@@ -768,14 +780,16 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
                       cudaEvent_t ev0, cudaEvent_t ev1) {
     GridK<T> gk = make_gridk<T>(dg);
     const int64_t m = grid_n(dg);
-    NGF_LAUNCH(k_curv_L<T>, ns, 256, 0, s, gk, a.y, L, spart, flag);
+    const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * dg.dims[2]);
+    const int nsb = (int)(cgrid.x * cgrid.y * cgrid.z);
+    if (nsb > ns) return NGF_EARG;
+    NGF_LAUNCH(k_curv_L<T>, cgrid, dim3(32, 8), 0, s, gk, a.y, L, spart, flag);
     if (ev0) cudaEventRecord(ev0, s);
     launch_variant<T>(a, s);
     if (ev1) cudaEventRecord(ev1, s);
     const double vol = dg.spacing[0] * dg.spacing[1] * dg.spacing[2];
-    NGF_LAUNCH(k_reduce<T>, blocks_for(3 * m, 256), 256, 0, s, gk, a.fp, a.partial, L, (T)vol,
-               (T)alpha, grad);
-    NGF_LAUNCH(k_finalize<T>, 1, 256, 0, s, a.dpart, a.fp.n_cta, spart, ns, a.half_hbar, vol / 2,
+    NGF_LAUNCH(k_reduce<T>, cgrid, dim3(32, 8), 0, s, gk, a.fp, a.partial, L, (T)vol, (T)alpha, grad);
+    NGF_LAUNCH(k_finalize<T>, 1, 256, 0, s, a.dpart, a.fp.n_cta, spart, nsb, a.half_hbar, vol / 2,
                alpha, flag, scalars);
     NGF_CHECK_LAUNCH();
     return 0;

@@ -13,7 +13,6 @@
 
 namespace ngf {
 
-constexpr int kCurvBlocks = 2 * kSMs;  // fixed grid of the curvature reduction (determinism)
 
 struct LevelWork {
     void* yhat = nullptr;   // 3N
@@ -43,7 +42,8 @@ struct ngf_level {
     void* fp_blob;   // device: windows + covers
     void* partial;   // n_cta x 3 x wz x wy x wx
     double* dpart;   // n_cta
-    double* spart;   // kCurvBlocks
+    double* spart;   // one partial per k_curv_L block
+    int ns;          // number of k_curv_L blocks
     void* L;         // 3M
     int* flag;       // non-finite y seen in this evaluation
     int timing;      // record events around the fused kernel
@@ -217,7 +217,8 @@ static int fused_setup(ngf_level* L) {
     const size_t win = (size_t)fp.wz * fp.wy * fp.wx;
     NGF_CUDA(cudaMalloc(&L->partial, (size_t)fp.n_cta * 3 * win * sizeof(T)));
     NGF_CUDA(cudaMalloc(&L->dpart, (size_t)fp.n_cta * sizeof(double)));
-    NGF_CUDA(cudaMalloc(&L->spart, (size_t)kCurvBlocks * sizeof(double)));
+    L->ns = (int)(((L->def.dims[0] + 31) / 32) * ((L->def.dims[1] + 7) / 8) * 3 * L->def.dims[2]);
+    NGF_CUDA(cudaMalloc(&L->spart, (size_t)L->ns * sizeof(double)));
     NGF_CUDA(cudaMalloc(&L->L, (size_t)3 * grid_n(L->def) * sizeof(T)));
     return fused_prepare<T>(variant, fp.smem_bytes);
 }
@@ -436,11 +437,11 @@ int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_de
     cudaEvent_t e0 = L->timing ? L->ev[0] : nullptr, e1 = L->timing ? L->ev[1] : nullptr;
     if (L->dtype == NGF_F32) {
         FusedArgs<float> a = fused_args<float>(L, y);
-        return fused_eval_launch<float>(a, L->def, L->alpha, (float*)L->L, L->spart, kCurvBlocks,
+        return fused_eval_launch<float>(a, L->def, L->alpha, (float*)L->L, L->spart, L->ns,
                                         L->flag, (float*)grad, scalars_dev, s, e0, e1);
     }
     FusedArgs<double> a = fused_args<double>(L, y);
-    return fused_eval_launch<double>(a, L->def, L->alpha, (double*)L->L, L->spart, kCurvBlocks,
+    return fused_eval_launch<double>(a, L->def, L->alpha, (double*)L->L, L->spart, L->ns,
                                      L->flag, (double*)grad, scalars_dev, s, e0, e1);
 }
 
