@@ -121,6 +121,14 @@ void ngf_level_destroy(ngf_level_t* level);
  * mode 1 = exact path (reference operation order, bit-exact D and grad D). */
 int ngf_level_eval(ngf_level_t* level, const void* y, void* grad, double* scalars_dev, int mode,
                    void* stream);
+/* Config-5 z-slab decomposition: restrict the fused evaluation to image
+ * planes [zlo, zhi).  mode 2 of ngf_level_eval then writes the slab's NGF partial
+ * (grad <- grad D_slab, scalars[1] <- D_slab, no curvature); after summing grad and
+ * scalars[1] over slabs (e.g. an NCCL all-reduce), ngf_level_add_curvature adds
+ * alpha grad S and sets scalars = (J, D, S), identically on every rank. */
+int ngf_level_set_zrange(ngf_level_t* level, int64_t zlo, int64_t zhi);
+int ngf_level_add_curvature(ngf_level_t* level, const void* y, void* grad, double* scalars_dev,
+                            void* stream);
 /* Device pointer of the level's reference terms (packed (gx, gy, gz, 1) / nR per voxel). */
 const void* ngf_level_ref_terms(const ngf_level_t* level);
 /* Record CUDA events around the fused kernel of every mode-0 evaluation (bench.py's

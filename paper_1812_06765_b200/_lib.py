@@ -66,6 +66,8 @@ _PROTOS = {
     "ngf_level_set_timing": (_i, [_vp, _i]),
     "ngf_level_kernel_ms": (_i, [_vp, ctypes.POINTER(ctypes.c_float)]),
     "ngf_level_info": (_i, [_vp, ctypes.POINTER(ctypes.c_int64)]),
+    "ngf_level_set_zrange": (_i, [_vp, _i64, _i64]),
+    "ngf_level_add_curvature": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "ngf_vec_dot": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),
     "ngf_vec_stats": (_i, [_i, _vp, _vp, _vp, _vp, _i64, _vp, _vp]),
     "ngf_vec_axpy_step": (_i, [_i, _vp, _d, _vp, _vp, _i64, _vp]),

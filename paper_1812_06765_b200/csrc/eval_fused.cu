@@ -402,8 +402,8 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
     const int ty = (m.cta / fp.ntx) % fp.nty;
     const int tz = m.cta / (fp.ntx * fp.nty);
     const int x0 = tx * C::TX, y0 = ty * C::TY;
-    m.z0 = tz * fp.cz;
-    m.z1 = min(m.z0 + fp.cz, a.nz);
+    m.z0 = fp.zlo + tz * fp.cz;
+    m.z1 = min(m.z0 + fp.cz, fp.zhi);
     m.zb = m.z0 - 1;  // first plane of the z tables
     m.jfirst = max(m.z0 - 1, 0);
     m.jlast = min(m.z1, a.nz - 1);
@@ -616,7 +616,7 @@ __device__ __forceinline__ T d2t(const T* w, unsigned idx, int i, int n, unsigne
 template <typename T>
 __global__ void __launch_bounds__(256) k_reduce(GridK<T> g, const FusedPlan fp,
                                                 const T* __restrict__ partial, const T* __restrict__ L,
-                                                T vol, T alpha, T* __restrict__ grad) {
+                                                T vol, T alpha, T* __restrict__ grad, int accumulate) {
     const int i = blockIdx.x * 32 + threadIdx.x;
     const int j = blockIdx.y * 8 + threadIdx.y;
     const int comp = blockIdx.z / g.nz, k = blockIdx.z - comp * g.nz;
@@ -625,7 +625,8 @@ __global__ void __launch_bounds__(256) k_reduce(GridK<T> g, const FusedPlan fp,
     const unsigned sy = g.nx, sz = (unsigned)g.nx * g.ny;
     const unsigned idx = (unsigned)k * sz + (unsigned)j * sy + (unsigned)i;
     const int win = fp.wz * fp.wy * fp.wx;
-    T gd = (T)0;
+    T gd = accumulate ? grad[(size_t)comp * m + idx] : (T)0;
+    if (partial) {
     const int32_t* cz = fp.cov_z + k * kCover * 2;
     const int32_t* cy = fp.cov_y + j * kCover * 2;
     const int32_t* cx = fp.cov_x + i * kCover * 2;
@@ -639,6 +640,11 @@ __global__ void __launch_bounds__(256) k_reduce(GridK<T> g, const FusedPlan fp,
             }
         }
     }
+    }
+    if (!L) {  // partial gradient of a z-slab: no curvature term
+        grad[(size_t)comp * m + idx] = gd;
+        return;
+    }
     // grad S = vol * L^T L u (curvature.py:74-81)
     const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
     const T* Lc = L + (size_t)comp * m;
@@ -650,7 +656,9 @@ __global__ void __launch_bounds__(256) k_reduce(GridK<T> g, const FusedPlan fp,
 template <typename T>
 __global__ void k_finalize(const double* __restrict__ dpart, int nd, const double* __restrict__ spart,
                            int ns, double half_hbar, double half_vol, double alpha, int* flag,
-                           double* __restrict__ out) {
+                           double* __restrict__ out, int mode) {
+    // mode 0: J = D + alpha S from both partial sets; 1: D only (slab partial, J = D, S = 0);
+    // 2: D already in out[1] (all-reduced over slabs), S from spart
     // fixed-order sums; D and S rounded like the reference's dtype products
     __shared__ double red[2][32];
     double a = 0.0, b = 0.0;
@@ -672,13 +680,17 @@ __global__ void k_finalize(const double* __restrict__ dpart, int nd, const doubl
             sa += red[0][w];
             sb += red[1][w];
         }
-        const double D = (double)((T)half_hbar * (T)sa);
-        const double S = (double)((T)half_vol * (T)sb);
+        const double D = mode == 2 ? out[1] : (double)((T)half_hbar * (T)sa);
+        const double S = mode == 1 ? 0.0 : (double)((T)half_vol * (T)sb);
         // a non-finite trial point gives J = inf (objective.py:55-57)
-        out[0] = *flag ? INFINITY : D + alpha * S;
+        if (mode == 1) {
+            out[0] = D;
+        } else {
+            out[0] = *flag ? INFINITY : D + alpha * S;
+            *flag = 0;
+        }
         out[1] = D;
         out[2] = S;
-        *flag = 0;
     }
 }
 
@@ -777,20 +789,24 @@ void launch_variant<double>(const FusedArgs<double>& a, cudaStream_t s) {
 template <typename T>
 int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, T* L, double* spart,
                       int ns, int* flag, T* grad, double* scalars, cudaStream_t s,
-                      cudaEvent_t ev0, cudaEvent_t ev1) {
+                      cudaEvent_t ev0, cudaEvent_t ev1, int part) {
+    // part 0: full evaluation; 1: NGF partial of the level's z-slab (grad <- grad D_slab,
+    // scalars <- D_slab); 2: add curvature to an all-reduced (grad D, D) in place
     GridK<T> gk = make_gridk<T>(dg);
-    const int64_t m = grid_n(dg);
     const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * dg.dims[2]);
     const int nsb = (int)(cgrid.x * cgrid.y * cgrid.z);
     if (nsb > ns) return NGF_EARG;
-    NGF_LAUNCH(k_curv_L<T>, cgrid, dim3(32, 8), 0, s, gk, a.y, L, spart, flag);
-    if (ev0) cudaEventRecord(ev0, s);
-    launch_variant<T>(a, s);
-    if (ev1) cudaEventRecord(ev1, s);
     const double vol = dg.spacing[0] * dg.spacing[1] * dg.spacing[2];
-    NGF_LAUNCH(k_reduce<T>, cgrid, dim3(32, 8), 0, s, gk, a.fp, a.partial, L, (T)vol, (T)alpha, grad);
+    if (part != 1) NGF_LAUNCH(k_curv_L<T>, cgrid, dim3(32, 8), 0, s, gk, a.y, L, spart, flag);
+    if (part != 2) {
+        if (ev0) cudaEventRecord(ev0, s);
+        launch_variant<T>(a, s);
+        if (ev1) cudaEventRecord(ev1, s);
+    }
+    NGF_LAUNCH(k_reduce<T>, cgrid, dim3(32, 8), 0, s, gk, a.fp, part == 2 ? nullptr : a.partial,
+               part == 1 ? nullptr : L, (T)vol, (T)alpha, grad, part == 2 ? 1 : 0);
     NGF_LAUNCH(k_finalize<T>, 1, 256, 0, s, a.dpart, a.fp.n_cta, spart, nsb, a.half_hbar, vol / 2,
-               alpha, flag, scalars);
+               alpha, flag, scalars, part);
     NGF_CHECK_LAUNCH();
     return 0;
 }
@@ -821,10 +837,10 @@ int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s) {
 
 template int fused_eval_launch<float>(const FusedArgs<float>&, const ngf_grid_t&, double, float*,
                                       double*, int, int*, float*, double*, cudaStream_t,
-                                      cudaEvent_t, cudaEvent_t);
+                                      cudaEvent_t, cudaEvent_t, int);
 template int fused_eval_launch<double>(const FusedArgs<double>&, const ngf_grid_t&, double, double*,
                                        double*, int, int*, double*, double*, cudaStream_t,
-                                       cudaEvent_t, cudaEvent_t);
+                                       cudaEvent_t, cudaEvent_t, int);
 template size_t fused_smem<float>(int, int, int);
 template size_t fused_smem<double>(int, int, int);
 template int pack_rt<float>(const float*, const float*, int64_t, void*, cudaStream_t);

@@ -12,6 +12,7 @@ struct FusedPlan {
     // kernel variant (tile rows, threads per CTA, occupancy) and tiles
     int variant, ty, nthreads;
     int ntx, nty, ntz, cz;
+    int zlo, zhi;  // image planes evaluated (a z-slab for config-5 decomposition; 0, nz otherwise)
     // P^T windows: max sizes and per-tile lower def index (device arrays)
     int wx, wy, wz;
     const int32_t* win_x;  // [ntx]

@@ -60,15 +60,18 @@ static bool is_pow2(double h) {
 }
 
 static int tile_windows(const int32_t* i0, int n, int nd, int tile, int ring_lo, std::vector<int>& lo,
-                        std::vector<int>& hi) {
-    const int nt = (n + tile - 1) / tile;
+                        std::vector<int>& hi, int org = 0, int end = -1) {
+    // tiles [org + t*tile, min(org + (t+1)*tile, end)) plus a one-voxel ring each side;
+    // window = def indices touched = [i0(first ring voxel), i0(last ring voxel) + 1]
+    if (end < 0) end = n;
+    const int nt = (end - org + tile - 1) / tile;
     lo.resize(nt);
     hi.resize(nt);
     int wmax = 1;
     for (int t = 0; t < nt; ++t) {
-        int a = t * tile - ring_lo;
+        int a = org + t * tile - ring_lo;
         if (a < 0) a = 0;
-        int b = t * tile + tile;  // ring voxel after the tile
+        int b = std::min(org + t * tile + tile, end);  // ring voxel after the tile
         if (b > n - 1) b = n - 1;
         int l = i0[a];
         int h = nd > 1 ? i0[b] + 1 : 0;
@@ -98,7 +101,7 @@ static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, 
 }
 
 template <typename T>
-static int fused_setup(ngf_level* L) {
+static int fused_setup(ngf_level* L, int zlo, int zhi) {
     const ngf_plan_t* p = L->plan;
     const int nx = (int)L->img.dims[0], ny = (int)L->img.dims[1], nz = (int)L->img.dims[2];
     const int ndx = (int)L->def.dims[0], ndy = (int)L->def.dims[1], ndz = (int)L->def.dims[2];
@@ -123,15 +126,16 @@ static int fused_setup(ngf_level* L) {
     // (waves of resident CTAs) x (planes marched per CTA, incl. the ring and pipeline).
     auto valid = [&](int c) {
         std::vector<int> a, b;
-        tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b);
+        tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b, zlo, zhi);
         std::vector<int32_t> cov;
         return build_cover(a, b, ndz, cov);
     };
     const int64_t resident = (int64_t)kSMs * kMinBlocks[variant];
     int cz = 0;
     double best = 1e300;
-    for (int c = std::min(nz, 96); c >= 1; --c) {
-        const int64_t nct = (int64_t)fp.ntx * fp.nty * ((nz + c - 1) / c);
+    const int nzs = zhi - zlo;
+    for (int c = std::min(nzs, 96); c >= 1; --c) {
+        const int64_t nct = (int64_t)fp.ntx * fp.nty * ((nzs + c - 1) / c);
         const double waves = (double)((nct + resident - 1) / resident);
         const double cost = waves * (c + 10);  // ~10 planes of per-CTA fixed cost (measured)
         if (cost < best * 0.999 && valid(c)) {
@@ -145,7 +149,9 @@ static int fused_setup(ngf_level* L) {
         if (forced > 0 && forced <= 96 && valid(forced)) cz = forced;
     }
     fp.cz = cz;
-    fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh);
+    fp.zlo = zlo;
+    fp.zhi = zhi;
+    fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh, zlo, zhi);
     fp.ntz = (int)zl.size();
     fp.n_cta = fp.ntx * fp.nty * fp.ntz;
     std::vector<int32_t> cx, cy, cz_;
@@ -293,6 +299,18 @@ __global__ void k_nonfinite(const T* __restrict__ y, int64_t n, int* flag) {
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
 }
 
+static int fused_part(ngf_level* L, const void* y, void* grad, double* scal, cudaStream_t s, int part) {
+    cudaEvent_t e0 = L->timing ? L->ev[0] : nullptr, e1 = L->timing ? L->ev[1] : nullptr;
+    if (L->dtype == NGF_F32) {
+        FusedArgs<float> a = fused_args<float>(L, y);
+        return fused_eval_launch<float>(a, L->def, L->alpha, (float*)L->L, L->spart, L->ns, L->flag,
+                                        (float*)grad, scal, s, e0, e1, part);
+    }
+    FusedArgs<double> a = fused_args<double>(L, y);
+    return fused_eval_launch<double>(a, L->def, L->alpha, (double*)L->L, L->spart, L->ns, L->flag,
+                                     (double*)grad, scal, s, e0, e1, part);
+}
+
 __global__ void k_finish_exact(const double* D, const double* S, double alpha, int* flag, double* out) {
     // J = D + alpha * S in python floats (objective.py:50-52); a non-finite trial point
     // gives J = inf to force a backtrack (objective.py:55-57)
@@ -383,10 +401,10 @@ static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_g
     if (!rc) {
         if (dtype == NGF_F32) {
             rc = pack_rt<float>((const float*)L->gR, (const float*)L->nR, n, L->RT, s);
-            if (!rc) rc = fused_setup<float>(L);
+            if (!rc) rc = fused_setup<float>(L, 0, (int)L->img.dims[2]);
         } else {
             rc = pack_rt<double>((const double*)L->gR, (const double*)L->nR, n, L->RT, s);
-            if (!rc) rc = fused_setup<double>(L);
+            if (!rc) rc = fused_setup<double>(L, 0, (int)L->img.dims[2]);
         }
     }
     if (rc) {
@@ -433,16 +451,26 @@ int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_de
         return L->dtype == NGF_F32 ? eval_exact<float>(L, y, grad, scalars_dev, s)
                                    : eval_exact<double>(L, y, grad, scalars_dev, s);
     }
-    if (mode != 0) return NGF_EARG;
-    cudaEvent_t e0 = L->timing ? L->ev[0] : nullptr, e1 = L->timing ? L->ev[1] : nullptr;
-    if (L->dtype == NGF_F32) {
-        FusedArgs<float> a = fused_args<float>(L, y);
-        return fused_eval_launch<float>(a, L->def, L->alpha, (float*)L->L, L->spart, L->ns,
-                                        L->flag, (float*)grad, scalars_dev, s, e0, e1);
-    }
-    FusedArgs<double> a = fused_args<double>(L, y);
-    return fused_eval_launch<double>(a, L->def, L->alpha, (double*)L->L, L->spart, L->ns,
-                                     L->flag, (double*)grad, scalars_dev, s, e0, e1);
+    if (mode != 0 && mode != 2) return NGF_EARG;
+    return fused_part(L, y, grad, scalars_dev, s, mode == 2 ? 1 : 0);
+}
+
+int ngf_level_add_curvature(ngf_level_t* L, const void* y, void* grad, double* scalars_dev,
+                            void* stream) {
+    if (!L || !y || !grad || !scalars_dev) return NGF_EARG;
+    return fused_part(L, y, grad, scalars_dev, as_stream(stream), 2);
+}
+
+int ngf_level_set_zrange(ngf_level_t* L, int64_t zlo, int64_t zhi) {
+    if (!L || zlo < 0 || zhi > L->img.dims[2] || zlo >= zhi) return NGF_EARG;
+    NGF_CUDA(cudaDeviceSynchronize());
+    void* bufs[] = {L->fp_blob, L->partial, L->dpart, L->spart, L->L};
+    for (void* b : bufs)
+        if (b) cudaFree(b);
+    L->fp_blob = L->partial = L->L = nullptr;
+    L->dpart = L->spart = nullptr;
+    return L->dtype == NGF_F32 ? fused_setup<float>(L, (int)zlo, (int)zhi)
+                               : fused_setup<double>(L, (int)zlo, (int)zhi);
 }
 
 int ngf_level_set_timing(ngf_level_t* L, int on) {
