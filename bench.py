@@ -38,6 +38,7 @@ WORKLOADS = {
     "c1": (64, 4, 1),
     "c2": (128, 4, 3),
     "c3": (256, 4, 4),
+    "c5": (512, 4, 4),  # z-slab decomposition over the ranks (strong scaling), evaluation only
 }
 
 
@@ -169,8 +170,8 @@ def run_reference(args):
     value = steps / dt
     line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": warm + 1, "ms_per_step": 1000 * dt / steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic", "impl": "reference",
+            "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair, {gd.dims[0]}^3 def grid, "
                                    "one LevelObjective evaluation per step"},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
@@ -198,13 +199,20 @@ def run_ours(args):
     dev_index = torch.cuda.current_device()
 
     n, ratio, levels = WORKLOADS[args.workload]
-    R, T, gd, y = make_inputs(n, ratio, seed=rank)
+    strong = args.workload == "c5"  # one pair split in z-slabs over all ranks
+    R, T, gd, y = make_inputs(n, ratio, seed=0 if strong else rank)
     gi = R.grid
     plan = ngf.build_gather_plan(gd, gi)
     T_dev = torch.from_numpy(T.values).cuda()
     R_dev = torch.from_numpy(R.values).cuda()
     obj = ngf.LevelObjective.from_device(T_dev, R_dev, plan, ngf.NgfParams(10.0, 10.0), 1.0)
     level = obj.level
+    zlo, zhi = 0, gi.dims[2]
+    evaluator = obj
+    if strong:
+        from paper_1812_06765_b200.distributed import DeviceSlab, SlabObjective, slab_ranges
+        zlo, zhi = slab_ranges(gi.dims[2], gd.dims[2], ws)[rank]
+        evaluator = SlabObjective(DeviceSlab(level, zlo, zhi))
     x = torch.from_numpy(y.ravel().copy()).cuda()
     g = torch.empty_like(x)
     sc = torch.zeros(3, dtype=torch.float64, device="cuda")
@@ -224,7 +232,7 @@ def run_ours(args):
 
     # ---------------- device-resident leg (value) ----------------
     for _ in range(max(3, args.warmup)):
-        obj.eval_device(x, g, sc)
+        evaluator.eval_device(x, g, sc)
     barrier()
     launches0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -232,18 +240,19 @@ def run_ours(args):
         barrier()
         e0.record(stream)
         for _ in range(args.steps):
-            obj.eval_device(x, g, sc)
+            evaluator.eval_device(x, g, sc)
         e1.record(stream)
         barrier()
     launches = _lib.launch_count() - launches0
     t_ms = max_over_ranks(e0.elapsed_time(e1))
-    value = ws * args.steps / (t_ms / 1000.0)
+    jobs = 1 if strong else ws  # evaluations completed per step, whole job
+    value = jobs * args.steps / (t_ms / 1000.0)
 
     # ---------------- fused kernel alone, CUDA events on the launching stream --------------
     _lib.check(_lib.lib().ngf_level_set_timing(level.handle, 1), "timing")
     kms = []
     for _ in range(max(5, min(args.steps, 50))):
-        obj.eval_device(x, g, sc)
+        evaluator.eval_device(x, g, sc)
         ms = ctypes.c_float()
         _lib.check(_lib.lib().ngf_level_kernel_ms(level.handle, ctypes.byref(ms)), "kernel_ms")
         kms.append(ms.value)
@@ -251,7 +260,7 @@ def run_ours(args):
     k_ms = float(np.mean(kms))
     info = (ctypes.c_int64 * 9)()
     _lib.check(_lib.lib().ngf_level_info(level.handle, info), "info")
-    N, M = gi.num_points, gd.num_points
+    N, M = gi.dims[0] * gi.dims[1] * (zhi - zlo), gd.num_points  # this rank's slab
     bytes_kernel = 20 * N + 12 * M          # T + packed reference terms + y
     bytes_eval = 20 * N + 24 * M            # + grad J written (B_eval)
     peak, peak_kind = peaks()
@@ -260,24 +269,39 @@ def run_ours(args):
 
     # ---------------- end to end through the numpy-facing LevelObjective -------------------
     y_host = y.ravel().copy()
+    if strong:
+        # public path of the slab decomposition: host y in, host (J, grad) out on every rank
+        x_pin = torch.from_numpy(y_host).pin_memory()
+        g_pin = torch.empty_like(x_pin).pin_memory()
+        s_pin = torch.empty(3, dtype=torch.float64).pin_memory()
+
+        def call(_):
+            x.copy_(x_pin, non_blocking=True)
+            evaluator.eval_device(x, g, sc)
+            g_pin.copy_(g, non_blocking=True)
+            s_pin.copy_(sc, non_blocking=True)
+            stream.synchronize()
+            return float(s_pin[0]), g_pin.numpy()
+    else:
+        call = obj  # LevelObjective.__call__: numpy in, (J, numpy grad) out
     for _ in range(2):
-        obj(y_host)
+        call(y_host)
     barrier()
     t0 = time.perf_counter()
     ee0 = torch.cuda.Event(enable_timing=True)
     ee1 = torch.cuda.Event(enable_timing=True)
     ee0.record(stream)
     for _ in range(args.steps):
-        J, gh = obj(y_host)
+        J, gh = call(y_host)
     ee1.record(stream)
     barrier()
     e2e_s = max_over_ranks(max(time.perf_counter() - t0, ee0.elapsed_time(ee1) / 1000.0))
-    e2e = {"value": ws * args.steps / e2e_s, "unit": "evals/s",
+    e2e = {"value": jobs * args.steps / e2e_s, "unit": "evals/s",
            "h2d_bytes_per_step": int(y_host.nbytes), "d2h_bytes_per_step": int(gh.nbytes + 24)}
 
     # ---------------- full coarse-to-fine registration (the paper's headline) -------------
     reg = None
-    if not args.no_register:
+    if not args.no_register and not strong:
         cfg = ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision="f32")
         ngf.register(R, T, cfg)  # warm-up (allocations, first-touch)
         barrier()
@@ -303,14 +327,16 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": eval_ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
+            "dtype": "f32",
             "data": "synthetic",
             "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair (1 mm), "
                                    f"{gd.dims[0]}^3 def grid, NGF tau=rho=10, alpha=1; one "
                                    "LevelObjective evaluation per step",
                        "l2": "inputs larger than L2 (T 4N + reference terms 16N = "
                              f"{(20 * N) / 1e6:.0f} MB > 126 MB)",
-                       "parallelism": f"replicas x{ws} (one independent pair per GPU)"},
+                       "parallelism": (f"z-slabs x{ws} (one pair; NCCL all-reduce of grad D and D)"
+                                       if strong else f"replicas x{ws} (one independent pair per GPU)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": None,
                          "kernel": "k_eval_fused", "kernel_ms": k_ms,

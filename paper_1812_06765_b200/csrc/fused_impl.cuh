@@ -68,64 +68,6 @@ __device__ __forceinline__ dbl4 ld_rt(const dbl4* p) {
     return r;
 }
 
-// Continuous template index along one axis: (p - o) / h with the reference's rounding
-// (warp.py:38).  Bit-exact, so inside/floor decisions match the reference.
-template <typename T>
-__device__ __forceinline__ T tcoord(T p, T o, T h, T ih, int pow2) {
-    const T d = sub_rn(p, o);
-    return pow2 ? mul_rn(d, ih) : div_rn(d, h);
-}
-
-template <typename T>
-__device__ __forceinline__ void axis_cell(T t, int n, bool& inside, int& lo, T& f) {
-    inside = inside && (t >= (T)0) && (t <= (T)(n - 1));
-    const T fl = floor(t);
-    const int hi = n - 2 > 0 ? n - 2 : 0;
-    if (!(fl >= (T)0))
-        lo = 0;
-    else if (fl > (T)hi)
-        lo = hi;
-    else
-        lo = (int)fl;
-    f = t - (T)lo;  // exact for inside samples (Sterbenz); outside samples are masked
-}
-
-// W = T(yhat) and the interpolant's spatial derivative / h (zero outside the hull)
-template <typename T>
-__device__ __forceinline__ void warp_point(const FusedArgs<T>& a, const T (&yh)[3], T& W, T& d0,
-                                           T& d1, T& d2) {
-    bool inside = true;
-    int ix, iy, iz;
-    T fx, fy, fz;
-    axis_cell(tcoord(yh[0], a.ox, a.hx, a.ihx, a.pow2x), a.nx, inside, ix, fx);
-    axis_cell(tcoord(yh[1], a.oy, a.hy, a.ihy, a.pow2y), a.ny, inside, iy, fy);
-    axis_cell(tcoord(yh[2], a.oz, a.hz, a.ihz, a.pow2z), a.nz, inside, iz, fz);
-    if (!inside) {
-        W = d0 = d1 = d2 = (T)0;
-        return;
-    }
-    const int64_t sx = a.nx > 1 ? 1 : 0;
-    const int64_t sy = a.ny > 1 ? a.nx : 0;
-    const int64_t sz = a.nz > 1 ? (int64_t)a.nx * a.ny : 0;
-    const T* b = a.Tv + ((int64_t)iz * a.ny + iy) * a.nx + ix;
-    const T c000 = __ldg(b), c100 = __ldg(b + sx);
-    const T c010 = __ldg(b + sy), c110 = __ldg(b + sy + sx);
-    const T c001 = __ldg(b + sz), c101 = __ldg(b + sz + sx);
-    const T c011 = __ldg(b + sz + sy), c111 = __ldg(b + sz + sy + sx);
-    // x differences and x-lerps on the four (y, z) edges
-    const T e00 = c100 - c000, e10 = c110 - c010, e01 = c101 - c001, e11 = c111 - c011;
-    const T a00 = fmaf_t(fx, e00, c000), a10 = fmaf_t(fx, e10, c010);
-    const T a01 = fmaf_t(fx, e01, c001), a11 = fmaf_t(fx, e11, c011);
-    const T dy0 = a10 - a00, dy1 = a11 - a01;
-    const T b0 = fmaf_t(fy, dy0, a00), b1 = fmaf_t(fy, dy1, a01);
-    const T dz = b1 - b0;
-    W = fmaf_t(fz, dz, b0);
-    const T ex0 = fmaf_t(fy, e10 - e00, e00), ex1 = fmaf_t(fy, e11 - e01, e01);
-    d0 = fmaf_t(fz, ex1 - ex0, ex0) * a.ihx;
-    d1 = fmaf_t(fz, dy1 - dy0, dy0) * a.ihy;
-    d2 = dz * a.ihz;
-}
-
 // Trilinear value and derivative / h from the 8 corners c[dx + 2 dy + 4 dz] (lerp form
 // of warp.py:79-85 and :111-120)
 template <typename T>
