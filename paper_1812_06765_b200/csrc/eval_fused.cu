@@ -15,7 +15,7 @@
 //       axes reordered z-first); when a deformation plane is complete, the CTA
 //       reduces it in x then y in a fixed order and writes its window partial.
 // yhat, W, grad W, q, s and ghat never leave the SM.  G^T and P^T are linear, so
-// ring voxels carry only this tile's contributions; k_reduce adds the tiles that
+// ring voxels carry only this tile's contributions; k_post adds the tiles that
 // share a deformation node in a fixed order (deterministic, no atomics).
 //
 // Shared memory has a compile-time layout (SmemL) so every access is one LDS/STS
@@ -543,154 +543,362 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
 
 // ------------------------------------------------------------------ reduce + curvature
 
-// Lu (3, M) of the displacement and per-block partial sums of (Lu)^2.  Grid: x/y tiles of
-// 32 x 8 nodes, blockIdx.z = comp * nz + k (32-bit index math only).
+// One kernel after the march: grad = grad D (fixed-order sum of the covering tiles'
+// partials) + alpha * vol * L^T L u (curvature.py:74-81), the per-block partial sums of
+// (L u)^2, and -- in the last block to finish -- the fixed-order totals J, D, S.
+// Grid: x/y tiles of 32 x 8 deformation nodes, blockIdx.z = comp * nchunk + z chunk.
+template <typename T>
+struct PostArgs {
+    GridK<T> g;
+    FusedPlan fp;
+    const T* partial;  // null: no grad D term (curvature added to an all-reduced grad D)
+    const T* y;        // null: no curvature term (z-slab partial)
+    T vol, alpha;
+    T* grad;
+    int accumulate;    // grad += ... instead of grad = ...
+    const double* dpart;
+    int nd;
+    double* spart;
+    int* flag;         // [0] non-finite y seen, [1] finished-block counter
+    double half_hbar, half_vol, dalpha;
+    double* out;
+    int mode;          // 0 full, 1 slab partial, 2 add curvature (see post_finalize)
+    int nchunk;        // z chunks of kPostKZ planes per component
+    T ihx2, ihy2, ihz2;  // 1 / h^2 in the working dtype (curvature.py:28-29)
+};
+
 template <typename T>
 __device__ __forceinline__ T ident(double o, double h, int i) {
     return (T)(o + h * (double)i);  // identity_field_array: f64 centres cast (geometry.py:148-155)
 }
 
+// fixed-order totals, reduced by one block (256 threads, strided then warp tree):
+// mode 0: J = D + alpha S from both partial sets; 1: D only (slab partial, J = D, S = 0);
+// 2: D already in out[1] (all-reduced over slabs), S from spart
 template <typename T>
-__global__ void __launch_bounds__(256) k_curv_L(GridK<T> g, const T* __restrict__ y, T* __restrict__ L,
-                                                double* __restrict__ spart, int* __restrict__ flag) {
-    const int i = blockIdx.x * 32 + threadIdx.x;
-    const int j = blockIdx.y * 8 + threadIdx.y;
-    const int comp = blockIdx.z / g.nz, k = blockIdx.z - comp * g.nz;
-    const unsigned m = (unsigned)g.nx * g.ny * g.nz;
-    const unsigned sy = g.nx, sz = (unsigned)g.nx * g.ny;
-    double acc = 0.0;
-    bool bad = false;
-    if (i < g.nx && j < g.ny) {
-        const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
-        const unsigned idx = (unsigned)k * sz + (unsigned)j * sy + (unsigned)i;
-        const T* yc = y + (size_t)comp * m;
-        // displacement u = y - id; id varies only along the component's own axis
-        const double o = comp == 0 ? g.dox : (comp == 1 ? g.doy : g.doz);
-        const double h = comp == 0 ? g.dhx : (comp == 1 ? g.dhy : g.dhz);
-        const int own = comp == 0 ? i : (comp == 1 ? j : k);
-        const T id0 = ident<T>(o, h, own);
-        const T yv = yc[idx];
-        bad = !isfinite(yv);
-        const T u0 = yv - id0;
-        T lap = (T)0;
-        if (g.nx >= 3 && i > 0 && i < g.nx - 1) {
-            const T idm = comp == 0 ? ident<T>(o, h, i - 1) : id0, idp = comp == 0 ? ident<T>(o, h, i + 1) : id0;
-            lap += ((yc[idx + 1] - idp) - (T)2 * u0 + (yc[idx - 1] - idm)) * ihx2;
-        }
-        if (g.ny >= 3 && j > 0 && j < g.ny - 1) {
-            const T idm = comp == 1 ? ident<T>(o, h, j - 1) : id0, idp = comp == 1 ? ident<T>(o, h, j + 1) : id0;
-            lap += ((yc[idx + sy] - idp) - (T)2 * u0 + (yc[idx - sy] - idm)) * ihy2;
-        }
-        if (g.nz >= 3 && k > 0 && k < g.nz - 1) {
-            const T idm = comp == 2 ? ident<T>(o, h, k - 1) : id0, idp = comp == 2 ? ident<T>(o, h, k + 1) : id0;
-            lap += ((yc[idx + sz] - idp) - (T)2 * u0 + (yc[idx - sz] - idm)) * ihz2;
-        }
-        L[(size_t)comp * m + idx] = lap;
-        acc = (double)lap * (double)lap;
-    }
-    __shared__ double red[8];
-    const int tid = threadIdx.y * 32 + threadIdx.x;
-    if (__syncthreads_or(bad) && tid == 0) atomicOr(flag, 1);
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (threadIdx.x == 0) red[threadIdx.y] = acc;
-    __syncthreads();
-    if (tid == 0) {
-        double s = 0.0;
-        for (int w = 0; w < 8; ++w) s += red[w];
-        spart[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = s;
-    }
-}
-
-template <typename T>
-__device__ __forceinline__ T d2t(const T* w, unsigned idx, int i, int n, unsigned stride, T ih2) {
-    if (n < 3) return (T)0;
-    T o = (T)0;
-    if (i <= n - 3) o += w[idx + stride];
-    if (i >= 1 && i <= n - 2) o -= (T)2 * w[idx];
-    if (i >= 2) o += w[idx - stride];
-    return o * ih2;
-}
-
-// grad = grad D (fixed-order sum of the covering tiles' partials) + alpha * vol * L^T L u
-template <typename T>
-__global__ void __launch_bounds__(256) k_reduce(GridK<T> g, const FusedPlan fp,
-                                                const T* __restrict__ partial, const T* __restrict__ L,
-                                                T vol, T alpha, T* __restrict__ grad, int accumulate) {
-    const int i = blockIdx.x * 32 + threadIdx.x;
-    const int j = blockIdx.y * 8 + threadIdx.y;
-    const int comp = blockIdx.z / g.nz, k = blockIdx.z - comp * g.nz;
-    if (i >= g.nx || j >= g.ny) return;
-    const unsigned m = (unsigned)g.nx * g.ny * g.nz;
-    const unsigned sy = g.nx, sz = (unsigned)g.nx * g.ny;
-    const unsigned idx = (unsigned)k * sz + (unsigned)j * sy + (unsigned)i;
-    const int win = fp.wz * fp.wy * fp.wx;
-    T gd = accumulate ? grad[(size_t)comp * m + idx] : (T)0;
-    if (partial) {
-    const int32_t* cz = fp.cov_z + k * kCover * 2;
-    const int32_t* cy = fp.cov_y + j * kCover * 2;
-    const int32_t* cx = fp.cov_x + i * kCover * 2;
-    for (int az = 0; az < kCover && cz[2 * az] >= 0; ++az) {
-        for (int ay = 0; ay < kCover && cy[2 * ay] >= 0; ++ay) {
-            const int rowc = (cz[2 * az] * fp.nty + cy[2 * ay]) * fp.ntx;
-            const int rowo = (cz[2 * az + 1] * fp.wy + cy[2 * ay + 1]) * fp.wx;
-            for (int ax = 0; ax < kCover && cx[2 * ax] >= 0; ++ax) {
-                const int cta = rowc + cx[2 * ax];
-                gd += __ldg(partial + ((size_t)cta * 3 + comp) * win + rowo + cx[2 * ax + 1]);
-            }
-        }
-    }
-    }
-    if (!L) {  // partial gradient of a z-slab: no curvature term
-        grad[(size_t)comp * m + idx] = gd;
-        return;
-    }
-    // grad S = vol * L^T L u (curvature.py:74-81)
-    const T ihx2 = (T)1 / (g.hx * g.hx), ihy2 = (T)1 / (g.hy * g.hy), ihz2 = (T)1 / (g.hz * g.hz);
-    const T* Lc = L + (size_t)comp * m;
-    const T lt = d2t(Lc, idx, i, g.nx, 1u, ihx2) + d2t(Lc, idx, j, g.ny, sy, ihy2) +
-                 d2t(Lc, idx, k, g.nz, sz, ihz2);
-    grad[(size_t)comp * m + idx] = gd + alpha * (vol * lt);
-}
-
-template <typename T>
-__global__ void k_finalize(const double* __restrict__ dpart, int nd, const double* __restrict__ spart,
-                           int ns, double half_hbar, double half_vol, double alpha, int* flag,
-                           double* __restrict__ out, int mode) {
-    // mode 0: J = D + alpha S from both partial sets; 1: D only (slab partial, J = D, S = 0);
-    // 2: D already in out[1] (all-reduced over slabs), S from spart
-    // fixed-order sums; D and S rounded like the reference's dtype products
+__device__ void post_finalize(const PostArgs<T>& p, int ns) {
     __shared__ double red[2][32];
+    const int tid = threadIdx.y * blockDim.x + threadIdx.x, nt = blockDim.x * blockDim.y;
     double a = 0.0, b = 0.0;
-    for (int t = threadIdx.x; t < nd; t += blockDim.x) a += dpart[t];
-    for (int t = threadIdx.x; t < ns; t += blockDim.x) b += spart[t];
+#pragma unroll 8
+    for (int t = tid; t < p.nd; t += nt) a += __ldcg(p.dpart + t);
+    if (p.mode != 1) {
+#pragma unroll 8
+        for (int t = tid; t < ns; t += nt) b += __ldcg(p.spart + t);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
         a += __shfl_xor_sync(0xffffffffu, a, o);
         b += __shfl_xor_sync(0xffffffffu, b, o);
     }
-    if ((threadIdx.x & 31) == 0) {
-        red[0][threadIdx.x >> 5] = a;
-        red[1][threadIdx.x >> 5] = b;
+    if ((tid & 31) == 0) {
+        red[0][tid >> 5] = a;
+        red[1][tid >> 5] = b;
     }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (tid == 0) {
         double sa = 0.0, sb = 0.0;
-        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+        for (int w = 0; w < (nt >> 5); ++w) {
             sa += red[0][w];
             sb += red[1][w];
         }
-        const double D = mode == 2 ? out[1] : (double)((T)half_hbar * (T)sa);
-        const double S = mode == 1 ? 0.0 : (double)((T)half_vol * (T)sb);
+        const double D = p.mode == 2 ? p.out[1] : (double)((T)p.half_hbar * (T)sa);
+        const double S = p.mode == 1 ? 0.0 : (double)((T)p.half_vol * (T)sb);
         // a non-finite trial point gives J = inf (objective.py:55-57)
-        if (mode == 1) {
-            out[0] = D;
+        if (p.mode == 1) {
+            p.out[0] = D;
         } else {
-            out[0] = *flag ? INFINITY : D + alpha * S;
-            *flag = 0;
+            const int bad = atomicOr(p.flag, 0);
+            p.out[0] = bad ? INFINITY : D + p.dalpha * S;
+            p.flag[0] = 0;
         }
-        out[1] = D;
-        out[2] = S;
+        p.out[1] = D;
+        p.out[2] = S;
+        p.flag[1] = 0;  // re-arm the block counter for the next launch
+    }
+}
+
+template <typename T>
+__device__ __forceinline__ T d2t_at(T lm, T l0, T lp, int i, int n, T ih2) {
+    // (L^T w)_i of the 1-D second difference with zero face rows (curvature.py:33-43)
+    if (n < 3) return (T)0;
+    T o = (T)0;
+    if (i <= n - 3) o += lp;
+    if (i >= 1 && i <= n - 2) o -= (T)2 * l0;
+    if (i >= 2) o += lm;
+    return o * ih2;
+}
+
+// k_post: one block = a 32 x 8 tile of deformation nodes on KZ consecutive planes of one
+// component.  All global loads -- the slot masks, the covering slots' partials and
+// u = y - id on the 36 x 12 x (KZ + 4) neighbourhood -- are issued before the first
+// barrier, so a block costs about two memory round trips; L u is then formed once per
+// node of the 34 x 10 x (KZ + 2) tile in shared memory.
+// k_post: one block = a 32 x 8 tile of deformation nodes on KZ consecutive planes of one
+// component.  u = y - id on the 36 x 12 x (KZ + 4) neighbourhood and the cover lists are
+// loaded and L u is formed (once per node of the 34 x 10 x (KZ + 2) tile) before the
+// kernel waits for the fused march (programmatic dependent launch, so this part overlaps
+// the march's last wave); then the covering tiles' partials of all KZ planes are loaded
+// together and summed in a fixed order.
+constexpr int kPostKZ = 4;
+constexpr int kPostUX = 36, kPostUY = 12, kPostLX = 34, kPostLY = 10;
+
+template <typename T>
+__device__ __forceinline__ T cover_sum_loop(const FusedPlan& fp, const T* __restrict__ partial, int comp,
+                                            int i, int j, int k) {
+    // general cover lists (short fused z chunks, tiny tiles): fixed order az, ay, ax
+    const int win = fp.wz * fp.wy * fp.wx;
+    const int32_t* gx = fp.cov_x + i * kCover * 2;
+    const int32_t* gy = fp.cov_y + j * kCover * 2;
+    const int32_t* gz = fp.cov_z + k * kCover * 2;
+    T gd = (T)0;
+    for (int az = 0; az < kCover && gz[2 * az] >= 0; ++az)
+        for (int ay = 0; ay < kCover && gy[2 * ay] >= 0; ++ay) {
+            const int rowc = (gz[2 * az] * fp.nty + gy[2 * ay]) * fp.ntx;
+            const int rowo = (gz[2 * az + 1] * fp.wy + gy[2 * ay + 1]) * fp.wx;
+            for (int ax = 0; ax < kCover && gx[2 * ax] >= 0; ++ax)
+                gd += __ldcg(partial + ((size_t)(rowc + gx[2 * ax]) * 3 + comp) * win + rowo + gx[2 * ax + 1]);
+        }
+    return gd;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArgs<T> p) {
+    constexpr int KZ = kPostKZ, NU = KZ + 4, NL = KZ + 2;
+    constexpr int UPT = (kPostUX * kPostUY + 255) / 256;  // u items per thread and plane
+    constexpr int LPT = (kPostLX * kPostLY + 255) / 256;  // L items per thread and plane
+    __shared__ T us[NU][kPostUY][kPostUX];
+    __shared__ T ls[NL][kPostLY][kPostLX];
+    __shared__ long long zsh[KZ][4];  // first four z covers of each plane: partial offset or -1
+    __shared__ int zslow[KZ];         // plane with more than four z covers
+    __shared__ double red[8];
+    __shared__ int last;
+    const GridK<T>& g = p.g;
+    const FusedPlan& fp = p.fp;
+    const int tid = threadIdx.y * 32 + threadIdx.x;
+    const int nblk = gridDim.x * gridDim.y * gridDim.z;
+    const int bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+    const int comp = blockIdx.z / p.nchunk, chunk = blockIdx.z - comp * p.nchunk;
+    const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
+    const int k0 = chunk * KZ;
+    const int i = x0 + threadIdx.x, j = y0 + threadIdx.y;
+    const bool mine = i < g.nx && j < g.ny;
+    const unsigned m = (unsigned)g.nx * g.ny * g.nz;
+    const T* yc = p.y ? p.y + (size_t)comp * m : nullptr;
+    const int win = fp.wz * fp.wy * fp.wx;
+
+    // ---- (1) cover lists: z covers are block-uniform (smem), x / y covers per thread
+    if (p.partial && tid < KZ) {
+        const int k = k0 + tid;
+        long long o[4] = {-1, -1, -1, -1};
+        int slow = 0;
+        if (k < g.nz) {
+            const int32_t* c = fp.cov_z + k * kCover * 2;
+            const int4 v0 = __ldg(reinterpret_cast<const int4*>(c)), v1 = __ldg(reinterpret_cast<const int4*>(c) + 1);
+            const int zt[4] = {v0.x, v0.z, v1.x, v1.z}, zo[4] = {v0.y, v0.w, v1.y, v1.w};
+            const long long plane = (long long)fp.nty * fp.ntx * 3 * win;
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+                if (zt[a] >= 0) o[a] = zt[a] * plane + (long long)zo[a] * fp.wy * fp.wx;
+            slow = __ldg(c + 8) >= 0;
+        }
+#pragma unroll
+        for (int a = 0; a < 4; ++a) zsh[tid][a] = o[a];
+        zslow[tid] = slow;
+    }
+    int bxy[2][2];  // ((y tile * ntx + x tile) * 3 + comp) * win + window offset, or -1
+    bool xyslow = false;
+    if (p.partial && mine) {
+        const int4 xv = __ldg(reinterpret_cast<const int4*>(fp.cov_x + i * kCover * 2));
+        const int4 yv = __ldg(reinterpret_cast<const int4*>(fp.cov_y + j * kCover * 2));
+        xyslow = __ldg(fp.cov_x + i * kCover * 2 + 4) >= 0 || __ldg(fp.cov_y + j * kCover * 2 + 4) >= 0;
+        const int cxt[2] = {xv.x, xv.z}, cxo[2] = {xv.y, xv.w};
+        const int cyt[2] = {yv.x, yv.z}, cyo[2] = {yv.y, yv.w};
+#pragma unroll
+        for (int ay = 0; ay < 2; ++ay)
+#pragma unroll
+            for (int ax = 0; ax < 2; ++ax)
+                bxy[ay][ax] = (cyt[ay] >= 0 && cxt[ax] >= 0)
+                                  ? ((cyt[ay] * fp.ntx + cxt[ax]) * 3 + comp) * win + cyo[ay] * fp.wx + cxo[ax]
+                                  : -1;
+    }
+
+    // ---- (2) u = y - id on planes k0-2 .. k0+KZ+1 (clamped; out-of-grid values unused)
+    double acc = 0.0;
+    bool bad = false;
+    if (yc) {
+        const double o = comp == 0 ? g.dox : (comp == 1 ? g.doy : g.doz);
+        const double h = comp == 0 ? g.dhx : (comp == 1 ? g.dhy : g.dhz);
+        int uoff[UPT];
+        T idr[UPT];
+#pragma unroll
+        for (int r = 0; r < UPT; ++r) {
+            const int t = min(tid + r * 256, kPostUX * kPostUY - 1);
+            const int ey = t / kPostUX, ex = t - ey * kPostUX;
+            const int a = min(max(x0 - 2 + ex, 0), g.nx - 1), b = min(max(y0 - 2 + ey, 0), g.ny - 1);
+            uoff[r] = b * g.nx + a;
+            idr[r] = ident<T>(o, h, comp == 0 ? a : b);
+        }
+        T uv[NU][UPT];
+#pragma unroll
+        for (int q = 0; q < NU; ++q) {
+            const int zc = min(max(k0 - 2 + q, 0), g.nz - 1);
+            const T* yp = yc + (unsigned)zc * (unsigned)(g.nx * g.ny);
+#pragma unroll
+            for (int r = 0; r < UPT; ++r) uv[q][r] = __ldg(yp + uoff[r]);
+        }
+#pragma unroll
+        for (int q = 0; q < NU; ++q) {
+            const T idz = ident<T>(o, h, min(max(k0 - 2 + q, 0), g.nz - 1));
+#pragma unroll
+            for (int r = 0; r < UPT; ++r) {
+                const int t = tid + r * 256;
+                if (t < kPostUX * kPostUY) (&us[q][0][0])[t] = uv[q][r] - (comp == 2 ? idz : idr[r]);
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- (3) L u on planes k0-1 .. k0+KZ over the 34 x 10 tile: second differences x, y, z
+    // with zero rows at the faces (curvature.py:20-30)
+    if (yc) {
+#pragma unroll
+        for (int r = 0; r < LPT; ++r) {
+            const int t = tid + r * 256;
+            if (t < kPostLX * kPostLY) {
+                const int ly = t / kPostLX, lx = t - ly * kPostLX;
+                const int a = x0 - 1 + lx, b = y0 - 1 + ly;
+                const bool fx = g.nx >= 3 && a > 0 && a < g.nx - 1, fy = g.ny >= 3 && b > 0 && b < g.ny - 1;
+                const int ux = lx + 1, uy = ly + 1;
+#pragma unroll
+                for (int q = 0; q < NL; ++q) {
+                    const int z = k0 - 1 + q, uz = q + 1;
+                    const T c = us[uz][uy][ux];
+                    T lap = (T)0;
+                    if (fx) lap += (us[uz][uy][ux + 1] - (T)2 * c + us[uz][uy][ux - 1]) * p.ihx2;
+                    if (fy) lap += (us[uz][uy + 1][ux] - (T)2 * c + us[uz][uy - 1][ux]) * p.ihy2;
+                    if (g.nz >= 3 && z > 0 && z < g.nz - 1)
+                        lap += (us[uz + 1][uy][ux] - (T)2 * c + us[uz - 1][uy][ux]) * p.ihz2;
+                    ls[q][ly][lx] = lap;
+                }
+            }
+        }
+        __syncthreads();
+    }
+
+    // ---- (4) the fused march's outputs are needed from here on (programmatic dependent
+    // launch: everything above overlaps the march's tail)
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the covering tiles' partials of the KZ planes: first two covers per axis, all loads
+    // in flight together (fixed order az, ay, ax)
+    T pv[KZ][2][2][2];
+    if (p.partial && mine && !xyslow) {
+#pragma unroll
+        for (int q = 0; q < KZ; ++q)
+#pragma unroll
+            for (int az = 0; az < 2; ++az) {
+                const long long zo = zsh[q][az];
+#pragma unroll
+                for (int ay = 0; ay < 2; ++ay)
+#pragma unroll
+                    for (int ax = 0; ax < 2; ++ax)
+                        pv[q][az][ay][ax] = (zo >= 0 && bxy[ay][ax] >= 0) ? __ldcg(p.partial + zo + bxy[ay][ax]) : (T)0;
+            }
+    }
+
+    // ---- (5) outputs
+    T gdp[KZ];
+#pragma unroll
+    for (int q = 0; q < KZ; ++q) gdp[q] = (T)0;
+    if (p.partial && mine) {
+        if (xyslow) {
+#pragma unroll
+            for (int q = 0; q < KZ; ++q)
+                if (k0 + q < g.nz) gdp[q] = cover_sum_loop<T>(fp, p.partial, comp, i, j, k0 + q);
+        } else {
+#pragma unroll
+            for (int q = 0; q < KZ; ++q)
+#pragma unroll
+                for (int az = 0; az < 2; ++az)
+#pragma unroll
+                    for (int ay = 0; ay < 2; ++ay)
+#pragma unroll
+                        for (int ax = 0; ax < 2; ++ax)
+                            if (zsh[q][az] >= 0 && bxy[ay][ax] >= 0) gdp[q] += pv[q][az][ay][ax];
+            bool more = false;  // short fused z chunks: covers 3 and 4 (block-uniform)
+#pragma unroll
+            for (int q = 0; q < KZ; ++q) more |= zsh[q][2] >= 0;
+            if (more) {
+#pragma unroll
+                for (int q = 0; q < KZ; ++q)
+#pragma unroll
+                    for (int az = 0; az < 2; ++az) {
+                        const long long zo = zsh[q][2 + az];
+#pragma unroll
+                        for (int ay = 0; ay < 2; ++ay)
+#pragma unroll
+                            for (int ax = 0; ax < 2; ++ax)
+                                pv[q][az][ay][ax] = (zo >= 0 && bxy[ay][ax] >= 0) ? __ldcg(p.partial + zo + bxy[ay][ax]) : (T)0;
+                    }
+#pragma unroll
+                for (int q = 0; q < KZ; ++q)
+#pragma unroll
+                    for (int az = 0; az < 2; ++az)
+#pragma unroll
+                        for (int ay = 0; ay < 2; ++ay)
+#pragma unroll
+                            for (int ax = 0; ax < 2; ++ax)
+                                if (zsh[q][2 + az] >= 0 && bxy[ay][ax] >= 0) gdp[q] += pv[q][az][ay][ax];
+            }
+#pragma unroll
+            for (int q = 0; q < KZ; ++q)  // more than four z covers: the general loop
+                if (zslow[q]) gdp[q] = cover_sum_loop<T>(fp, p.partial, comp, i, j, k0 + q);
+        }
+    }
+    if (mine) {
+#pragma unroll
+        for (int q = 0; q < KZ; ++q) {
+            const int k = k0 + q;
+            if (k >= g.nz) break;
+            const unsigned idx = ((unsigned)k * g.ny + (unsigned)j) * g.nx + (unsigned)i;
+            T gd = p.accumulate ? p.grad[(size_t)comp * m + idx] : (T)0;
+            if (p.partial) gd += gdp[q];
+            if (yc) {
+                // grad S = vol * L^T L u (curvature.py:74-81)
+                const int lx = threadIdx.x + 1, ly = threadIdx.y + 1, lz = q + 1;
+                const T lc = ls[lz][ly][lx];
+                bad |= !isfinite(us[lz + 1][ly + 1][lx + 1]);
+                acc += (double)lc * (double)lc;
+                T lt = (T)0;
+                if (g.nx >= 3) lt = d2t_at<T>(ls[lz][ly][lx - 1], lc, ls[lz][ly][lx + 1], i, g.nx, p.ihx2);
+                if (g.ny >= 3) lt = lt + d2t_at<T>(ls[lz][ly - 1][lx], lc, ls[lz][ly + 1][lx], j, g.ny, p.ihy2);
+                if (g.nz >= 3) lt = lt + d2t_at<T>(ls[lz - 1][ly][lx], lc, ls[lz + 1][ly][lx], k, g.nz, p.ihz2);
+                gd = gd + p.alpha * (p.vol * lt);
+            }
+            p.grad[(size_t)comp * m + idx] = gd;
+        }
+    }
+    if (__syncthreads_or(bad) && tid == 0) atomicOr(p.flag, 1);
+    if (yc) {
+#pragma unroll
+        for (int off = 16; off > 0; off >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+        if (threadIdx.x == 0) red[threadIdx.y] = acc;
+        __syncthreads();
+        if (tid == 0) {
+            double s = 0.0;
+            for (int w = 0; w < 8; ++w) s += red[w];
+            p.spart[bid] = s;
+        }
+    }
+    // last block done: fixed-order totals
+    if (tid == 0) {
+        __threadfence();
+        last = atomicAdd(p.flag + 1, 1) == nblk - 1;
+    }
+    __syncthreads();
+    if (last) {
+        __threadfence();
+        post_finalize<T>(p, nblk);
     }
 }
 
@@ -787,26 +995,61 @@ void launch_variant<double>(const FusedArgs<double>& a, cudaStream_t s) {
 }
 
 template <typename T>
-int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, T* L, double* spart,
-                      int ns, int* flag, T* grad, double* scalars, cudaStream_t s,
-                      cudaEvent_t ev0, cudaEvent_t ev1, int part) {
+int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns,
+                      int* flag, T* grad, double* scalars, cudaStream_t s, cudaEvent_t ev0,
+                      cudaEvent_t ev1, int part) {
     // part 0: full evaluation; 1: NGF partial of the level's z-slab (grad <- grad D_slab,
     // scalars <- D_slab); 2: add curvature to an all-reduced (grad D, D) in place
-    GridK<T> gk = make_gridk<T>(dg);
-    const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * dg.dims[2]);
+    const int nchunk = (int)((dg.dims[2] + kPostKZ - 1) / kPostKZ);
+    const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * nchunk);
     const int nsb = (int)(cgrid.x * cgrid.y * cgrid.z);
     if (nsb > ns) return NGF_EARG;
     const double vol = dg.spacing[0] * dg.spacing[1] * dg.spacing[2];
-    if (part != 1) NGF_LAUNCH(k_curv_L<T>, cgrid, dim3(32, 8), 0, s, gk, a.y, L, spart, flag);
     if (part != 2) {
         if (ev0) cudaEventRecord(ev0, s);
         launch_variant<T>(a, s);
         if (ev1) cudaEventRecord(ev1, s);
     }
-    NGF_LAUNCH(k_reduce<T>, cgrid, dim3(32, 8), 0, s, gk, a.fp, part == 2 ? nullptr : a.partial,
-               part == 1 ? nullptr : L, (T)vol, (T)alpha, grad, part == 2 ? 1 : 0);
-    NGF_LAUNCH(k_finalize<T>, 1, 256, 0, s, a.dpart, a.fp.n_cta, spart, nsb, a.half_hbar, vol / 2,
-               alpha, flag, scalars, part);
+    PostArgs<T> p;
+    p.g = make_gridk<T>(dg);
+    p.fp = a.fp;
+    p.partial = part == 2 ? nullptr : a.partial;
+    p.y = part == 1 ? nullptr : a.y;
+    p.vol = (T)vol;
+    p.alpha = (T)alpha;
+    p.grad = grad;
+    p.accumulate = part == 2 ? 1 : 0;
+    p.dpart = a.dpart;
+    p.nd = a.fp.n_cta;
+    p.spart = spart;
+    p.flag = flag;
+    p.half_hbar = a.half_hbar;
+    p.half_vol = vol / 2;
+    p.dalpha = alpha;
+    p.out = scalars;
+    p.mode = part;
+    p.nchunk = nchunk;
+    p.ihx2 = (T)1 / (p.g.hx * p.g.hx);
+    p.ihy2 = (T)1 / (p.g.hy * p.g.hy);
+    p.ihz2 = (T)1 / (p.g.hz * p.g.hz);
+    if (part == 2) {
+        NGF_LAUNCH(k_post<T>, cgrid, dim3(32, 8), 0, s, p);
+    } else {
+        // programmatic dependent launch after the march
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = cgrid;
+        cfg.blockDim = dim3(32, 8);
+        cfg.dynamicSmemBytes = 0;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        ::ngf::g_launches.fetch_add(1, std::memory_order_relaxed);
+        const cudaError_t e = cudaLaunchKernelEx(&cfg, k_post<T>, p);
+        if (e != cudaSuccess) return (int)e;
+    }
     NGF_CHECK_LAUNCH();
     return 0;
 }
@@ -835,12 +1078,12 @@ int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s) {
 }
 
 
-template int fused_eval_launch<float>(const FusedArgs<float>&, const ngf_grid_t&, double, float*,
-                                      double*, int, int*, float*, double*, cudaStream_t,
-                                      cudaEvent_t, cudaEvent_t, int);
+template int fused_eval_launch<float>(const FusedArgs<float>&, const ngf_grid_t&, double, double*, int,
+                                      int*, float*, double*, cudaStream_t, cudaEvent_t, cudaEvent_t,
+                                      int);
 template int fused_eval_launch<double>(const FusedArgs<double>&, const ngf_grid_t&, double, double*,
-                                       double*, int, int*, double*, double*, cudaStream_t,
-                                       cudaEvent_t, cudaEvent_t, int);
+                                       int, int*, double*, double*, cudaStream_t, cudaEvent_t,
+                                       cudaEvent_t, int);
 template size_t fused_smem<float>(int, int, int);
 template size_t fused_smem<double>(int, int, int);
 template int pack_rt<float>(const float*, const float*, int64_t, void*, cudaStream_t);

@@ -104,9 +104,9 @@ __device__ __forceinline__ void ngf_q(const FusedArgs<T>& a, T gx, T gy, T gz, c
 }
 
 template <typename T>
-int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, T* L, double* spart,
-                      int ns, int* flag, T* grad, double* scalars, cudaStream_t s,
-                      cudaEvent_t ev0 = nullptr, cudaEvent_t ev1 = nullptr, int part = 0);
+int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns,
+                      int* flag, T* grad, double* scalars, cudaStream_t s, cudaEvent_t ev0 = nullptr,
+                      cudaEvent_t ev1 = nullptr, int part = 0);
 template <typename T> int fused_prepare(int variant, size_t smem);
 template <typename T> size_t fused_smem(int variant, int wx, int wy);
 void fused_variant_geom(int variant, int* ty, int* nthreads);

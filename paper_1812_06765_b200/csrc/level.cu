@@ -42,10 +42,9 @@ struct ngf_level {
     void* fp_blob;   // device: windows + covers
     void* partial;   // n_cta x 3 x wz x wy x wx
     double* dpart;   // n_cta
-    double* spart;   // one partial per k_curv_L block
-    int ns;          // number of k_curv_L blocks
-    void* L;         // 3M
-    int* flag;       // non-finite y seen in this evaluation
+    double* spart;   // one (L u)^2 partial per k_post block
+    int ns;          // capacity of spart (>= k_post blocks)
+    int* flag;       // [0] non-finite y seen in this evaluation, [1] k_post block counter
     int timing;      // record events around the fused kernel
     cudaEvent_t ev[2];
     ngf::LevelWork ex;
@@ -225,7 +224,6 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     NGF_CUDA(cudaMalloc(&L->dpart, (size_t)fp.n_cta * sizeof(double)));
     L->ns = (int)(((L->def.dims[0] + 31) / 32) * ((L->def.dims[1] + 7) / 8) * 3 * L->def.dims[2]);
     NGF_CUDA(cudaMalloc(&L->spart, (size_t)L->ns * sizeof(double)));
-    NGF_CUDA(cudaMalloc(&L->L, (size_t)3 * grid_n(L->def) * sizeof(T)));
     return fused_prepare<T>(variant, fp.smem_bytes);
 }
 
@@ -303,11 +301,11 @@ static int fused_part(ngf_level* L, const void* y, void* grad, double* scal, cud
     cudaEvent_t e0 = L->timing ? L->ev[0] : nullptr, e1 = L->timing ? L->ev[1] : nullptr;
     if (L->dtype == NGF_F32) {
         FusedArgs<float> a = fused_args<float>(L, y);
-        return fused_eval_launch<float>(a, L->def, L->alpha, (float*)L->L, L->spart, L->ns, L->flag,
+        return fused_eval_launch<float>(a, L->def, L->alpha, L->spart, L->ns, L->flag,
                                         (float*)grad, scal, s, e0, e1, part);
     }
     FusedArgs<double> a = fused_args<double>(L, y);
-    return fused_eval_launch<double>(a, L->def, L->alpha, (double*)L->L, L->spart, L->ns, L->flag,
+    return fused_eval_launch<double>(a, L->def, L->alpha, L->spart, L->ns, L->flag,
                                      (double*)grad, scal, s, e0, e1, part);
 }
 
@@ -433,7 +431,7 @@ int ngf_level_create_terms(const ngf_grid_t* img_grid, const ngf_grid_t* def_gri
 void ngf_level_destroy(ngf_level_t* L) {
     if (!L) return;
     if (L->plan) ngf_plan_destroy(L->plan);
-    void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart, L->L,
+    void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart,
                     L->ex.yhat, L->ex.W, L->ex.terms, L->ex.q, L->ex.s, L->ex.ghat, L->ex.gD,
                     L->ex.cws, L->ex.dws};
     for (void* b : bufs)
@@ -464,10 +462,10 @@ int ngf_level_add_curvature(ngf_level_t* L, const void* y, void* grad, double* s
 int ngf_level_set_zrange(ngf_level_t* L, int64_t zlo, int64_t zhi) {
     if (!L || zlo < 0 || zhi > L->img.dims[2] || zlo >= zhi) return NGF_EARG;
     NGF_CUDA(cudaDeviceSynchronize());
-    void* bufs[] = {L->fp_blob, L->partial, L->dpart, L->spart, L->L};
+    void* bufs[] = {L->fp_blob, L->partial, L->dpart, L->spart};
     for (void* b : bufs)
         if (b) cudaFree(b);
-    L->fp_blob = L->partial = L->L = nullptr;
+    L->fp_blob = L->partial = nullptr;
     L->dpart = L->spart = nullptr;
     return L->dtype == NGF_F32 ? fused_setup<float>(L, (int)zlo, (int)zhi)
                                : fused_setup<double>(L, (int)zlo, (int)zhi);
