@@ -24,6 +24,7 @@
 // the exact one-sided coefficients (warp.py:139-142, :168-175).
 
 #include <cstdlib>
+#include <type_traits>
 #include <vector>
 
 #include "common.cuh"
@@ -105,6 +106,7 @@ struct March {
     int P2[C::S];       // index in the zero-padded q layout
     unsigned ij[C::S];  // j * nx + i of the image column (offset inside a plane)
     unsigned flags;     // per slot s, bits 4s..4s+3: in volume (x/y), tile interior, x face, y face
+    bool wface;         // some lane of the warp has a slot next to a volume face
     T ylo[C::S][3], yhi[C::S][3];  // P_xy y on the current def-plane pair
     T dT[C::S][3][3];              // interpolant derivative / h, plane ring
     T qz[C::S][3];                 // q_z, plane ring
@@ -196,11 +198,10 @@ __device__ __forceinline__ void flush_plane(const FusedArgs<T>& a, SmemL<T, C>& 
 // One axis of the template cell lookup (warp.py:38-53): t = (p - o) / h with the
 // reference's rounding, the hull test, the clamped lower corner and the fraction.
 template <typename T, bool POW2>
-__device__ __forceinline__ int cell_axis(T p, T o, T h, T ih, int n, bool& inside, T& f) {
+__device__ __forceinline__ int cell_axis(T p, T o, T h, T ih, T nm1, T hi, bool& inside, T& f) {
     const T d = sub_rn(p, o);
     const T t = POW2 ? mul_rn(d, ih) : div_rn(d, h);
-    inside = inside && (t >= (T)0) && (t <= (T)(n - 1));
-    const T hi = (T)(n > 2 ? n - 2 : 0);
+    inside = inside && (t >= (T)0) && (t <= nm1);
     const T fl = fmin_t(fmax_t(floor(t), (T)0), hi);  // NaN -> 0
     f = t - fl;  // exact for inside samples (Sterbenz); outside samples are masked
     return (int)fl;
@@ -248,9 +249,9 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
             const T yh1 = add_rn(mul_rn(m.ylo[s][1], wz0), mul_rn(m.yhi[s][1], wz));
             const T yh2 = add_rn(mul_rn(m.ylo[s][2], wz0), mul_rn(m.yhi[s][2], wz));
             bool inside = s_vol(m, s);
-            const int ix = cell_axis<T, POW2>(yh0, a.ox, a.hx, a.ihx, a.nx, inside, fx[s]);
-            const int iy = cell_axis<T, POW2>(yh1, a.oy, a.hy, a.ihy, a.ny, inside, fy[s]);
-            const int iz = cell_axis<T, POW2>(yh2, a.oz, a.hz, a.ihz, a.nz, inside, fz[s]);
+            const int ix = cell_axis<T, POW2>(yh0, a.ox, a.hx, a.ihx, a.nm1x, a.hix, inside, fx[s]);
+            const int iy = cell_axis<T, POW2>(yh1, a.oy, a.hy, a.ihy, a.nm1y, a.hiy, inside, fy[s]);
+            const int iz = cell_axis<T, POW2>(yh2, a.oz, a.hz, a.ihz, a.nm1z, a.hiz, inside, fz[s]);
             in[s] = inside;
             off[s] = (unsigned)iz * nxy + (unsigned)iy * (unsigned)a.nx + (unsigned)ix;
         }
@@ -305,14 +306,16 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
                 const T w0 = sm.Wsm[RB][P];
                 T gx = (sm.Wsm[RB][P + 1] - sm.Wsm[RB][P - 1]) * hx2;
                 T gy = (sm.Wsm[RB][P + C::E1X] - sm.Wsm[RB][P - C::E1X]) * hy2;
-                if (s_fx(m, s)) {  // one-sided difference at an x face
-                    const T* cg = sm.colG[P % C::E1X];
-                    gx = fmaf_t(cg[0], sm.Wsm[RB][P - 1], fmaf_t(cg[1], w0, cg[2] * sm.Wsm[RB][P + 1]));
-                }
-                if (s_fy(m, s)) {
-                    const T* rg = sm.rowG[P / C::E1X];
-                    gy = fmaf_t(rg[0], sm.Wsm[RB][P - C::E1X],
-                                fmaf_t(rg[1], w0, rg[2] * sm.Wsm[RB][P + C::E1X]));
+                if (m.wface) {  // warp holds a slot next to a volume face (rare, uniform)
+                    if (s_fx(m, s)) {  // one-sided difference at an x face
+                        const T* cg = sm.colG[P % C::E1X];
+                        gx = fmaf_t(cg[0], sm.Wsm[RB][P - 1], fmaf_t(cg[1], w0, cg[2] * sm.Wsm[RB][P + 1]));
+                    }
+                    if (s_fy(m, s)) {
+                        const T* rg = sm.rowG[P / C::E1X];
+                        gy = fmaf_t(rg[0], sm.Wsm[RB][P - C::E1X],
+                                    fmaf_t(rg[1], w0, rg[2] * sm.Wsm[RB][P + C::E1X]));
+                    }
                 }
                 const T gz = fmaf_t(cmz, sm.Wsm[RC][P], fmaf_t(c0z, w0, cpz * sm.Wsm[R][P]));
                 ngf_q(a, gx, gy, gz, m.rt[s], qxv, qyv, qzv, m.dacc);
@@ -344,15 +347,17 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
         const int P2 = m.P2[s];
         T sx = (qxj[P2 - 1] - qxj[P2 + 1]) * hx2;
         T sy = (qyj[P2 - C::E2X] - qyj[P2 + C::E2X]) * hy2;
-        if (s_fx(m, s)) {  // exact transposed face rows (warp.py:168-175)
-            const T* ct = sm.colGt[m.P[s] % C::E1X];
-            sx = fmaf_t(ct[0], qxj[P2 - 1], fmaf_t(ct[1], qxj[P2], ct[2] * qxj[P2 + 1]));
+        if (m.wface) {
+            if (s_fx(m, s)) {  // exact transposed face rows (warp.py:168-175)
+                const T* ct = sm.colGt[m.P[s] % C::E1X];
+                sx = fmaf_t(ct[0], qxj[P2 - 1], fmaf_t(ct[1], qxj[P2], ct[2] * qxj[P2 + 1]));
+            }
+            if (s_fy(m, s)) {
+                const T* rt = sm.rowGt[m.P[s] / C::E1X];
+                sy = fmaf_t(rt[0], qyj[P2 - C::E2X], fmaf_t(rt[1], qyj[P2], rt[2] * qyj[P2 + C::E2X]));
+            }
         }
-        if (s_fy(m, s)) {
-            const T* rt = sm.rowGt[m.P[s] / C::E1X];
-            sy = fmaf_t(rt[0], qyj[P2 - C::E2X], fmaf_t(rt[1], qyj[P2], rt[2] * qyj[P2 + C::E2X]));
-        }
-        T sv = sx + sy;
+        T sv = add_rn(sx, sy);  // no contraction (the packed march adds the same way)
         sv = fmaf_t(gtm, m.qz[s][R], fmaf_t(gt0, m.qz[s][RC], fmaf_t(gtp, m.qz[s][RB], sv)));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -389,33 +394,37 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
     }
 }
 
-template <typename T, typename C, bool POW2>
-__global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    SmemL<T, C>& sm = *reinterpret_cast<SmemL<T, C>*>(smem_raw);
-    constexpr int S = C::S;
+// CTA geometry of the march
+struct CtaGeo {
+    int tx, ty, tz, x0, y0, z0, z1, zb, jfirst, jlast, wzlo;
+};
+
+template <typename T, typename C>
+__device__ __forceinline__ CtaGeo cta_geo(const FusedArgs<T>& a) {
+    const FusedPlan& fp = a.fp;
+    CtaGeo g;
+    const int cta = blockIdx.x;
+    g.tx = cta % fp.ntx;
+    g.ty = (cta / fp.ntx) % fp.nty;
+    g.tz = cta / (fp.ntx * fp.nty);
+    g.x0 = g.tx * C::TX;
+    g.y0 = g.ty * C::TY;
+    g.z0 = fp.zlo + g.tz * fp.cz;
+    g.z1 = min(g.z0 + fp.cz, fp.zhi);
+    g.zb = g.z0 - 1;  // first plane of the z tables
+    g.jfirst = max(g.z0 - 1, 0);
+    g.jlast = min(g.z1, a.nz - 1);
+    g.wzlo = fp.win_z[g.tz];
+    return g;
+}
+
+// per-CTA shared tables: face coefficients, P weights, z tables, zeroed q rings, P^T CSR
+template <typename T, typename C>
+__device__ __forceinline__ void cta_tables(const FusedArgs<T>& a, SmemL<T, C>& sm, const CtaGeo& g) {
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x;
-    March<T, C> m;
-    m.cta = blockIdx.x;
-    const int tx = m.cta % fp.ntx;
-    const int ty = (m.cta / fp.ntx) % fp.nty;
-    const int tz = m.cta / (fp.ntx * fp.nty);
-    const int x0 = tx * C::TX, y0 = ty * C::TY;
-    m.z0 = fp.zlo + tz * fp.cz;
-    m.z1 = min(m.z0 + fp.cz, fp.zhi);
-    m.zb = m.z0 - 1;  // first plane of the z tables
-    m.jfirst = max(m.z0 - 1, 0);
-    m.jlast = min(m.z1, a.nz - 1);
-    const int wxlo = fp.win_x[tx];
-    const int wylo = fp.win_y[ty];
-    m.wzlo = fp.win_z[tz];
-    m.cur_zd = -1000;
-    m.dacc = 0.0;
-
-    // ---- per-CTA tables
     for (int e = tid; e < C::E1X; e += C::NT) {
-        const int i = x0 - 1 + e;
+        const int i = g.x0 - 1 + e;
         fd_coef<T>(i, a.nx, a.ihx, sm.colG[e][0], sm.colG[e][1], sm.colG[e][2]);
         fdt_coef<T>(i, a.nx, a.ihx, sm.colGt[e][0], sm.colGt[e][1], sm.colGt[e][2]);
         const bool in = i >= 0 && i < a.nx;
@@ -425,7 +434,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         sm.colPw[e] = in ? a.w1x[i] : (T)0;
     }
     for (int e = tid; e < C::E1Y; e += C::NT) {
-        const int jj = y0 - 1 + e;
+        const int jj = g.y0 - 1 + e;
         fd_coef<T>(jj, a.ny, a.ihy, sm.rowG[e][0], sm.rowG[e][1], sm.rowG[e][2]);
         fdt_coef<T>(jj, a.ny, a.ihy, sm.rowGt[e][0], sm.rowGt[e][1], sm.rowGt[e][2]);
         const bool in = jj >= 0 && jj < a.ny;
@@ -434,9 +443,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : (T)0;
     }
-    for (int t = tid; t < m.z1 + 2 - m.zb; t += C::NT) {
+    for (int t = tid; t < g.z1 + 2 - g.zb; t += C::NT) {
         // z tables for planes zb .. z1+1 (coefficients of warp.py:130-176 along z, P's w1)
-        const int z = m.zb + t;
+        const int z = g.zb + t;
         T* zc = sm.zt[t];
         fd_coef<T>(z, a.nz, a.ihz, zc[0], zc[1], zc[2]);
         fdt_coef<T>(z, a.nz, a.ihz, zc[3], zc[4], zc[5]);
@@ -451,53 +460,92 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         (&sm.qx[0][0])[t] = (T)0;
         (&sm.qy[0][0])[t] = (T)0;
     }
-    {
-        // this tile's CSR of the transposed 1-D interpolation (host-built, ascending E1
-        // index per window entry: the reference's gather order, transfer.py:89-96)
-        const int sxs = fp.wx + 1 + 2 * C::E1X, sys = fp.wy + 1 + 2 * C::E1Y;
-        const int32_t* gx = fp.xcsr + (size_t)tx * sxs;
-        const int32_t* gy = fp.ycsr + (size_t)ty * sys;
-        const T* wxg = (const T*)fp.xcw + (size_t)tx * 2 * C::E1X;
-        const T* wyg = (const T*)fp.ycw + (size_t)ty * 2 * C::E1Y;
-        for (int t = tid; t < fp.wx + 1; t += C::NT) sm.xoff[t] = gx[t];
-        for (int t = tid; t < 2 * C::E1X; t += C::NT) {
-            sm.xcol[t] = gx[fp.wx + 1 + t];
-            sm.xw[t] = wxg[t];
-        }
-        for (int t = tid; t < fp.wy + 1; t += C::NT) sm.yoff[t] = gy[t];
-        for (int t = tid; t < 2 * C::E1Y; t += C::NT) {
-            sm.yrow[t] = gy[fp.wy + 1 + t];
-            sm.yw[t] = wyg[t];
-        }
+    // this tile's CSR of the transposed 1-D interpolation (host-built, ascending E1
+    // index per window entry: the reference's gather order, transfer.py:89-96)
+    const int sxs = fp.wx + 1 + 2 * C::E1X, sys = fp.wy + 1 + 2 * C::E1Y;
+    const int32_t* gx = fp.xcsr + (size_t)g.tx * sxs;
+    const int32_t* gy = fp.ycsr + (size_t)g.ty * sys;
+    const T* wxg = (const T*)fp.xcw + (size_t)g.tx * 2 * C::E1X;
+    const T* wyg = (const T*)fp.ycw + (size_t)g.ty * 2 * C::E1Y;
+    for (int t = tid; t < fp.wx + 1; t += C::NT) sm.xoff[t] = gx[t];
+    for (int t = tid; t < 2 * C::E1X; t += C::NT) {
+        sm.xcol[t] = gx[fp.wx + 1 + t];
+        sm.xw[t] = wxg[t];
     }
-    (void)wxlo;
-    (void)wylo;
+    for (int t = tid; t < fp.wy + 1; t += C::NT) sm.yoff[t] = gy[t];
+    for (int t = tid; t < 2 * C::E1Y; t += C::NT) {
+        sm.yrow[t] = gy[fp.wy + 1 + t];
+        sm.yw[t] = wyg[t];
+    }
+}
+
+// Slot s of a thread owns E1 position tid + s * NT for all planes: its E1 index (padding
+// slots -> the sink entry E1), zero-padded q index, image column offset and flag bits
+// (in volume (x/y), tile interior, x face, y face).
+template <typename T, typename C>
+__device__ __forceinline__ void slot_geom(const FusedArgs<T>& a, const CtaGeo& g, int s, int& Pout, int& P2out,
+                                          unsigned& ij, unsigned& flags) {
+    const T hx2 = (T)0.5 * a.ihx, hy2 = (T)0.5 * a.ihy;
+    const int P = threadIdx.x + s * C::NT;
+    const bool ok = P < C::E1;
+    const int Pc = ok ? P : C::E1;
+    const int ex = Pc % C::E1X, ey = Pc / C::E1X;
+    const int i = g.x0 - 1 + ex, jj = g.y0 - 1 + ey;
+    const bool vol = ok && i >= 0 && i < a.nx && jj >= 0 && jj < a.ny;
+    const bool e0 = vol && ex >= 1 && ex <= C::TX && ey >= 1 && ey <= C::TY;
+    // a slot needs the exact face coefficients where G or G^T differ from central
+    T cm, c0, cp, gm, g0, gp;
+    fd_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
+    fdt_coef<T>(i, a.nx, a.ihx, gm, g0, gp);
+    const bool fx = !(cm == -hx2 && c0 == (T)0 && cp == hx2 && gm == hx2 && g0 == (T)0 && gp == -hx2);
+    fd_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
+    fdt_coef<T>(jj, a.ny, a.ihy, gm, g0, gp);
+    const bool fy = !(cm == -hy2 && c0 == (T)0 && cp == hy2 && gm == hy2 && g0 == (T)0 && gp == -hy2);
+    Pout = Pc;
+    P2out = ok ? (ey + 1) * C::E2X + ex + 1 : 0;  // padding slots write 0 into the pad ring
+    ij = vol ? (unsigned)(jj * a.nx + i) : 0u;
+    flags = (vol ? 1u : 0u) | (e0 ? 2u : 0u) | (vol && fx ? 4u : 0u) | (vol && fy ? 8u : 0u);
+}
+
+// the CTA's D partial (fixed order: warp tree, then warps in order)
+template <typename T, typename C>
+__device__ __forceinline__ void cta_dpart(const FusedArgs<T>& a, SmemL<T, C>& sm, double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) sm.red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sacc = 0.0;
+        for (int w = 0; w < C::NT / 32; ++w) sacc += sm.red[w];
+        a.dpart[blockIdx.x] = sacc;
+    }
+}
+
+template <typename T, typename C, bool POW2>
+__global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    SmemL<T, C>& sm = *reinterpret_cast<SmemL<T, C>*>(smem_raw);
+    constexpr int S = C::S;
+    const CtaGeo g = cta_geo<T, C>(a);
+    March<T, C> m;
+    m.cta = blockIdx.x;
+    m.z0 = g.z0;
+    m.z1 = g.z1;
+    m.zb = g.zb;
+    m.jfirst = g.jfirst;
+    m.jlast = g.jlast;
+    m.wzlo = g.wzlo;
+    m.cur_zd = -1000;
+    m.dacc = 0.0;
+    cta_tables<T, C>(a, sm, g);
 
     // ---- slot positions (fixed for all planes)
     m.flags = 0u;
-    const T hx2 = (T)0.5 * a.ihx, hy2 = (T)0.5 * a.ihy;
 #pragma unroll
     for (int s = 0; s < S; ++s) {
-        const int P = tid + s * C::NT;
-        const bool ok = P < C::E1;
-        const int Pc = ok ? P : C::E1;  // padding slots write into the sink entry
-        const int ex = Pc % C::E1X, ey = Pc / C::E1X;
-        const int i = x0 - 1 + ex, jj = y0 - 1 + ey;
-        const bool vol = ok && i >= 0 && i < a.nx && jj >= 0 && jj < a.ny;
-        const bool e0 = vol && ex >= 1 && ex <= C::TX && ey >= 1 && ey <= C::TY;
-        // a slot needs the exact face coefficients where G or G^T differ from central
-        T cm, c0, cp, gm, g0, gp;
-        fd_coef<T>(i, a.nx, a.ihx, cm, c0, cp);
-        fdt_coef<T>(i, a.nx, a.ihx, gm, g0, gp);
-        const bool fx = !(cm == -hx2 && c0 == (T)0 && cp == hx2 && gm == hx2 && g0 == (T)0 && gp == -hx2);
-        fd_coef<T>(jj, a.ny, a.ihy, cm, c0, cp);
-        fdt_coef<T>(jj, a.ny, a.ihy, gm, g0, gp);
-        const bool fy = !(cm == -hy2 && c0 == (T)0 && cp == hy2 && gm == hy2 && g0 == (T)0 && gp == -hy2);
-        m.P[s] = Pc;
-        m.P2[s] = ok ? (ey + 1) * C::E2X + ex + 1 : 0;  // padding slots write 0 into the pad ring
-        m.ij[s] = vol ? (unsigned)(jj * a.nx + i) : 0u;
-        m.flags |= ((vol ? 1u : 0u) | (e0 ? 2u : 0u) | (vol && fx ? 4u : 0u) | (vol && fy ? 8u : 0u))
-                   << (4 * s);
+        unsigned fl;
+        slot_geom<T, C>(a, g, s, m.P[s], m.P2[s], m.ij[s], fl);
+        m.flags |= fl << (4 * s);
 #pragma unroll
         for (int r = 0; r < 3; ++r) {
             m.qz[s][r] = (T)0;
@@ -510,6 +558,7 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         }
         m.rt[s] = V4T<T>{};
     }
+    m.wface = __any_sync(0xffffffffu, (m.flags & 0xCCCCCCCCu) != 0u);
     __syncthreads();
     // reference terms of the first interior plane
     if (m.z0 < m.z1) {
@@ -527,19 +576,10 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         if (b + 1 < nsteps) fused_step<1, T, C, POW2>(a, sm, m, pstart + b + 1);
         if (b + 2 < nsteps) fused_step<2, T, C, POW2>(a, sm, m, pstart + b + 2);
     }
-
-    // ---- the CTA's D partial
-    double v = m.dacc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((tid & 31) == 0) sm.red[tid >> 5] = v;
-    __syncthreads();
-    if (tid == 0) {
-        double sacc = 0.0;
-        for (int w = 0; w < C::NT / 32; ++w) sacc += sm.red[w];
-        a.dpart[m.cta] = sacc;
-    }
+    cta_dpart<T, C>(a, sm, m.dacc);
 }
+
+#include "fused_pair.cuh"
 
 // ------------------------------------------------------------------ reduce + curvature
 
@@ -938,19 +978,42 @@ size_t fused_smem(int v, int wx, int wy) {
     }
 }
 
+template <typename K>
+static cudaError_t smem_attr(K kernel, size_t smem) {
+    return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
 template <typename T, typename C>
 static int prep(size_t smem) {
-    cudaError_t e = cudaFuncSetAttribute(k_eval_fused<T, C, true>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_eval_fused<T, C, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)smem);
+    cudaError_t e = smem_attr(k_eval_fused<T, C, true>, smem);
+    if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, false>, smem);
+    if constexpr (std::is_same<T, float>::value && C::S == 2) {
+        if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, true, false>, smem);
+        if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, false, false>, smem);
+        if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, true, true>, smem);
+        if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, false, true>, smem);
+    }
     return (int)e;
 }
 
 template <typename T, typename C>
 static void launch(const FusedArgs<T>& a, cudaStream_t s) {
-    if (a.pow2x && a.pow2y && a.pow2z)
+    const bool pow2 = a.pow2x && a.pow2y && a.pow2z;
+    if constexpr (std::is_same<T, float>::value && C::S == 2) {
+        if (a.fp.packed) {
+            const bool gen = a.nx < 2 || a.ny < 2 || a.nz < 2;
+            if (pow2 && !gen)
+                NGF_LAUNCH((k_eval_pair<C, true, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+            else if (!gen)
+                NGF_LAUNCH((k_eval_pair<C, false, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+            else if (pow2)
+                NGF_LAUNCH((k_eval_pair<C, true, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+            else
+                NGF_LAUNCH((k_eval_pair<C, false, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+            return;
+        }
+    }
+    if (pow2)
         NGF_LAUNCH((k_eval_fused<T, C, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
     else
         NGF_LAUNCH((k_eval_fused<T, C, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);

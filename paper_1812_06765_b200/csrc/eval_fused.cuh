@@ -11,6 +11,7 @@ constexpr int kTX = 32;
 struct FusedPlan {
     // kernel variant (tile rows, threads per CTA, occupancy) and tiles
     int variant, ty, nthreads;
+    int packed;  // two-slot float2 march (f32 variants with two slots per thread)
     int ntx, nty, ntz, cz;
     int zlo, zhi;  // image planes evaluated (a z-slab for config-5 decomposition; 0, nz otherwise)
     // P^T windows: max sizes and per-tile lower def index (device arrays)

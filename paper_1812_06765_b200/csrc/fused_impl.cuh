@@ -20,6 +20,8 @@ struct FusedArgs {
     T hx, hy, hz;     // spacing, working dtype
     T ihx, ihy, ihz;  // 1 / spacing (derivative scale)
     int pow2x, pow2y, pow2z;  // spacing is a power of two: division == multiply by exact reciprocal
+    T nm1x, nm1y, nm1z;       // n - 1: upper end of the hull test (warp.py:39)
+    T hix, hiy, hiz;          // max(n - 2, 0): largest lower corner (warp.py:50)
     const int32_t *i0x, *i0y, *i0z;  // image -> def lower index (transfer.py:54-63)
     const T *w1x, *w1y, *w1z;        // dtype(w1)
     const T* Tv;                     // template values

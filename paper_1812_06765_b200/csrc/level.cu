@@ -113,6 +113,9 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     if (sizeof(T) == 8) variant = 0;
     static const int kMinBlocks[] = {2, 2, 3, 1, 2, 1};
     fp.variant = variant;
+    // two-slot float2 march: opt-in (measured 388 us vs 375 us for the scalar march at
+    // 256^3 -- the FP issue slots it saves are spent on pair formation and masking)
+    fp.packed = std::getenv("NGF_FUSED_PACKED") ? 1 : 0;
     fused_variant_geom(variant, &fp.ty, &fp.nthreads);
     fp.wx = tile_windows(p->h_i0[0], nx, ndx, kTX, 1, xl, xh);
     fp.wy = tile_windows(p->h_i0[1], ny, ndy, fp.ty, 1, yl, yh);
@@ -256,6 +259,12 @@ static FusedArgs<T> fused_args(const ngf_level* L, const void* y) {
     a.w1x = w1_host_sel<T>(p->axes[0]);
     a.w1y = w1_host_sel<T>(p->axes[1]);
     a.w1z = w1_host_sel<T>(p->axes[2]);
+    a.nm1x = (T)(a.nx - 1);
+    a.nm1y = (T)(a.ny - 1);
+    a.nm1z = (T)(a.nz - 1);
+    a.hix = (T)(a.nx > 2 ? a.nx - 2 : 0);
+    a.hiy = (T)(a.ny > 2 ? a.ny - 2 : 0);
+    a.hiz = (T)(a.nz > 2 ? a.nz - 2 : 0);
     a.Tv = (const T*)L->T;
     a.RT = (const V4T<T>*)L->RT;
     a.y = (const T*)y;
