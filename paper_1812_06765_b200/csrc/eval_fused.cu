@@ -207,7 +207,7 @@ __device__ __forceinline__ int cell_axis(T p, T o, T h, T ih, T nm1, T hi, bool&
     return (int)fl;
 }
 
-template <int R, typename T, typename C, bool POW2>
+template <int R, typename T, typename C, bool POW2, bool GEN>
 __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& sm, March<T, C>& m,
                                            int p) {
     constexpr int RB = (R + 2) % 3;  // plane p-1
@@ -255,21 +255,39 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
             in[s] = inside;
             off[s] = (unsigned)iz * nxy + (unsigned)iy * (unsigned)a.nx + (unsigned)ix;
         }
-        const unsigned sx = a.nx > 1 ? 1u : 0u;
-        const unsigned sy = a.ny > 1 ? (unsigned)a.nx : 0u;
-        const unsigned sz = a.nz > 1 ? nxy : 0u;
         T cv[S][8];
+        if (GEN) {  // degenerate axes: the +1 corner is the same voxel
+            const unsigned sx = a.nx > 1 ? 1u : 0u;
+            const unsigned sy = a.ny > 1 ? (unsigned)a.nx : 0u;
+            const unsigned sz = a.nz > 1 ? nxy : 0u;
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const unsigned o = off[s];
-            cv[s][0] = __ldg(a.Tv + o);
-            cv[s][1] = __ldg(a.Tv + (o + sx));
-            cv[s][2] = __ldg(a.Tv + (o + sy));
-            cv[s][3] = __ldg(a.Tv + (o + sy + sx));
-            cv[s][4] = __ldg(a.Tv + (o + sz));
-            cv[s][5] = __ldg(a.Tv + (o + sz + sx));
-            cv[s][6] = __ldg(a.Tv + (o + sz + sy));
-            cv[s][7] = __ldg(a.Tv + (o + sz + sy + sx));
+            for (int s = 0; s < S; ++s) {
+                const unsigned o = off[s];
+                cv[s][0] = __ldg(a.Tv + o);
+                cv[s][1] = __ldg(a.Tv + (o + sx));
+                cv[s][2] = __ldg(a.Tv + (o + sy));
+                cv[s][3] = __ldg(a.Tv + (o + sy + sx));
+                cv[s][4] = __ldg(a.Tv + (o + sz));
+                cv[s][5] = __ldg(a.Tv + (o + sz + sx));
+                cv[s][6] = __ldg(a.Tv + (o + sz + sy));
+                cv[s][7] = __ldg(a.Tv + (o + sz + sy + sx));
+            }
+        } else {  // one base address per slot, +x corners as immediate offsets
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const T* b = a.Tv + off[s];
+                const T* by = b + a.nx;
+                const T* bz = b + nxy;
+                const T* byz = bz + a.nx;
+                cv[s][0] = __ldg(b);
+                cv[s][1] = __ldg(b + 1);
+                cv[s][2] = __ldg(by);
+                cv[s][3] = __ldg(by + 1);
+                cv[s][4] = __ldg(bz);
+                cv[s][5] = __ldg(bz + 1);
+                cv[s][6] = __ldg(byz);
+                cv[s][7] = __ldg(byz + 1);
+            }
         }
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -521,7 +539,7 @@ __device__ __forceinline__ void cta_dpart(const FusedArgs<T>& a, SmemL<T, C>& sm
     }
 }
 
-template <typename T, typename C, bool POW2>
+template <typename T, typename C, bool POW2, bool GEN>
 __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_constant__ FusedArgs<T> a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     SmemL<T, C>& sm = *reinterpret_cast<SmemL<T, C>*>(smem_raw);
@@ -572,9 +590,9 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
     const int pstart = m.z0 - 1;
     const int nsteps = (m.z1 + 2) - pstart + 1;
     for (int b = 0; b < nsteps; b += 3) {
-        fused_step<0, T, C, POW2>(a, sm, m, pstart + b);
-        if (b + 1 < nsteps) fused_step<1, T, C, POW2>(a, sm, m, pstart + b + 1);
-        if (b + 2 < nsteps) fused_step<2, T, C, POW2>(a, sm, m, pstart + b + 2);
+        fused_step<0, T, C, POW2, GEN>(a, sm, m, pstart + b);
+        if (b + 1 < nsteps) fused_step<1, T, C, POW2, GEN>(a, sm, m, pstart + b + 1);
+        if (b + 2 < nsteps) fused_step<2, T, C, POW2, GEN>(a, sm, m, pstart + b + 2);
     }
     cta_dpart<T, C>(a, sm, m.dacc);
 }
@@ -944,22 +962,20 @@ __global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArg
 
 // ------------------------------------------------------------------ host launchers
 
-// Kernel variants: tile rows TY, threads per CTA, minimum resident CTAs per SM.
+// Kernel variants: tile rows TY, threads per CTA, minimum resident CTAs per SM
+// (tools/sweep.py; 32 x 12 / 256 threads / 2 CTAs per SM is the fastest f32 shape at
+// 128^3 .. 256^3, the f64 march uses 32 x 20).
 using V0 = Cfg<20, 256, 2>;
 using V1 = Cfg<12, 256, 2>;
-using V2 = Cfg<12, 256, 3>;
-using V3 = Cfg<28, 512, 1>;
-using V4 = Cfg<12, 512, 2>;
-using V5 = Cfg<20, 256, 1>;
-constexpr int kNumVariants = 6;
+using V2 = Cfg<28, 512, 1>;
+using V3 = Cfg<12, 512, 2>;
+constexpr int kNumVariants = 4;
 
 void fused_variant_geom(int v, int* ty, int* nt) {
     switch (v) {
         case 1: *ty = V1::TY; *nt = V1::NT; return;
         case 2: *ty = V2::TY; *nt = V2::NT; return;
         case 3: *ty = V3::TY; *nt = V3::NT; return;
-        case 4: *ty = V4::TY; *nt = V4::NT; return;
-        case 5: *ty = V5::TY; *nt = V5::NT; return;
         default: *ty = V0::TY; *nt = V0::NT; return;
     }
 }
@@ -972,8 +988,6 @@ size_t fused_smem(int v, int wx, int wy) {
         case 1: return smem_bytes_cfg<T, V1>(wx, wy);
         case 2: return smem_bytes_cfg<T, V2>(wx, wy);
         case 3: return smem_bytes_cfg<T, V3>(wx, wy);
-        case 4: return smem_bytes_cfg<T, V4>(wx, wy);
-        case 5: return smem_bytes_cfg<T, V5>(wx, wy);
         default: return smem_bytes_cfg<T, V0>(wx, wy);
     }
 }
@@ -985,8 +999,10 @@ static cudaError_t smem_attr(K kernel, size_t smem) {
 
 template <typename T, typename C>
 static int prep(size_t smem) {
-    cudaError_t e = smem_attr(k_eval_fused<T, C, true>, smem);
-    if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, false>, smem);
+    cudaError_t e = smem_attr(k_eval_fused<T, C, true, false>, smem);
+    if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, false, false>, smem);
+    if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, true, true>, smem);
+    if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, false, true>, smem);
     if constexpr (std::is_same<T, float>::value && C::S == 2) {
         if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, true, false>, smem);
         if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, false, false>, smem);
@@ -999,9 +1015,9 @@ static int prep(size_t smem) {
 template <typename T, typename C>
 static void launch(const FusedArgs<T>& a, cudaStream_t s) {
     const bool pow2 = a.pow2x && a.pow2y && a.pow2z;
+    const bool gen = a.nx < 2 || a.ny < 2 || a.nz < 2;  // a degenerate image axis
     if constexpr (std::is_same<T, float>::value && C::S == 2) {
         if (a.fp.packed) {
-            const bool gen = a.nx < 2 || a.ny < 2 || a.nz < 2;
             if (pow2 && !gen)
                 NGF_LAUNCH((k_eval_pair<C, true, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
             else if (!gen)
@@ -1013,10 +1029,14 @@ static void launch(const FusedArgs<T>& a, cudaStream_t s) {
             return;
         }
     }
-    if (pow2)
-        NGF_LAUNCH((k_eval_fused<T, C, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+    if (pow2 && !gen)
+        NGF_LAUNCH((k_eval_fused<T, C, true, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+    else if (!gen)
+        NGF_LAUNCH((k_eval_fused<T, C, false, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+    else if (pow2)
+        NGF_LAUNCH((k_eval_fused<T, C, true, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
     else
-        NGF_LAUNCH((k_eval_fused<T, C, false>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
+        NGF_LAUNCH((k_eval_fused<T, C, false, true>), a.fp.n_cta, C::NT, a.fp.smem_bytes, s, a);
 }
 
 template <>
@@ -1025,8 +1045,6 @@ int fused_prepare<float>(int v, size_t smem) {
         case 1: return prep<float, V1>(smem);
         case 2: return prep<float, V2>(smem);
         case 3: return prep<float, V3>(smem);
-        case 4: return prep<float, V4>(smem);
-        case 5: return prep<float, V5>(smem);
         default: return prep<float, V0>(smem);
     }
 }
@@ -1046,8 +1064,6 @@ void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
         case 1: launch<float, V1>(a, s); return;
         case 2: launch<float, V2>(a, s); return;
         case 3: launch<float, V3>(a, s); return;
-        case 4: launch<float, V4>(a, s); return;
-        case 5: launch<float, V5>(a, s); return;
         default: launch<float, V0>(a, s); return;
     }
 }

@@ -111,7 +111,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     if (const char* env = std::getenv("NGF_FUSED_VARIANT"))
         variant = std::atoi(env) % fused_variant_count();
     if (sizeof(T) == 8) variant = 0;
-    static const int kMinBlocks[] = {2, 2, 3, 1, 2, 1};
+    static const int kMinBlocks[] = {2, 2, 1, 2};
     fp.variant = variant;
     // two-slot float2 march: opt-in (measured 388 us vs 375 us for the scalar march at
     // 256^3 -- the FP issue slots it saves are spent on pair formation and masking)

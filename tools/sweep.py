@@ -1,6 +1,6 @@
 """Time the fused kernel per variant / z-chunk at one size (CUDA events inside the library).
 
-    python tools/sweep.py [--n 256] [--variants 0,1,2,3,4,5] [--cz 0]
+    python tools/sweep.py [--n 256] [--variants 0,1,2,3] [--cz 0]
 """
 
 import argparse
@@ -20,7 +20,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--ratio", type=int, default=4)
-    ap.add_argument("--variants", default="0,1,2,3,4,5")
+    ap.add_argument("--variants", default="0,1,2,3")
     ap.add_argument("--cz", default="0")
     ap.add_argument("--reps", type=int, default=20)
     a = ap.parse_args()
