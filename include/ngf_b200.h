@@ -72,6 +72,15 @@ int ngf_plan_axis(const ngf_plan_t* plan, int axis, int32_t* host_i0, double* ho
 int ngf_apply_P(const ngf_plan_t* plan, int dtype, const void* y, void* yhat, void* stream);
 /* out = P^T r, deterministic gather (transfer.py:173-192, the "gather" variant). */
 int ngf_apply_Pt(const ngf_plan_t* plan, int dtype, const void* r, void* out, void* stream);
+/* out = P^T r with the reference's variant `variant`: NGF_PT_GATHER (= ngf_apply_Pt),
+ * NGF_PT_SCATTER (transfer.py:199-222, float atomics: equal to the gather up to
+ * reassociation), NGF_PT_REDBLACK (transfer.py:225-256, two parity launches:
+ * bit-identical to the reference's red-black). */
+#define NGF_PT_GATHER 0
+#define NGF_PT_SCATTER 1
+#define NGF_PT_REDBLACK 2
+int ngf_apply_Pt_variant(const ngf_plan_t* plan, int dtype, int variant, const void* r, void* out,
+                         void* stream);
 /* W = T(yhat), mask (warp.py:64-90).  mask may be NULL. */
 int ngf_warp(const ngf_grid_t* tgrid, int dtype, const void* T, const void* yhat, int64_t n,
              void* W, uint8_t* mask, void* stream);

@@ -83,3 +83,8 @@ def stream() -> int:
 
 def to_host(x) -> np.ndarray:
     return x.detach().cpu().numpy()
+
+
+def synchronize() -> None:
+    """Wait for the current stream's work (host-side timing of device calls)."""
+    torch().cuda.current_stream().synchronize()

@@ -26,6 +26,14 @@ int ngf_apply_Pt(const ngf_plan_t* p, int dtype, const void* r, void* out, void*
                  apply_Pt_impl<double>(p, (const double*)r, (double*)out, as_stream(stream)));
 }
 
+int ngf_apply_Pt_variant(const ngf_plan_t* p, int dtype, int variant, const void* r, void* out,
+                         void* stream) {
+    if (!p || !r || !out) return NGF_EARG;
+    NGF_DISPATCH(dtype,
+                 apply_Pt_variant_impl<float>(p, variant, (const float*)r, (float*)out, as_stream(stream)),
+                 apply_Pt_variant_impl<double>(p, variant, (const double*)r, (double*)out, as_stream(stream)));
+}
+
 int ngf_warp(const ngf_grid_t* tg, int dtype, const void* T, const void* yhat, int64_t n, void* W,
              uint8_t* mask, void* stream) {
     if (!grid_ok(tg) || !T || !yhat || !W || n < 0) return NGF_EARG;

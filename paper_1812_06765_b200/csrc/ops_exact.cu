@@ -133,6 +133,100 @@ int apply_Pt_impl(const ngf_plan_t* p, const T* r, T* out, cudaStream_t s) {
     return 0;
 }
 
+// ------------------------------------------------------------------ P^T scatter / red-black
+// The reference's two other P^T variants (transfer.py:199-256): the image slices are
+// reduced in x then y exactly like the gather (k_pt_xy, `_reduce_slice_xy`), then each
+// slice k is pushed onto def planes i0z[k] and i0z[k]+1 with w1 = dtype(w1z[k]),
+// w0 = 1 - w1 (working dtype), `out += w * sl` (product then sum, no contraction).
+
+// scatter: one thread per reduced slice value, float atomics (order is not fixed:
+// equal to the gather up to floating-point reassociation, like the reference's
+// lock-based scatter, transfer.py:199-222)
+template <typename T>
+__global__ void k_pt_z_scatter(AxisDev az, int ndy, int ndx, const T* __restrict__ tmp, T* __restrict__ out) {
+    const int nz = az.ni, ndz = az.nd;
+    const int64_t plane = (int64_t)ndy * ndx;
+    const int64_t tot = (int64_t)3 * nz * plane;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < tot;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xy = v % plane;
+        const int k = (int)((v / plane) % nz);
+        const int c = (int)(v / (plane * nz));
+        const T val = tmp[v];
+        const T w1 = w1_of<T>(az)[k];
+        const T w0 = (T)1 - w1;
+        T* o = out + ((int64_t)c * ndz + az.i0[k]) * plane + xy;
+        atomicAdd(o, w0 * val);
+        if (w1 != (T)0) atomicAdd(o + plane, w1 * val);
+    }
+}
+
+// red-black: slices grouped by their lower def plane d0 (a contiguous k range, i0z is
+// non-decreasing); one launch per parity of d0, one thread per (component, group,
+// def column) adding the group's slices in ascending k.  Groups of one colour write
+// disjoint planes, so every output receives its terms in the reference's order
+// (transfer.py:225-256): bit-identical to the reference.
+template <typename T>
+__global__ void k_pt_z_redblack(AxisDev az, int ndy, int ndx, int parity, const T* __restrict__ tmp,
+                                T* __restrict__ out) {
+    const int nz = az.ni, ndz = az.nd;
+    const int ng = (ndz - parity + 1) / 2;  // candidate groups d0 = parity, parity + 2, ...
+    const int64_t plane = (int64_t)ndy * ndx;
+    const int64_t tot = (int64_t)3 * ng * plane;
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < tot;
+         v += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xy = v % plane;
+        const int gi = (int)((v / plane) % ng);
+        const int c = (int)(v / (plane * ng));
+        const int d0 = parity + 2 * gi;
+        // slices with i0z[k] == d0: [lo, hi) by binary search
+        int lo = 0, hi = nz;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (az.i0[mid] < d0) lo = mid + 1; else hi = mid;
+        }
+        int k1 = lo, e = nz;
+        while (k1 < e) {
+            const int mid = (k1 + e) >> 1;
+            if (az.i0[mid] <= d0) k1 = mid + 1; else e = mid;
+        }
+        if (lo == k1) continue;  // empty group
+        T* o0 = out + ((int64_t)c * ndz + d0) * plane + xy;
+        const T* src = tmp + (int64_t)c * nz * plane + xy;
+        for (int k = lo; k < k1; ++k) {
+            const T val = src[(int64_t)k * plane];
+            const T w1 = w1_of<T>(az)[k];
+            const T w0 = (T)1 - w1;
+            o0[0] = o0[0] + w0 * val;
+            if (w1 != (T)0) o0[plane] = o0[plane] + w1 * val;
+        }
+    }
+}
+
+template <typename T>
+int apply_Pt_variant_impl(const ngf_plan_t* p, int variant, const T* r, T* out, cudaStream_t s) {
+    if (variant == 0) return apply_Pt_impl<T>(p, r, out, s);
+    if (variant != 1 && variant != 2) return NGF_EARG;
+    if (int rc = plan_upload(const_cast<ngf_plan_t*>(p))) return rc;
+    const int nz = p->n_img[2], ndy = p->n_def[1], ndx = p->n_def[0], ndz = p->n_def[2];
+    T* tmp = (T*)p->d_tmp;
+    const int64_t ta = (int64_t)3 * nz * ndy * ndx;
+    NGF_LAUNCH(k_pt_xy<T>, blocks_for(ta, 256), 256, 0, s, p->axes[0], p->axes[1], nz, r, tmp);
+    NGF_CUDA(cudaMemsetAsync(out, 0, (size_t)3 * ndz * ndy * ndx * sizeof(T), s));
+    if (variant == 1) {
+        NGF_LAUNCH(k_pt_z_scatter<T>, blocks_for(ta, 256), 256, 0, s, p->axes[2], ndy, ndx, tmp, out);
+    } else {
+        for (int parity = 0; parity < 2; ++parity) {
+            const int64_t tb = (int64_t)3 * ((ndz - parity + 1) / 2) * ndy * ndx;
+            if (tb > 0)
+                NGF_LAUNCH(k_pt_z_redblack<T>, blocks_for(tb, 256), 256, 0, s, p->axes[2], ndy, ndx, parity,
+                           tmp, out);
+        }
+    }
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
 // ------------------------------------------------------------------ warp (warp.py:26-127)
 
 template <typename T>
@@ -843,6 +937,7 @@ int prolong_impl(const ngf_plan_t* p, const T* yc, T* yf, cudaStream_t s) {
 #define NGF_INST(T)                                                                              \
     template int apply_P_impl<T>(const ngf_plan_t*, const T*, T*, cudaStream_t);                 \
     template int apply_Pt_impl<T>(const ngf_plan_t*, const T*, T*, cudaStream_t);                \
+    template int apply_Pt_variant_impl<T>(const ngf_plan_t*, int, const T*, T*, cudaStream_t);   \
     template int warp_impl<T>(const ngf_grid_t*, const T*, const T*, int64_t, T*, uint8_t*,      \
                               cudaStream_t);                                                     \
     template int warp_jt_impl<T>(const ngf_grid_t*, const T*, const T*, const T*, int64_t, T*,  \

@@ -6,6 +6,8 @@ namespace ngf {
 
 template <typename T> int apply_P_impl(const ngf_plan_t*, const T*, T*, cudaStream_t);
 template <typename T> int apply_Pt_impl(const ngf_plan_t*, const T*, T*, cudaStream_t);
+// variant 0 gather, 1 scatter (atomics), 2 red-black (transfer.py:199-256)
+template <typename T> int apply_Pt_variant_impl(const ngf_plan_t*, int, const T*, T*, cudaStream_t);
 template <typename T>
 int warp_impl(const ngf_grid_t*, const T*, const T*, int64_t, T*, uint8_t*, cudaStream_t);
 template <typename T>

@@ -2,10 +2,10 @@
 
 The index maps and gather plans are computed by libngfb200's host code in IEEE
 f64 (bit-exact with transfer.py:54-110); P and P^T run as sm_100a kernels that
-reproduce the reference operation order (transfer.py:117-192).  All three
-reference P^T variants ("gather", "scatter", "redblack") are accepted and run
-the deterministic gather kernel: they are the same operator up to summation
-order (pkg/README.md:33-39), and the device build keeps one deterministic P^T.
+reproduce the reference operation order (transfer.py:117-192).  The three reference
+P^T variants run as their own kernels (transfer.py:173-256): "gather" and "redblack"
+bit-identical to the reference, "scatter" with float atomics (equal up to
+reassociation, as the reference's lock-based scatter, pkg/README.md:33-39).
 """
 
 from __future__ import annotations
@@ -151,22 +151,40 @@ def apply_Pt_gather(r: VectorField3, plan: GatherPlan, workers: int = 1):
     return _ret(plan.def_grid, out, np_out)
 
 
+def _apply_Pt_variant(r: VectorField3, plan: GatherPlan, variant: int, name: str):
+    rd, np_out = _field_io(r.field)
+    out = dev.empty((3,) + plan.def_grid.shape, rd.dtype)
+    check(lib().ngf_apply_Pt_variant(plan.handle, dtype_code(rd.dtype), variant, dev.ptr(rd),
+                                     dev.ptr(out), dev.stream()), name)
+    return _ret(plan.def_grid, out, np_out)
+
+
 def apply_Pt_scatter_atomic(r: VectorField3, def_grid: Grid3, workers: int = 1):
-    """Reference variant name (transfer.py:199-222); runs the deterministic gather kernel."""
+    """P^T by scattering the x/y-reduced image slices onto their two def planes with
+    float atomics (transfer.py:199-222): equal to the gather up to floating-point
+    reassociation, like the reference's lock-based scatter."""
     check_compatible(def_grid, r.grid)
-    return apply_Pt_gather(r, GatherPlan(def_grid, r.grid), workers)
+    return _apply_Pt_variant(r, GatherPlan(def_grid, r.grid), 1, "ngf_apply_Pt_variant(scatter)")
 
 
 def apply_Pt_redblack(r: VectorField3, def_grid: Grid3, workers: int = 1):
-    """Reference variant name (transfer.py:225-256); runs the deterministic gather kernel."""
+    """P^T with slices grouped by target def plane, even then odd groups
+    (transfer.py:225-256); bit-identical to the reference's red-black."""
     check_compatible(def_grid, r.grid)
-    return apply_Pt_gather(r, GatherPlan(def_grid, r.grid), workers)
+    return _apply_Pt_variant(r, GatherPlan(def_grid, r.grid), 2, "ngf_apply_Pt_variant(redblack)")
 
 
 def apply_Pt(r: VectorField3, plan: GatherPlan, variant: str = "gather", workers: int = 1):
-    if variant not in PT_VARIANTS:
-        raise ValueError(f"unknown P^T variant {variant!r}, expected one of {PT_VARIANTS}")
-    return apply_Pt_gather(r, plan, workers)
+    """Dispatcher (transfer.py:259-266)."""
+    if variant == "gather":
+        return apply_Pt_gather(r, plan, workers)
+    if variant == "scatter":
+        check_compatible(plan.def_grid, r.grid)
+        return _apply_Pt_variant(r, plan, 1, "ngf_apply_Pt_variant(scatter)")
+    if variant == "redblack":
+        check_compatible(plan.def_grid, r.grid)
+        return _apply_Pt_variant(r, plan, 2, "ngf_apply_Pt_variant(redblack)")
+    raise ValueError(f"unknown P^T variant {variant!r}, expected one of {PT_VARIANTS}")
 
 
 def dense_P_oracle(def_grid: Grid3, image_grid: Grid3) -> np.ndarray:

@@ -87,6 +87,9 @@ def transfer_cases():
             out[f"{k}_r_{p}"] = r.field
             out[f"{k}_P_{p}"] = transfer.apply_P(y, gi).field
             out[f"{k}_Pt_{p}"] = transfer.apply_Pt_gather(r, plan).field
+            # the other two P^T variants (transfer.py:199-256), one worker
+            out[f"{k}_Pts_{p}"] = transfer.apply_Pt_scatter_atomic(r, gd).field
+            out[f"{k}_Ptrb_{p}"] = transfer.apply_Pt_redblack(r, gd).field
     out["n"] = np.array(len(pairs))
     save("transfer", **out)
 
@@ -294,6 +297,10 @@ def register_run(R, T, cfg):
 
 
 if __name__ == "__main__":
+    if len(sys.argv) > 1:  # regenerate selected fixtures, e.g. `make_golden.py transfer`
+        for name in sys.argv[1:]:
+            globals()[name + "_cases"]()
+        sys.exit(0)
     transfer_cases()
     warp_cases()
     ngf_cases()

@@ -48,6 +48,9 @@ def test_transfer_golden():
         for p in PRECS:
             assert np.array_equal(O.apply_P(z[f"{k}_y_{p}"], gd, gi), z[f"{k}_P_{p}"])
             assert np.array_equal(O.apply_Pt(z[f"{k}_r_{p}"], gd, gi, plan), z[f"{k}_Pt_{p}"])
+            # scatter / red-black variants (transfer.py:199-256), one worker
+            assert np.array_equal(O.apply_Pt_scatter(z[f"{k}_r_{p}"], gd, gi), z[f"{k}_Pts_{p}"])
+            assert np.array_equal(O.apply_Pt_redblack(z[f"{k}_r_{p}"], gd, gi), z[f"{k}_Ptrb_{p}"])
 
 
 def test_warp_golden():
