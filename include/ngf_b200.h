@@ -140,6 +140,10 @@ int ngf_level_add_curvature(ngf_level_t* level, const void* y, void* grad, doubl
                             void* stream);
 /* Device pointer of the level's reference terms (packed (gx, gy, gz, 1) / nR per voxel). */
 const void* ngf_level_ref_terms(const ngf_level_t* level);
+/* P^T variant used by the exact evaluation (mode 1): NGF_PT_GATHER (default),
+ * NGF_PT_SCATTER or NGF_PT_REDBLACK (objective.py:22-60 `pt_variant`).  The fused
+ * evaluation always uses its deterministic tile gather. */
+int ngf_level_set_pt_variant(ngf_level_t* level, int variant);
 /* Record CUDA events around the fused kernel of every mode-0 evaluation (bench.py's
  * roofline), and read the last one's duration in ms (synchronises on the event). */
 int ngf_level_set_timing(ngf_level_t* level, int on);

@@ -46,6 +46,7 @@ struct ngf_level {
     int ns;          // capacity of spart (>= k_post blocks)
     int* flag;       // [0] non-finite y seen in this evaluation, [1] k_post block counter
     int timing;      // record events around the fused kernel
+    int pt_variant;  // P^T variant of the exact path (0 gather, 1 scatter, 2 red-black)
     cudaEvent_t ev[2];
     ngf::LevelWork ex;
 };
@@ -345,7 +346,7 @@ static int eval_exact(ngf_level* L, const void* y, void* grad, double* scal, cud
     if ((rc = warp_jt_impl<T>(&L->img, (const T*)L->T, (const T*)w.yhat, (const T*)w.s, n,
                               (T*)w.ghat, s)))
         return rc;
-    if ((rc = apply_Pt_impl<T>(L->plan, (const T*)w.ghat, (T*)w.gD, s))) return rc;
+    if ((rc = apply_Pt_variant_impl<T>(L->plan, L->pt_variant, (const T*)w.ghat, (T*)w.gD, s))) return rc;
     if ((rc = curvature_impl<T>(&L->def, (const T*)y, w.dws + 5, (T*)grad, (const T*)w.gD, L->alpha,
                                 (T*)w.cws, w.dws, s)))
         return rc;
@@ -478,6 +479,12 @@ int ngf_level_set_zrange(ngf_level_t* L, int64_t zlo, int64_t zhi) {
     L->dpart = L->spart = nullptr;
     return L->dtype == NGF_F32 ? fused_setup<float>(L, (int)zlo, (int)zhi)
                                : fused_setup<double>(L, (int)zlo, (int)zhi);
+}
+
+int ngf_level_set_pt_variant(ngf_level_t* L, int variant) {
+    if (!L || variant < 0 || variant > 2) return NGF_EARG;
+    L->pt_variant = variant;
+    return 0;
 }
 
 int ngf_level_set_timing(ngf_level_t* L, int on) {

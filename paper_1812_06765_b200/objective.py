@@ -19,7 +19,7 @@ from . import _device as dev
 from ._lib import check, dtype_code, lib, ngf_grid
 from .geometry import DeformationField, Grid3, Image3
 from .ngf import NgfParams, ReferenceTerms
-from .transfer import GatherPlan
+from .transfer import PT_VARIANTS, GatherPlan
 
 __all__ = ["LevelObjective", "DeviceLevel"]
 
@@ -86,15 +86,26 @@ class LevelObjective:
     _level: DeviceLevel | None = field(default=None, repr=False)
     _R_dev: object = field(default=None, repr=False)
 
+    def __post_init__(self):
+        if self.pt_variant not in PT_VARIANTS:
+            raise ValueError(f"unknown P^T variant {self.pt_variant!r}, expected one of {PT_VARIANTS}")
+
     @classmethod
     def from_device(cls, T_dev, R_dev, plan: GatherPlan, params: NgfParams, alpha: float,
-                    exact: bool = False):
+                    exact: bool = False, pt_variant: str = "gather"):
         """Device-resident construction used by `register`: reference terms are
         computed on the device from R (ngf.py:60-67) inside the level."""
         obj = cls(template=Image3(plan.image_grid, T_dev), ref=None, plan=plan, params=params,
-                  alpha=alpha, exact=exact)
+                  alpha=alpha, pt_variant=pt_variant, exact=exact)
         obj._level = DeviceLevel(plan.image_grid, plan.def_grid, T_dev, params, alpha, R_dev=R_dev)
+        obj._set_variant()
         return obj
+
+    def _set_variant(self):
+        # the exact path runs the requested P^T variant; the fused march always uses its
+        # deterministic tile gather (the reference's default, ngf.py:121)
+        check(lib().ngf_level_set_pt_variant(self._level.handle, PT_VARIANTS.index(self.pt_variant)),
+              "ngf_level_set_pt_variant")
 
     @property
     def def_grid(self) -> Grid3:
@@ -109,6 +120,7 @@ class LevelObjective:
             nR = dev.to_device(self.ref.norm, dt)
             self._level = DeviceLevel(self.plan.image_grid, self.plan.def_grid, T, self.params,
                                       self.alpha, gR_dev=gR, nR_dev=nR)
+            self._set_variant()
         return self._level
 
     def field_from_flat(self, x) -> DeformationField:

@@ -163,6 +163,12 @@ def ngf_cases():
             out[f"{k}_Jd_{p}"] = np.array(obj.last_D)
             out[f"{k}_Js_{p}"] = np.array(obj.last_S)
             out[f"{k}_gJ_{p}"] = gJ
+            # the objective with the red-black P^T (objective.py:22-60 pt_variant)
+            obj_rb = LevelObjective(template=T, ref=ref, plan=plan, params=params, alpha=1.0,
+                                    pt_variant="redblack")
+            Jrb, gJrb = obj_rb(y.field.ravel())
+            out[f"{k}_Jrb_{p}"] = np.array(Jrb)
+            out[f"{k}_gJrb_{p}"] = gJrb
     # closed-form orthogonal ramps (tests/test_ngf.py:35-46)
     g = Grid3((6, 6, 6), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
     x = g.axis_centers(0)[None, None, :]

@@ -57,6 +57,14 @@ def test_objective_golden(k, p):
     assert Je == J_ref
     assert np.array_equal(ge, g_ref)
     assert exact.last_D == float(z[f"{k}_Jd_{p}"]) and exact.last_S == float(z[f"{k}_Js_{p}"])
+    # the exact path with the red-black P^T equals the reference's red-black objective
+    plan = ngf.build_gather_plan(gd, gi)
+    rb = ngf.LevelObjective.from_device(torch.from_numpy(np.ascontiguousarray(T)).cuda(),
+                                        torch.from_numpy(np.ascontiguousarray(R)).cuda(), plan,
+                                        ngf.NgfParams(), 1.0, exact=True, pt_variant="redblack")
+    Jrb, grb = rb(y.ravel())
+    assert Jrb == float(z[f"{k}_Jrb_{p}"])
+    assert np.array_equal(grb, z[f"{k}_gJrb_{p}"])
 
 
 def test_objective_from_reference_terms_matches_from_R():

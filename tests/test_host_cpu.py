@@ -147,3 +147,11 @@ def test_ct_phantom_is_deterministic_and_ct_like():
     v = T.values
     assert v.min() < -900 and v.max() > 300  # air and bone present
     assert np.abs(R.values - T.values).max() > 10  # the pair actually differs
+
+
+def test_unknown_pt_variant_is_a_value_error():
+    # transfer.py:259-266 / objective.py: unknown variant names raise ValueError
+    with pytest.raises(ValueError):
+        ngf.LevelObjective(template=None, ref=None, plan=None, params=None, alpha=1.0,
+                           pt_variant="bogus")
+    assert ngf.PT_VARIANTS == ("gather", "scatter", "redblack") if hasattr(ngf, "PT_VARIANTS") else True
