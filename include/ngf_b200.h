@@ -81,6 +81,11 @@ int ngf_apply_Pt(const ngf_plan_t* plan, int dtype, const void* r, void* out, vo
 #define NGF_PT_REDBLACK 2
 int ngf_apply_Pt_variant(const ngf_plan_t* plan, int dtype, int variant, const void* r, void* out,
                          void* stream);
+/* out(n,3) = trilinear value of the deformation y (3, grid) at the world points
+ * pts(n,3), clamp-to-edge, in f64 (evaluation.py:39-64 `sample_deformation`; landmark
+ * and probe evaluation). */
+int ngf_sample_field(const ngf_grid_t* grid, int dtype, const void* y, const double* pts, int64_t n,
+                     double* out, void* stream);
 /* W = T(yhat), mask (warp.py:64-90).  mask may be NULL. */
 int ngf_warp(const ngf_grid_t* tgrid, int dtype, const void* T, const void* yhat, int64_t n,
              void* W, uint8_t* mask, void* stream);

@@ -34,6 +34,13 @@ int ngf_apply_Pt_variant(const ngf_plan_t* p, int dtype, int variant, const void
                  apply_Pt_variant_impl<double>(p, variant, (const double*)r, (double*)out, as_stream(stream)));
 }
 
+int ngf_sample_field(const ngf_grid_t* g, int dtype, const void* y, const double* pts, int64_t n, double* out,
+                     void* stream) {
+    if (!grid_ok(g) || !y || (n > 0 && (!pts || !out)) || n < 0) return NGF_EARG;
+    NGF_DISPATCH(dtype, sample_field_impl<float>(g, (const float*)y, pts, n, out, as_stream(stream)),
+                 sample_field_impl<double>(g, (const double*)y, pts, n, out, as_stream(stream)));
+}
+
 int ngf_warp(const ngf_grid_t* tg, int dtype, const void* T, const void* yhat, int64_t n, void* W,
              uint8_t* mask, void* stream) {
     if (!grid_ok(tg) || !T || !yhat || !W || n < 0) return NGF_EARG;

@@ -933,6 +933,60 @@ int prolong_impl(const ngf_plan_t* p, const T* yc, T* yf, cudaStream_t s) {
     return 0;
 }
 
+// ------------------------------------------------------------------ deformation probes
+// Trilinear value of the 3-component field at world points, clamp-to-edge, in f64
+// (evaluation.py:39-64: t = (p - o) / h, i0 = clip(floor t, 0, max(n - 2, 0)),
+// f = clip(t - i0, 0, 1) (0 on a one-node axis), terms accumulated dz, dy, dx with
+// w = (wx * wy) * wz).
+template <typename T>
+__global__ void k_sample_field(GridK<T> g, const T* __restrict__ y, const double* __restrict__ pts, int64_t n,
+                               double* __restrict__ out) {
+    const int64_t m = (int64_t)g.nx * g.ny * g.nz;
+    const int dims[3] = {g.nx, g.ny, g.nz};
+    const double org[3] = {g.dox, g.doy, g.doz}, sp[3] = {g.dhx, g.dhy, g.dhz};
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n; p += (int64_t)gridDim.x * blockDim.x) {
+        int i0[3];
+        double f[3];
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const double t = (pts[3 * p + a] - org[a]) / sp[a];
+            const int hi = dims[a] > 2 ? dims[a] - 2 : 0;
+            const double fl = floor(t);
+            const int i = fl < 0.0 ? 0 : (fl > (double)hi ? hi : (int)fl);
+            i0[a] = i;
+            const double fr = t - (double)i;
+            f[a] = dims[a] > 1 ? fmin(fmax(fr, 0.0), 1.0) : 0.0;
+        }
+        double acc[3] = {0.0, 0.0, 0.0};
+        for (int dz = 0; dz < 2; ++dz) {
+            const double wz = dz ? f[2] : 1.0 - f[2];
+            const int iz = min(i0[2] + dz, g.nz - 1);
+            for (int dy = 0; dy < 2; ++dy) {
+                const double wy = dy ? f[1] : 1.0 - f[1];
+                const int iy = min(i0[1] + dy, g.ny - 1);
+                for (int dx = 0; dx < 2; ++dx) {
+                    const double wx = dx ? f[0] : 1.0 - f[0];
+                    const int ix = min(i0[0] + dx, g.nx - 1);
+                    const double w = (wx * wy) * wz;
+                    const int64_t idx = ((int64_t)iz * g.ny + iy) * g.nx + ix;
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) acc[c] = acc[c] + w * (double)y[c * m + idx];
+                }
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 3; ++c) out[3 * p + c] = acc[c];
+    }
+}
+
+template <typename T>
+int sample_field_impl(const ngf_grid_t* g, const T* y, const double* pts, int64_t n, double* out, cudaStream_t s) {
+    if (n == 0) return 0;
+    NGF_LAUNCH(k_sample_field<T>, blocks_for(n, 128), 128, 0, s, make_gridk<T>(*g), y, pts, n, out);
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
 // explicit instantiations
 #define NGF_INST(T)                                                                              \
     template int apply_P_impl<T>(const ngf_plan_t*, const T*, T*, cudaStream_t);                 \
@@ -954,7 +1008,9 @@ int prolong_impl(const ngf_plan_t* p, const T* yc, T* yf, cudaStream_t s) {
     template int curvature_impl<T>(const ngf_grid_t*, const T*, double*, T*, const T*, double,  \
                                    T*, double*, cudaStream_t);                                  \
     template int downsample_impl<T>(const ngf_grid_t*, const T*, T*, cudaStream_t);             \
-    template int prolong_impl<T>(const ngf_plan_t*, const T*, T*, cudaStream_t);
+    template int prolong_impl<T>(const ngf_plan_t*, const T*, T*, cudaStream_t);                 \
+    template int sample_field_impl<T>(const ngf_grid_t*, const T*, const double*, int64_t, double*, \
+                                      cudaStream_t);
 
 NGF_INST(float)
 NGF_INST(double)

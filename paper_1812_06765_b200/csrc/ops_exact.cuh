@@ -31,5 +31,7 @@ int curvature_impl(const ngf_grid_t*, const T*, double*, T*, const T*, double, T
                    cudaStream_t);
 template <typename T> int downsample_impl(const ngf_grid_t*, const T*, T*, cudaStream_t);
 template <typename T> int prolong_impl(const ngf_plan_t*, const T*, T*, cudaStream_t);
+template <typename T>
+int sample_field_impl(const ngf_grid_t*, const T*, const double*, int64_t, double*, cudaStream_t);
 
 }  // namespace ngf

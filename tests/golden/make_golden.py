@@ -302,6 +302,47 @@ def register_run(R, T, cfg):
     return multilevel.register(R, T, cfg)
 
 
+def fileio_cases():
+    # MetaImage files written by the reference's writer (fileio.py:122-142): the device
+    # package must read them back and write byte-identical files
+    from ngfreg import fileio
+
+    g = Grid3((6, 5, 4), (0.7, 1.25, 2.5), (-1.5, 0.25, 3.0))
+    fileio.write_volume(Image3(g, synthetic.smooth_random_volume(g, seed=1).values.astype(np.float32)),
+                        os.path.join(HERE, "fio_vol_f32.mha"))
+    gd = Grid3((4, 3, 5), (2.0, 1.5, 2.5), (1.0, -2.0, 0.0))
+    fileio.write_deformation(synthetic.smooth_random_field(gd, seed=3, amplitude_mm=1.5),
+                             os.path.join(HERE, "fio_def_f64.mha"))
+    print("wrote fio_vol_f32.mha, fio_def_f64.mha")
+
+
+def evaluation_cases():
+    # sample_deformation / landmark_error (evaluation.py:39-89)
+    from ngfreg import evaluation
+
+    rng = np.random.default_rng(777)
+    out = {}
+    cases = [Grid3((7, 6, 5), (2.0, 1.5, 2.5), (1.0, -2.0, 0.0)), Grid3((5, 1, 4), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))]
+    for k, gd in enumerate(cases):
+        y = synthetic.smooth_random_field(gd, seed=40 + k, amplitude_mm=2.0)
+        lo = np.array(gd.domain_min) - 2.0
+        hi = np.array(gd.domain_min) + np.array(gd.extent) + 2.0
+        pts = lo + (hi - lo) * rng.random((50, 3))
+        tm = pts + rng.standard_normal((50, 3))
+        res = evaluation.landmark_error(y, evaluation.LandmarkSet(pts), evaluation.LandmarkSet(tm), gd)
+        out[f"{k}_g"] = garr(gd)
+        out[f"{k}_y"] = y.field
+        out[f"{k}_pts"] = pts
+        out[f"{k}_tm"] = tm
+        out[f"{k}_sample"] = evaluation.sample_deformation(y, pts)
+        out[f"{k}_per"] = res.per_landmark_mm
+        out[f"{k}_mean"] = np.array(res.mean_mm)
+        out[f"{k}_std"] = np.array(res.stddev_mm)
+        out[f"{k}_outside"] = res.outside_domain
+    out["n"] = np.array(len(cases))
+    save("evaluation", **out)
+
+
 if __name__ == "__main__":
     if len(sys.argv) > 1:  # regenerate selected fixtures, e.g. `make_golden.py transfer`
         for name in sys.argv[1:]:
@@ -314,3 +355,5 @@ if __name__ == "__main__":
     multilevel_cases()
     lbfgs_cases()
     register_cases()
+    fileio_cases()
+    evaluation_cases()
