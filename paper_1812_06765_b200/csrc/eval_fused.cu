@@ -967,7 +967,7 @@ __global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArg
 // 128^3 .. 256^3, the f64 march uses 32 x 20).
 using V0 = Cfg<20, 256, 2>;
 using V1 = Cfg<12, 256, 2>;
-using V2 = Cfg<28, 512, 1>;
+using V2 = Cfg<16, 320, 2>;
 using V3 = Cfg<12, 512, 2>;
 constexpr int kNumVariants = 4;
 

@@ -107,12 +107,54 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     const int ndx = (int)L->def.dims[0], ndy = (int)L->def.dims[1], ndz = (int)L->def.dims[2];
     std::vector<int> xl, xh, yl, yh, zl, zh;
     FusedPlan& fp = L->fp;
-    // kernel variant (f32: several tile/occupancy shapes; f64: one)
-    int variant = 1;  // 32x12 tiles, 256 threads, 2 CTAs/SM: fastest at 256^3 (tools/sweep.py)
-    if (const char* env = std::getenv("NGF_FUSED_VARIANT"))
-        variant = std::atoi(env) % fused_variant_count();
-    if (sizeof(T) == 8) variant = 0;
-    static const int kMinBlocks[] = {2, 2, 1, 2};
+    // kernel variant and z chunk, chosen together by minimising the modelled march time
+    //   ceil(CTAs / resident CTAs) x (cz + 10 planes of per-CTA fixed cost) x plane cost
+    // where the plane cost of a CTA is relative to variant 1 (measured, tools/sweep.py:
+    // 32 x 16 tiles of 320 threads do 1.26x the work of 32 x 12 tiles of 256 threads per
+    // plane in 1.26x the time, but waste less on the ring; which wins depends on how
+    // the CTA count fills the waves).  Every candidate chunk must keep each def node
+    // covered by at most kCover chunks (k_post's fixed-order sum).
+    static const int kMinBlocks[] = {2, 2, 2, 2};
+    static const double kPlaneCost[] = {1.6, 1.0, 1.26, 1.3};
+    std::vector<int> cand;
+    if (sizeof(T) == 8) {
+        cand = {0};  // one f64 variant
+    } else if (const char* env = std::getenv("NGF_FUSED_VARIANT")) {
+        cand = {std::atoi(env) % fused_variant_count()};
+    } else {
+        cand = {1, 2};
+    }
+    const int nzs = zhi - zlo;
+    auto valid = [&](int c) {
+        std::vector<int> a, b;
+        tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b, zlo, zhi);
+        std::vector<int32_t> cov;
+        return build_cover(a, b, ndz, cov);
+    };
+    int variant = -1, cz = 0;
+    double best = 1e300;
+    for (int v : cand) {
+        int ty, nth;
+        fused_variant_geom(v, &ty, &nth);
+        std::vector<int> a, b;
+        const int wx = tile_windows(p->h_i0[0], nx, ndx, kTX, 1, a, b);
+        const int ntx = (int)a.size();
+        const int wy = tile_windows(p->h_i0[1], ny, ndy, ty, 1, a, b);
+        const int nty = (int)a.size();
+        if (fused_smem<T>(v, wx, wy) > size_t(220) * 1024) continue;
+        const int64_t resident = (int64_t)kSMs * kMinBlocks[v];
+        for (int c = std::min(nzs, 96); c >= 1; --c) {
+            const int64_t nct = (int64_t)ntx * nty * ((nzs + c - 1) / c);
+            const double waves = (double)((nct + resident - 1) / resident);
+            const double cost = waves * (c + 10) * kPlaneCost[v];
+            if (cost < best * 0.999 && valid(c)) {
+                best = cost;
+                cz = c;
+                variant = v;
+            }
+        }
+    }
+    if (variant < 0) return NGF_EARG;
     fp.variant = variant;
     // two-slot float2 march: opt-in (measured 388 us vs 375 us for the scalar march at
     // 256^3 -- the FP issue slots it saves are spent on pair formation and masking)
@@ -123,29 +165,6 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     fp.ntx = (int)xl.size();
     fp.nty = (int)yl.size();
     fp.smem_bytes = fused_smem<T>(variant, fp.wx, fp.wy);
-    if (fp.smem_bytes > size_t(220) * 1024) return NGF_EARG;
-    // z chunk: every candidate must keep each def node covered by at most kCover chunks
-    // (the reduce kernel's fixed-order sum).  Among those, minimise the modelled time
-    // (waves of resident CTAs) x (planes marched per CTA, incl. the ring and pipeline).
-    auto valid = [&](int c) {
-        std::vector<int> a, b;
-        tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b, zlo, zhi);
-        std::vector<int32_t> cov;
-        return build_cover(a, b, ndz, cov);
-    };
-    const int64_t resident = (int64_t)kSMs * kMinBlocks[variant];
-    int cz = 0;
-    double best = 1e300;
-    const int nzs = zhi - zlo;
-    for (int c = std::min(nzs, 96); c >= 1; --c) {
-        const int64_t nct = (int64_t)fp.ntx * fp.nty * ((nzs + c - 1) / c);
-        const double waves = (double)((nct + resident - 1) / resident);
-        const double cost = waves * (c + 10);  // ~10 planes of per-CTA fixed cost (measured)
-        if (cost < best * 0.999 && valid(c)) {
-            best = cost;
-            cz = c;
-        }
-    }
     if (!cz) return NGF_EARG;
     if (const char* env = std::getenv("NGF_FUSED_CZ")) {  // tuning / debugging override
         const int forced = std::atoi(env);
