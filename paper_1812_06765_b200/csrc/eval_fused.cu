@@ -33,7 +33,6 @@
 
 namespace ngf {
 
-constexpr int kCzMax = 96;  // longest z chunk a CTA marches
 
 // Tile / launch configuration of one kernel variant.
 template <int TY_, int NT_, int MINB_>
@@ -427,8 +426,8 @@ __device__ __forceinline__ CtaGeo cta_geo(const FusedArgs<T>& a) {
     g.tz = cta / (fp.ntx * fp.nty);
     g.x0 = g.tx * C::TX;
     g.y0 = g.ty * C::TY;
-    g.z0 = fp.zlo + g.tz * fp.cz;
-    g.z1 = min(g.z0 + fp.cz, fp.zhi);
+    g.z0 = fp.zb_tab[g.tz];
+    g.z1 = fp.zb_tab[g.tz + 1];
     g.zb = g.z0 - 1;  // first plane of the z tables
     g.jfirst = max(g.z0 - 1, 0);
     g.jlast = min(g.z1, a.nz - 1);

@@ -7,18 +7,20 @@ namespace ngf {
 // Tile geometry of the fused kernel: kTX x TY image voxels per CTA in x/y (TY per
 // kernel variant), a ring of one voxel around it, marching cz planes in z.
 constexpr int kTX = 32;
+constexpr int kCzMax = 96;  // longest z chunk a CTA marches (shared z tables)
 
 struct FusedPlan {
     // kernel variant (tile rows, threads per CTA, occupancy) and tiles
     int variant, ty, nthreads;
     int packed;  // two-slot float2 march (f32 variants with two slots per thread)
-    int ntx, nty, ntz, cz;
+    int ntx, nty, ntz, cz;  // cz: largest z chunk
     int zlo, zhi;  // image planes evaluated (a z-slab for config-5 decomposition; 0, nz otherwise)
     // P^T windows: max sizes and per-tile lower def index (device arrays)
     int wx, wy, wz;
     const int32_t* win_x;  // [ntx]
     const int32_t* win_y;  // [nty]
     const int32_t* win_z;  // [ntz]
+    const int32_t* zb_tab; // [ntz + 1] z chunk boundaries (image planes), chunk sizes non-increasing
     // reduce cover lists: per def index up to kCover (tile, offset) pairs, -1 terminated
     const int32_t* cov_x;  // [ndx * kCover * 2]
     const int32_t* cov_y;

@@ -4,6 +4,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <vector>
 
 #include "common.cuh"
@@ -83,6 +84,47 @@ static int tile_windows(const int32_t* i0, int n, int nd, int tile, int ring_lo,
     return wmax;
 }
 
+// windows of explicit z chunks [bounds[t], bounds[t+1]) plus a one-plane ring each side
+static int chunk_windows(const int32_t* i0, int n, int nd, const std::vector<int>& bounds, std::vector<int>& lo,
+                         std::vector<int>& hi) {
+    const int nt = (int)bounds.size() - 1;
+    lo.resize(nt);
+    hi.resize(nt);
+    int wmax = 1;
+    for (int t = 0; t < nt; ++t) {
+        const int a = std::max(bounds[t] - 1, 0);
+        const int b = std::min(bounds[t + 1], n - 1);  // ring plane after the chunk
+        const int l = i0[a];
+        int h = nd > 1 ? i0[b] + 1 : 0;
+        if (h > nd - 1) h = nd - 1;
+        lo[t] = l;
+        hi[t] = h;
+        wmax = std::max(wmax, h - l + 1);
+    }
+    return wmax;
+}
+
+// Makespan of greedy list scheduling (the hardware CTA dispatcher in blockIdx order) of
+// `classes` = (item count, item cost) in order on `slots` identical slots.
+static double list_schedule(const std::vector<std::pair<int64_t, double>>& classes, int64_t slots) {
+    std::map<double, int64_t> free_at{{0.0, slots}};
+    double makespan = 0.0;
+    for (const auto& cl : classes) {
+        int64_t left = cl.first;
+        while (left > 0) {
+            auto it = free_at.begin();
+            const double t = it->first;
+            const int64_t k = std::min(left, it->second);
+            it->second -= k;
+            if (it->second == 0) free_at.erase(it);
+            free_at[t + cl.second] += k;
+            makespan = std::max(makespan, t + cl.second);
+            left -= k;
+        }
+    }
+    return makespan;
+}
+
 static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, int nd,
                         std::vector<int32_t>& cov) {
     cov.assign((size_t)nd * kCover * 2, -1);
@@ -107,13 +149,15 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     const int ndx = (int)L->def.dims[0], ndy = (int)L->def.dims[1], ndz = (int)L->def.dims[2];
     std::vector<int> xl, xh, yl, yh, zl, zh;
     FusedPlan& fp = L->fp;
-    // kernel variant and z chunk, chosen together by minimising the modelled march time
-    //   ceil(CTAs / resident CTAs) x (cz + 10 planes of per-CTA fixed cost) x plane cost
-    // where the plane cost of a CTA is relative to variant 1 (measured, tools/sweep.py:
-    // 32 x 16 tiles of 320 threads do 1.26x the work of 32 x 12 tiles of 256 threads per
-    // plane in 1.26x the time, but waste less on the ring; which wins depends on how
-    // the CTA count fills the waves).  Every candidate chunk must keep each def node
-    // covered by at most kCover chunks (k_post's fixed-order sum).
+    // Kernel variant and z chunking, chosen together by simulating the CTA dispatch:
+    // every tile column is cut into nb chunks of B planes followed by the remainder in
+    // m near-equal smaller chunks; CTAs are numbered chunk-major, so all columns' big
+    // chunks are dispatched first and the small ones fill the last wave (longest
+    // processing time first).  A chunk of c planes costs (c + 10) x plane cost: ~10 planes
+    // of per-CTA fixed work (tables, ring planes, pipeline fill), and a plane cost
+    // relative to variant 1 (tools/sweep.py: 32 x 16 tiles of 320 threads take 1.26x the
+    // time of 32 x 12 tiles of 256 threads per plane for 1.33x the voxels).  Every
+    // chunking must keep each def node covered by at most kCover chunks (k_post's sum).
     static const int kMinBlocks[] = {2, 2, 2, 2};
     static const double kPlaneCost[] = {1.6, 1.0, 1.26, 1.3};
     std::vector<int> cand;
@@ -125,14 +169,13 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         cand = {1, 2};
     }
     const int nzs = zhi - zlo;
-    auto valid = [&](int c) {
-        std::vector<int> a, b;
-        tile_windows(p->h_i0[2], nz, ndz, c, 1, a, b, zlo, zhi);
-        std::vector<int32_t> cov;
-        return build_cover(a, b, ndz, cov);
+    const int forced_cz = std::getenv("NGF_FUSED_CZ") ? std::atoi(std::getenv("NGF_FUSED_CZ")) : 0;
+    struct Choice {
+        double cost;
+        int variant;
+        std::vector<int> sizes;
     };
-    int variant = -1, cz = 0;
-    double best = 1e300;
+    std::vector<Choice> choices;
     for (int v : cand) {
         int ty, nth;
         fused_variant_geom(v, &ty, &nth);
@@ -142,16 +185,52 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         const int wy = tile_windows(p->h_i0[1], ny, ndy, ty, 1, a, b);
         const int nty = (int)a.size();
         if (fused_smem<T>(v, wx, wy) > size_t(220) * 1024) continue;
-        const int64_t resident = (int64_t)kSMs * kMinBlocks[v];
-        for (int c = std::min(nzs, 96); c >= 1; --c) {
-            const int64_t nct = (int64_t)ntx * nty * ((nzs + c - 1) / c);
-            const double waves = (double)((nct + resident - 1) / resident);
-            const double cost = waves * (c + 10) * kPlaneCost[v];
-            if (cost < best * 0.999 && valid(c)) {
-                best = cost;
-                cz = c;
-                variant = v;
+        const int64_t cols = (int64_t)ntx * nty, slots = (int64_t)kSMs * kMinBlocks[v];
+        auto add = [&](std::vector<int> sizes) {
+            std::vector<std::pair<int64_t, double>> cls;
+            for (int s : sizes) cls.push_back({cols, (s + 10) * kPlaneCost[v]});
+            choices.push_back({list_schedule(cls, slots), v, std::move(sizes)});
+        };
+        for (int B = std::min(nzs, kCzMax); B >= 1; --B) {
+            if (forced_cz > 0 && B != std::min(forced_cz, nzs)) continue;
+            for (int nb = 1; nb * B <= nzs; ++nb) {
+                const int r = nzs - nb * B;
+                std::vector<int> big(nb, B);
+                if (r == 0) {
+                    add(big);
+                    continue;
+                }
+                if (forced_cz > 0) {  // uniform chunks of the forced size
+                    if (nb == nzs / B) {
+                        big.push_back(r);
+                        add(big);
+                    }
+                    continue;
+                }
+                for (int div = 1; div <= 4; ++div) {  // remainder in m chunks of <= B / div
+                    const int cap = std::max(1, B / div);
+                    const int m = (r + cap - 1) / cap;
+                    std::vector<int> sizes = big;
+                    for (int i = 0; i < m; ++i) sizes.push_back(r / m + (i < r % m ? 1 : 0));
+                    std::sort(sizes.begin() + nb, sizes.end(), std::greater<int>());
+                    add(sizes);
+                }
             }
+        }
+    }
+    std::stable_sort(choices.begin(), choices.end(),
+                     [](const Choice& x, const Choice& y) { return x.cost < y.cost; });
+    std::vector<int> bounds;
+    int variant = -1;
+    for (const Choice& ch : choices) {  // cheapest valid chunking
+        std::vector<int> bd(1, zlo), a, b;
+        for (int s : ch.sizes) bd.push_back(bd.back() + s);
+        chunk_windows(p->h_i0[2], nz, ndz, bd, a, b);
+        std::vector<int32_t> cov;
+        if (build_cover(a, b, ndz, cov)) {
+            bounds = bd;
+            variant = ch.variant;
+            break;
         }
     }
     if (variant < 0) return NGF_EARG;
@@ -165,15 +244,11 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     fp.ntx = (int)xl.size();
     fp.nty = (int)yl.size();
     fp.smem_bytes = fused_smem<T>(variant, fp.wx, fp.wy);
-    if (!cz) return NGF_EARG;
-    if (const char* env = std::getenv("NGF_FUSED_CZ")) {  // tuning / debugging override
-        const int forced = std::atoi(env);
-        if (forced > 0 && forced <= 96 && valid(forced)) cz = forced;
-    }
-    fp.cz = cz;
+    fp.cz = 0;
+    for (size_t t = 0; t + 1 < bounds.size(); ++t) fp.cz = std::max(fp.cz, bounds[t + 1] - bounds[t]);
     fp.zlo = zlo;
     fp.zhi = zhi;
-    fp.wz = tile_windows(p->h_i0[2], nz, ndz, cz, 1, zl, zh, zlo, zhi);
+    fp.wz = chunk_windows(p->h_i0[2], nz, ndz, bounds, zl, zh);
     fp.ntz = (int)zl.size();
     fp.n_cta = fp.ntx * fp.nty * fp.ntz;
     std::vector<int32_t> cx, cy, cz_;
@@ -225,9 +300,10 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         return off;
     };
     std::vector<int32_t> wxv(xl.begin(), xl.end()), wyv(yl.begin(), yl.end()), wzv(zl.begin(), zl.end());
+    std::vector<int32_t> zbv(bounds.begin(), bounds.end());
     auto appv = [&](const std::vector<int32_t>& v) { return app(v.data(), v.size() * 4); };
     size_t o_wx = appv(wxv), o_wy = appv(wyv), o_wz = appv(wzv), o_cx = appv(cx), o_cy = appv(cy),
-           o_cz = appv(cz_), o_xcsr = appv(xcsr), o_ycsr = appv(ycsr),
+           o_cz = appv(cz_), o_zb = appv(zbv), o_xcsr = appv(xcsr), o_ycsr = appv(ycsr),
            o_xcw = app(xcw.data(), xcw.size() * sizeof(T)), o_ycw = app(ycw.data(), ycw.size() * sizeof(T));
     NGF_CUDA(cudaMalloc(&L->fp_blob, blob.size() * 4));
     NGF_CUDA(cudaMemcpy(L->fp_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice));
@@ -238,6 +314,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     fp.cov_x = b + o_cx;
     fp.cov_y = b + o_cy;
     fp.cov_z = b + o_cz;
+    fp.zb_tab = b + o_zb;
     fp.xcsr = b + o_xcsr;
     fp.ycsr = b + o_ycsr;
     fp.xcw = b + o_xcw;
