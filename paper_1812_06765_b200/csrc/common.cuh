@@ -12,6 +12,10 @@ namespace ngf {
 
 extern std::atomic<int64_t> g_launches;
 
+// Stream-ordered pool allocations for plans and levels (plan.cu); 0 or NGF_ENOMEM.
+int dev_alloc(void** ptr, size_t bytes);
+void dev_free(void* ptr);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Count every kernel launch issued by the library (bench.py reports them).

@@ -193,7 +193,8 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         };
         for (int B = std::min(nzs, kCzMax); B >= 1; --B) {
             if (forced_cz > 0 && B != std::min(forced_cz, nzs)) continue;
-            for (int nb = 1; nb * B <= nzs; ++nb) {
+            // big-chunk counts that leave less than ~3 big chunks for the remainder
+            for (int nb = std::max(1, nzs / B - 2); nb * B <= nzs; ++nb) {
                 const int r = nzs - nb * B;
                 std::vector<int> big(nb, B);
                 if (r == 0) {
@@ -305,7 +306,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     size_t o_wx = appv(wxv), o_wy = appv(wyv), o_wz = appv(wzv), o_cx = appv(cx), o_cy = appv(cy),
            o_cz = appv(cz_), o_zb = appv(zbv), o_xcsr = appv(xcsr), o_ycsr = appv(ycsr),
            o_xcw = app(xcw.data(), xcw.size() * sizeof(T)), o_ycw = app(ycw.data(), ycw.size() * sizeof(T));
-    NGF_CUDA(cudaMalloc(&L->fp_blob, blob.size() * 4));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&L->fp_blob, blob.size() * 4));
     NGF_CUDA(cudaMemcpy(L->fp_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice));
     const int32_t* b = (const int32_t*)L->fp_blob;
     fp.win_x = b + o_wx;
@@ -320,10 +321,10 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     fp.xcw = b + o_xcw;
     fp.ycw = b + o_ycw;
     const size_t win = (size_t)fp.wz * fp.wy * fp.wx;
-    NGF_CUDA(cudaMalloc(&L->partial, (size_t)fp.n_cta * 3 * win * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&L->dpart, (size_t)fp.n_cta * sizeof(double)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&L->partial, (size_t)fp.n_cta * 3 * win * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&L->dpart, (size_t)fp.n_cta * sizeof(double)));
     L->ns = (int)(((L->def.dims[0] + 31) / 32) * ((L->def.dims[1] + 7) / 8) * 3 * L->def.dims[2]);
-    NGF_CUDA(cudaMalloc(&L->spart, (size_t)L->ns * sizeof(double)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&L->spart, (size_t)L->ns * sizeof(double)));
     return fused_prepare<T>(variant, fp.smem_bytes);
 }
 
@@ -382,15 +383,15 @@ static int exact_alloc(ngf_level* L) {
     LevelWork& w = L->ex;
     if (w.yhat) return 0;
     const int64_t n = grid_n(L->img), m = grid_n(L->def);
-    NGF_CUDA(cudaMalloc(&w.yhat, 3 * n * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.W, n * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.terms, n * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.q, 3 * n * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.s, n * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.ghat, 3 * n * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.gD, 3 * m * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.cws, 6 * m * sizeof(T)));
-    NGF_CUDA(cudaMalloc(&w.dws, 8 * sizeof(double)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.yhat, 3 * n * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.W, n * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.terms, n * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.q, 3 * n * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.s, n * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.ghat, 3 * n * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.gD, 3 * m * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.cws, 6 * m * sizeof(T)));
+    NGF_CUDA((cudaError_t)dev_alloc((void**)&w.dws, 8 * sizeof(double)));
     return 0;
 }
 
@@ -487,8 +488,8 @@ static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_g
     cudaStream_t s = as_stream(stream);
     const int64_t n = grid_n(L->img);
     const size_t es = dtype == NGF_F32 ? 4 : 8;
-    if (cudaMalloc(&L->gR, 3 * n * es) || cudaMalloc(&L->nR, n * es) ||
-        cudaMalloc(&L->RT, n * 4 * es) || cudaMalloc(&L->flag, 16)) {
+    if (dev_alloc(&L->gR, 3 * n * es) || dev_alloc(&L->nR, n * es) || dev_alloc(&L->RT, n * 4 * es) ||
+        dev_alloc((void**)&L->flag, 16)) {
         ngf_level_destroy(L);
         return NGF_ENOMEM;
     }
@@ -540,8 +541,8 @@ void ngf_level_destroy(ngf_level_t* L) {
     void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart,
                     L->ex.yhat, L->ex.W, L->ex.terms, L->ex.q, L->ex.s, L->ex.ghat, L->ex.gD,
                     L->ex.cws, L->ex.dws};
-    for (void* b : bufs)
-        if (b) cudaFree(b);
+    cudaDeviceSynchronize();  // no kernel may still use them
+    for (void* b : bufs) dev_free(b);
     for (int k = 0; k < 2; ++k)
         if (L->ev[k]) cudaEventDestroy(L->ev[k]);
     std::free(L);
@@ -569,8 +570,7 @@ int ngf_level_set_zrange(ngf_level_t* L, int64_t zlo, int64_t zhi) {
     if (!L || zlo < 0 || zhi > L->img.dims[2] || zlo >= zhi) return NGF_EARG;
     NGF_CUDA(cudaDeviceSynchronize());
     void* bufs[] = {L->fp_blob, L->partial, L->dpart, L->spart};
-    for (void* b : bufs)
-        if (b) cudaFree(b);
+    for (void* b : bufs) dev_free(b);
     L->fp_blob = L->partial = nullptr;
     L->dpart = L->spart = nullptr;
     return L->dtype == NGF_F32 ? fused_setup<float>(L, (int)zlo, (int)zhi)

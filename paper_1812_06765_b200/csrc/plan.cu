@@ -17,6 +17,31 @@ namespace ngf {
 
 std::atomic<int64_t> g_launches{0};
 
+// Device memory of plans and levels comes from the device's stream-ordered pool
+// (cudaMallocAsync on the legacy default stream), configured once per device to keep
+// freed blocks: the levels of the next registration reuse them without driver calls
+// (a 256^3 level needs ~0.6 GB).
+int dev_alloc(void** ptr, size_t bytes) {
+    static std::atomic<uint64_t> ready{0};
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) return NGF_ENOMEM;
+    if (d < 64 && !(ready.load() & (1ull << d))) {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, d) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+        ready.fetch_or(1ull << d);
+    }
+    *ptr = nullptr;
+    if (bytes == 0) bytes = 1;
+    return cudaMallocAsync(ptr, bytes, 0) == cudaSuccess ? NGF_OK : NGF_ENOMEM;
+}
+
+void dev_free(void* ptr) {
+    if (ptr) cudaFreeAsync(ptr, 0);
+}
+
 static bool same_extent(const ngf_grid_t& a, const ngf_grid_t& b, double tol = 1e-9) {
     for (int k = 0; k < 3; ++k) {
         double lo_a = a.origin[k] - a.spacing[k] / 2;
@@ -138,7 +163,7 @@ int plan_upload(ngf_plan_t* p) {
     }
     std::vector<char> host(blob);
     void* d_blob = nullptr;
-    if (cudaMalloc(&d_blob, blob) != cudaSuccess) return NGF_ENOMEM;
+    if (dev_alloc(&d_blob, blob)) return NGF_ENOMEM;
     size_t off = 0;
     char* dbase = (char*)d_blob;
     for (int k = 0; k < 3; ++k) {
@@ -164,12 +189,12 @@ int plan_upload(ngf_plan_t* p) {
         a.wd = (const double*)put(p->h_w[k], (size_t)nd * w * 8);
     }
     if (cudaMemcpy(d_blob, host.data(), blob, cudaMemcpyHostToDevice) != cudaSuccess) {
-        cudaFree(d_blob);
+        dev_free(d_blob);
         return NGF_ENOMEM;
     }
     p->tmp_bytes = (size_t)3 * p->img_grid.dims[2] * p->def_grid.dims[1] * p->def_grid.dims[0] * 8;
-    if (cudaMalloc(&p->d_tmp, p->tmp_bytes) != cudaSuccess) {
-        cudaFree(d_blob);
+    if (dev_alloc(&p->d_tmp, p->tmp_bytes)) {
+        dev_free(d_blob);
         return NGF_ENOMEM;
     }
     p->d_blob = d_blob;
@@ -197,8 +222,9 @@ void ngf_plan_destroy(ngf_plan_t* p) {
         std::free(p->h_counts[k]);
         std::free(p->h_w[k]);
     }
-    if (p->d_blob) cudaFree(p->d_blob);
-    if (p->d_tmp) cudaFree(p->d_tmp);
+    if (p->d_blob || p->d_tmp) cudaDeviceSynchronize();  // no kernel may still use them
+    ngf::dev_free(p->d_blob);
+    ngf::dev_free(p->d_tmp);
     std::free(p);
 }
 
