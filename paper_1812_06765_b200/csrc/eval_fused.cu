@@ -35,9 +35,10 @@ namespace ngf {
 
 
 // Tile / launch configuration of one kernel variant.
-template <int TY_, int NT_, int MINB_>
+template <int TY_, int NT_, int MINB_, bool DTS_ = false>
 struct Cfg {
     static constexpr int TX = 32, TY = TY_, NT = NT_, MINB = MINB_;
+    static constexpr bool DTS = DTS_;  // interpolant derivative ring in shared memory (frees 9 S registers)
     static constexpr int E1X = TX + 2, E1Y = TY + 2, E1 = E1X * E1Y;
     static constexpr int S = (E1 + NT - 1) / NT;
     static constexpr int E2X = TX + 4, E2Y = TY + 4, E2 = E2X * E2Y;
@@ -81,6 +82,8 @@ struct SmemL {
     T Wsm[3][C::E1 + 1];        // W ring (planes p-2, p-1, p); [E1] = padding-slot sink
     T qx[2][C::E2], qy[2][C::E2];  // q_x, q_y of planes p-1 (written) / p-2 (read), zero-padded
     T buf[3][C::E1 + 1];        // completed deformation plane (z-reduced ghat)
+    T dTs[C::DTS ? 4 : 1][3][C::DTS ? C::E1 + 1 : 1];  // DTS: interpolant derivative / h,
+                                // [plane & 3][axis][E1 position] (4 slots: (C) of step p-1 may still read plane p-3)
     T Xr[3][C::E1Y][C::WXMAX];  // x-reduced
     T colG[C::E1X][3], colGt[C::E1X][3], rowG[C::E1Y][3], rowGt[C::E1Y][3];  // face coefficients
     T colPw[C::E1X], rowPw[C::E1Y];  // P weights
@@ -107,9 +110,9 @@ struct March {
     unsigned flags;     // per slot s, bits 4s..4s+3: in volume (x/y), tile interior, x face, y face
     bool wface;         // some lane of the warp has a slot next to a volume face
     T ylo[C::S][3], yhi[C::S][3];  // P_xy y on the current def-plane pair
-    T dT[C::S][3][3];              // interpolant derivative / h, plane ring
     T qz[C::S][3];                 // q_z, plane ring
     T A0[C::S][3], A1[C::S][3];    // z-accumulated ghat for def planes zd, zd+1
+    T dT[C::DTS ? 1 : C::S][3][3];  // !DTS: interpolant derivative / h, plane ring
     V4T<T> rt[C::S];               // prefetched reference terms (next B plane)
     int z0, z1, zb, jfirst, jlast, wzlo, cur_zd, cta;
     double dacc;
@@ -293,15 +296,24 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
             T W, d0, d1, d2;
             trilinear(a, cv[s], fx[s], fy[s], fz[s], W, d0, d1, d2);
             if (!in[s]) W = d0 = d1 = d2 = (T)0;
-            m.dT[s][R][0] = d0;
-            m.dT[s][R][1] = d1;
-            m.dT[s][R][2] = d2;
+            if constexpr (C::DTS) {
+                sm.dTs[p & 3][0][m.P[s]] = d0;
+                sm.dTs[p & 3][1][m.P[s]] = d1;
+                sm.dTs[p & 3][2][m.P[s]] = d2;
+            } else {
+                m.dT[s][R][0] = d0;
+                m.dT[s][R][1] = d1;
+                m.dT[s][R][2] = d2;
+            }
             sm.Wsm[R][m.P[s]] = W;
         }
     } else {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
-            m.dT[s][R][0] = m.dT[s][R][1] = m.dT[s][R][2] = (T)0;
+            if constexpr (C::DTS)
+                sm.dTs[p & 3][0][m.P[s]] = sm.dTs[p & 3][1][m.P[s]] = sm.dTs[p & 3][2][m.P[s]] = (T)0;
+            else
+                m.dT[s][R][0] = m.dT[s][R][1] = m.dT[s][R][2] = (T)0;
             sm.Wsm[R][m.P[s]] = (T)0;
         }
     }
@@ -378,7 +390,7 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
         sv = fmaf_t(gtm, m.qz[s][R], fmaf_t(gt0, m.qz[s][RC], fmaf_t(gtp, m.qz[s][RB], sv)));
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-            const T g = sv * m.dT[s][RC][c];
+            const T g = sv * (C::DTS ? sm.dTs[j & 3][c][m.P[s]] : m.dT[s][RC][c]);
             m.A0[s][c] = fmaf_t(w0, g, m.A0[s][c]);
             m.A1[s][c] = fmaf_t(w1, g, m.A1[s][c]);
         }
@@ -564,9 +576,13 @@ __global__ void __launch_bounds__(C::NT, C::MINB) k_eval_fused(const __grid_cons
         slot_geom<T, C>(a, g, s, m.P[s], m.P2[s], m.ij[s], fl);
         m.flags |= fl << (4 * s);
 #pragma unroll
-        for (int r = 0; r < 3; ++r) {
-            m.qz[s][r] = (T)0;
-            m.dT[s][r][0] = m.dT[s][r][1] = m.dT[s][r][2] = (T)0;
+        for (int r = 0; r < 3; ++r) m.qz[s][r] = (T)0;
+        if constexpr (C::DTS) {
+#pragma unroll
+            for (int r = 0; r < 4; ++r) sm.dTs[r][0][m.P[s]] = sm.dTs[r][1][m.P[s]] = sm.dTs[r][2][m.P[s]] = (T)0;
+        } else {
+#pragma unroll
+            for (int r = 0; r < 3; ++r) m.dT[s][r][0] = m.dT[s][r][1] = m.dT[s][r][2] = (T)0;
         }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
@@ -961,13 +977,15 @@ __global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArg
 
 // ------------------------------------------------------------------ host launchers
 
-// Kernel variants: tile rows TY, threads per CTA, minimum resident CTAs per SM
-// (tools/sweep.py; 32 x 12 / 256 threads / 2 CTAs per SM is the fastest f32 shape at
-// 128^3 .. 256^3, the f64 march uses 32 x 20).
+// Kernel variants: tile rows TY, threads per CTA, minimum resident CTAs per SM, derivative
+// ring in shared memory (tools/sweep.py).  f32 default: 32 x 16 tiles of 320 threads with
+// the ring in shared memory (96 registers, 2 CTAs = 20 warps per SM, ring overhead 1.2);
+// 32 x 12 / 256 threads keeps the ring in registers (128 registers, 16 warps per SM) and
+// wins when its CTA count fills the waves better; the f64 march uses 32 x 20.
 using V0 = Cfg<20, 256, 2>;
 using V1 = Cfg<12, 256, 2>;
-using V2 = Cfg<16, 320, 2>;
-using V3 = Cfg<12, 512, 2>;
+using V2 = Cfg<16, 320, 2, true>;
+using V3 = Cfg<18, 352, 2, true>;
 constexpr int kNumVariants = 4;
 
 void fused_variant_geom(int v, int* ty, int* nt) {

@@ -155,11 +155,12 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     // chunks are dispatched first and the small ones fill the last wave (longest
     // processing time first).  A chunk of c planes costs (c + 10) x plane cost: ~10 planes
     // of per-CTA fixed work (tables, ring planes, pipeline fill), and a plane cost
-    // relative to variant 1 (tools/sweep.py: 32 x 16 tiles of 320 threads take 1.26x the
-    // time of 32 x 12 tiles of 256 threads per plane for 1.33x the voxels).  Every
+    // relative to variant 1 (tools/sweep.py at 128^3 .. 512^3: 32 x 16 tiles of 320
+    // threads with the derivative ring in shared memory take 1.16x the time of 32 x 12
+    // tiles of 256 threads per plane for 1.33x the voxels).  Every
     // chunking must keep each def node covered by at most kCover chunks (k_post's sum).
     static const int kMinBlocks[] = {2, 2, 2, 2};
-    static const double kPlaneCost[] = {1.6, 1.0, 1.26, 1.3};
+    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5};
     std::vector<int> cand;
     if (sizeof(T) == 8) {
         cand = {0};  // one f64 variant
