@@ -61,6 +61,17 @@ def dist_env():
     return ws, rank, local
 
 
+def ncu_traffic(workload):
+    """DRAM bytes per launch of the fused kernel from the committed ncu capture
+    (profiles/ncu_traffic.json), or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            t = json.load(fh).get(workload)
+        return None if t is None else int(t["dram_read_bytes"]) + int(t["dram_write_bytes"])
+    except (OSError, ValueError, KeyError):
+        return None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -338,7 +349,7 @@ def run_ours(args):
                        "parallelism": (f"z-slabs x{ws} (one pair; NCCL all-reduce of grad D and D)"
                                        if strong else f"replicas x{ws} (one independent pair per GPU)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
                          "kernel": "k_eval_fused", "kernel_ms": k_ms,
                          "bytes_per_launch": bytes_kernel, "peak_kind": peak_kind,
                          "eval_frac": bytes_eval / (eval_ms / 1000.0) / 1e9 / peak,
