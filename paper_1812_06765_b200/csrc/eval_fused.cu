@@ -42,7 +42,9 @@ struct Cfg {
     static constexpr int E1X = TX + 2, E1Y = TY + 2, E1 = E1X * E1Y;
     static constexpr int S = (E1 + NT - 1) / NT;
     static constexpr int E2X = TX + 4, E2Y = TY + 4, E2 = E2X * E2Y;
-    static constexpr int WXMAX = E1X + 1, WYMAX = E1Y + 1;  // P^T window bounds
+    // P^T window bounds: the ring widens a tile by 2 voxels, +1 for the upper node, +1 where
+    // the index map advances by 2 (w1 rounding to just below 1 when grids nearly coincide)
+    static constexpr int WXMAX = E1X + 2, WYMAX = E1Y + 2;
 };
 
 template <typename T>

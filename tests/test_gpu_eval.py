@@ -207,3 +207,20 @@ def test_packed_march_matches_scalar_march(monkeypatch, dims, spacing, ratio):
         out.append((sc, g.cpu().numpy()))
     assert out[0][0][1] == out[1][0][1]  # D: forward terms bit-identical
     assert np.max(np.abs(out[0][1] - out[1][1])) <= 1e-5 * np.max(np.abs(out[0][1]))
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("dims,ratio", [((40, 40, 40), 1), ((70, 45, 33), 4)])
+def test_every_kernel_variant_within_tolerance(monkeypatch, variant, dims, ratio):
+    """Each tile/occupancy variant of the fused march (forced with NGF_FUSED_VARIANT),
+    incl. ratio 1 on non-unit spacing where the index map can advance by 2 (widest windows)."""
+    monkeypatch.setenv("NGF_FUSED_VARIANT", variant)
+    gi = ngf.Grid3(dims, (1.0, 1.1, 0.9), (-3.0, 2.0, 1.0))
+    gd = ngf.deformation_grid_for(gi, ratio)
+    R = ngf.smooth_random_volume(gi, seed=5).values.astype(np.float32)
+    T = ngf.smooth_random_volume(gi, seed=6).values.astype(np.float32)
+    y = ngf.smooth_random_field(gd, seed=7, amplitude_mm=2.5).field.astype(np.float32)
+    J_ref, g_ref = O.Objective(T, R, _og(gd), _og(gi))(y.ravel())
+    J, g = _device_obj(T, R, gd, gi)(y.ravel())
+    assert abs(J - J_ref) <= TOL_J * abs(J_ref), (J, J_ref)
+    assert _rel(g, g_ref) <= TOL_G
