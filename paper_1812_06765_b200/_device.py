@@ -72,6 +72,23 @@ _BIG_UPLOAD = 8 << 20
 _stage = {"buf": None, "event": None, "pool": None}
 
 
+def par_copy(dst: np.ndarray, src: np.ndarray, parts: int = 4) -> None:
+    """dst[...] = src with a few threads (numpy copies release the GIL): host staging
+    copies of multi-MB vectors run at ~4x the single-thread bandwidth."""
+    d, s = dst.reshape(-1), src.reshape(-1)
+    if s.nbytes < (1 << 20):
+        d[:] = s
+        return
+    st = _stage
+    if st["pool"] is None:
+        from concurrent.futures import ThreadPoolExecutor
+
+        st["pool"] = ThreadPoolExecutor(4)
+    step = (s.size + parts - 1) // parts
+    list(st["pool"].map(lambda i: np.copyto(d[i * step:(i + 1) * step], s[i * step:(i + 1) * step]),
+                        range(parts)))
+
+
 def _upload_pinned(t, arr: np.ndarray):
     st = _stage
     if st["buf"] is None or st["buf"].numel() < arr.nbytes:
@@ -79,18 +96,10 @@ def _upload_pinned(t, arr: np.ndarray):
             st["event"].synchronize()
         st["buf"] = t.empty(arr.nbytes, dtype=t.uint8, pin_memory=True)
         st["event"] = None
-    if st["pool"] is None:
-        from concurrent.futures import ThreadPoolExecutor
-
-        st["pool"] = ThreadPoolExecutor(4)
     if st["event"] is not None:
         st["event"].synchronize()  # the previous upload has left the staging buffer
     stage = st["buf"][: arr.nbytes].numpy().view(arr.dtype).reshape(arr.shape)
-    flat_src, flat_dst = arr.reshape(-1), stage.reshape(-1)
-    k = 4
-    step = (flat_src.size + k - 1) // k
-    list(st["pool"].map(lambda i: np.copyto(flat_dst[i * step:(i + 1) * step], flat_src[i * step:(i + 1) * step]),
-                        range(k)))
+    par_copy(stage, arr)
     out = t.empty(arr.shape, dtype=torch_dtype(arr.dtype), device="cuda")
     out.view(-1).view(t.uint8).copy_(st["buf"][: arr.nbytes], non_blocking=True)
     ev = t.cuda.Event()
