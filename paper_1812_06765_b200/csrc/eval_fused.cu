@@ -983,18 +983,26 @@ __global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArg
 // ring in shared memory (tools/sweep.py).  f32 default: 32 x 16 tiles of 320 threads with
 // the ring in shared memory (96 registers, 2 CTAs = 20 warps per SM, ring overhead 1.2);
 // 32 x 12 / 256 threads keeps the ring in registers (128 registers, 16 warps per SM) and
-// wins when its CTA count fills the waves better; the f64 march uses 32 x 20.
+// wins when its CTA count fills the waves better.  f64 uses one slot per thread (32 x 16
+// tiles of 640 threads or 32 x 12 of 512, one CTA per SM): its march state per slot is
+// twice as large, and the two-slot 32 x 20 shape (variant 0) spills 1.3 KB per thread
+// (942 us vs 638 us at 256^3).
 using V0 = Cfg<20, 256, 2>;
 using V1 = Cfg<12, 256, 2>;
 using V2 = Cfg<16, 320, 2, true>;
 using V3 = Cfg<18, 352, 2, true>;
-constexpr int kNumVariants = 4;
+// f64 shapes: one slot per thread (a slot's f64 march state needs about twice the registers)
+using V4 = Cfg<12, 512, 1, true>;
+using V5 = Cfg<16, 640, 1, true>;
+constexpr int kNumVariants = 6;
 
 void fused_variant_geom(int v, int* ty, int* nt) {
     switch (v) {
         case 1: *ty = V1::TY; *nt = V1::NT; return;
         case 2: *ty = V2::TY; *nt = V2::NT; return;
         case 3: *ty = V3::TY; *nt = V3::NT; return;
+        case 4: *ty = V4::TY; *nt = V4::NT; return;
+        case 5: *ty = V5::TY; *nt = V5::NT; return;
         default: *ty = V0::TY; *nt = V0::NT; return;
     }
 }
@@ -1007,6 +1015,8 @@ size_t fused_smem(int v, int wx, int wy) {
         case 1: return smem_bytes_cfg<T, V1>(wx, wy);
         case 2: return smem_bytes_cfg<T, V2>(wx, wy);
         case 3: return smem_bytes_cfg<T, V3>(wx, wy);
+        case 4: return smem_bytes_cfg<T, V4>(wx, wy);
+        case 5: return smem_bytes_cfg<T, V5>(wx, wy);
         default: return smem_bytes_cfg<T, V0>(wx, wy);
     }
 }
@@ -1070,8 +1080,11 @@ int fused_prepare<float>(int v, size_t smem) {
 
 template <>
 int fused_prepare<double>(int v, size_t smem) {
-    (void)v;
-    return prep<double, V0>(smem);  // one f64 variant
+    switch (v) {
+        case 4: return prep<double, V4>(smem);
+        case 5: return prep<double, V5>(smem);
+        default: return prep<double, V0>(smem);
+    }
 }
 
 template <typename T>
@@ -1089,7 +1102,11 @@ void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
 
 template <>
 void launch_variant<double>(const FusedArgs<double>& a, cudaStream_t s) {
-    launch<double, V0>(a, s);
+    switch (a.fp.variant) {
+        case 4: launch<double, V4>(a, s); return;
+        case 5: launch<double, V5>(a, s); return;
+        default: launch<double, V0>(a, s); return;
+    }
 }
 
 template <typename T>

@@ -159,13 +159,16 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     // threads with the derivative ring in shared memory take 1.16x the time of 32 x 12
     // tiles of 256 threads per plane for 1.33x the voxels).  Every
     // chunking must keep each def node covered by at most kCover chunks (k_post's sum).
-    static const int kMinBlocks[] = {2, 2, 2, 2};
-    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5};
+    static const int kMinBlocks[] = {2, 2, 2, 2, 1, 1};
+    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5, 1.0, 1.14};  // f64 (4, 5) relative to 4
     std::vector<int> cand;
-    if (sizeof(T) == 8) {
-        cand = {0};  // one f64 variant
-    } else if (const char* env = std::getenv("NGF_FUSED_VARIANT")) {
-        cand = {std::atoi(env) % fused_variant_count()};
+    const char* env = std::getenv("NGF_FUSED_VARIANT");
+    if (sizeof(T) == 8) {  // f64 shapes: 0, 4, 5
+        const int v = env ? std::atoi(env) : -1;
+        cand = (v == 0 || v == 4 || v == 5) ? std::vector<int>{v} : std::vector<int>{4, 5};
+    } else if (env) {
+        const int v = std::atoi(env) % 4;  // f32 shapes: 0 .. 3
+        cand = {v};
     } else {
         cand = {1, 2};
     }

@@ -209,18 +209,21 @@ def test_packed_march_matches_scalar_march(monkeypatch, dims, spacing, ratio):
     assert np.max(np.abs(out[0][1] - out[1][1])) <= 1e-5 * np.max(np.abs(out[0][1]))
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("variant,prec", [("0", "f32"), ("1", "f32"), ("2", "f32"), ("3", "f32"),
+                                          ("0", "f64"), ("4", "f64"), ("5", "f64")])
 @pytest.mark.parametrize("dims,ratio", [((40, 40, 40), 1), ((70, 45, 33), 4)])
-def test_every_kernel_variant_within_tolerance(monkeypatch, variant, dims, ratio):
+def test_every_kernel_variant_within_tolerance(monkeypatch, variant, prec, dims, ratio):
     """Each tile/occupancy variant of the fused march (forced with NGF_FUSED_VARIANT),
     incl. ratio 1 on non-unit spacing where the index map can advance by 2 (widest windows)."""
     monkeypatch.setenv("NGF_FUSED_VARIANT", variant)
     gi = ngf.Grid3(dims, (1.0, 1.1, 0.9), (-3.0, 2.0, 1.0))
     gd = ngf.deformation_grid_for(gi, ratio)
-    R = ngf.smooth_random_volume(gi, seed=5).values.astype(np.float32)
-    T = ngf.smooth_random_volume(gi, seed=6).values.astype(np.float32)
-    y = ngf.smooth_random_field(gd, seed=7, amplitude_mm=2.5).field.astype(np.float32)
+    dt = np.float32 if prec == "f32" else np.float64
+    R = ngf.smooth_random_volume(gi, seed=5).values.astype(dt)
+    T = ngf.smooth_random_volume(gi, seed=6).values.astype(dt)
+    y = ngf.smooth_random_field(gd, seed=7, amplitude_mm=2.5).field.astype(dt)
     J_ref, g_ref = O.Objective(T, R, _og(gd), _og(gi))(y.ravel())
     J, g = _device_obj(T, R, gd, gi)(y.ravel())
-    assert abs(J - J_ref) <= TOL_J * abs(J_ref), (J, J_ref)
-    assert _rel(g, g_ref) <= TOL_G
+    tol_J, tol_G = (TOL_J, TOL_G) if prec == "f32" else (1e-10, 1e-10)
+    assert abs(J - J_ref) <= tol_J * abs(J_ref), (J, J_ref)
+    assert _rel(g, g_ref) <= tol_G
