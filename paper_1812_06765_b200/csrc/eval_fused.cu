@@ -517,10 +517,28 @@ template <typename T, typename C>
 __device__ __forceinline__ void slot_geom(const FusedArgs<T>& a, const CtaGeo& g, int s, int& Pout, int& P2out,
                                           unsigned& ij, unsigned& flags) {
     const T hx2 = (T)0.5 * a.ihx, hy2 = (T)0.5 * a.ihy;
-    const int P = threadIdx.x + s * C::NT;
-    const bool ok = P < C::E1;
-    const int Pc = ok ? P : C::E1;
-    const int ex = Pc % C::E1X, ey = Pc / C::E1X;
+    // slot q -> E1 position: the tile interior first, row by row (each warp's lanes cover
+    // one 32-wide interior row, so (B), which only runs on the interior, is warp-uniform),
+    // then the ring (top row, bottom row, left/right columns), then padding
+    const int q = threadIdx.x + s * C::NT;
+    constexpr int NI = C::TX * C::TY;
+    const bool ok = q < C::E1;
+    int ex = 0, ey = 0;
+    if (q < NI) {
+        ex = q % C::TX + 1;
+        ey = q / C::TX + 1;
+    } else if (q < NI + C::E1X) {
+        ex = q - NI;
+    } else if (q < NI + 2 * C::E1X) {
+        ex = q - NI - C::E1X;
+        ey = C::E1Y - 1;
+    } else if (ok) {
+        const int rr = q - NI - 2 * C::E1X;
+        ey = 1 + rr / 2;
+        ex = (rr & 1) ? C::E1X - 1 : 0;
+    }
+    const int Pc = ok ? ey * C::E1X + ex : C::E1;
+    if (!ok) ex = ey = 0;
     const int i = g.x0 - 1 + ex, jj = g.y0 - 1 + ey;
     const bool vol = ok && i >= 0 && i < a.nx && jj >= 0 && jj < a.ny;
     const bool e0 = vol && ex >= 1 && ex <= C::TX && ey >= 1 && ey <= C::TY;
