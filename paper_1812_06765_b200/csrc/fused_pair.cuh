@@ -1,5 +1,5 @@
-// Two-slot packed march (f32 variants with two slots per thread; opt-in with
-// NGF_FUSED_PACKED=1), included by eval_fused.cu.  Same algorithm and shared-memory
+// Two-slot packed march (f32, the 32 x 12 / 256-thread shape; opt-in with
+// NGF_FUSED_PACKED=1 NGF_FUSED_VARIANT=1), included by eval_fused.cu.  Same algorithm and shared-memory
 // layout as fused_step; the two E1 positions a thread owns are carried as the halves of
 // float2 registers, so the f32 arithmetic of both issues as one FADD2 / FMUL2 / FFMA2
 // (sm_100).  The forward terms (W, yhat, the NGF ratio, D) equal the scalar march bit for

@@ -1,0 +1,8 @@
+// March kernels of variant 3 (see fused_cfg.cuh), one translation unit per variant so
+// the variants compile in parallel.
+#include "fused_march.cuh"
+
+namespace ngf {
+template int march_prepare<float, V3>(size_t);
+template void march_launch<float, V3>(const FusedArgs<float>&, cudaStream_t);
+}  // namespace ngf

@@ -195,6 +195,7 @@ def test_packed_march_matches_scalar_march(monkeypatch, dims, spacing, ratio):
     T = ngf.smooth_random_volume(gi, seed=8).values.astype(np.float32)
     y = ngf.smooth_random_field(gd, seed=9, amplitude_mm=2.0).field.astype(np.float32)
     x = torch.from_numpy(y.ravel().copy()).cuda()
+    monkeypatch.setenv("NGF_FUSED_VARIANT", "1")  # the shape the packed march is built for
     out = []
     for packed in (False, True):
         if packed:
