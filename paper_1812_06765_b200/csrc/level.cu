@@ -153,8 +153,9 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     // every tile column is cut into nb chunks of B planes followed by the remainder in
     // m near-equal smaller chunks; CTAs are numbered chunk-major, so all columns' big
     // chunks are dispatched first and the small ones fill the last wave (longest
-    // processing time first).  A chunk of c planes costs (c + 10) x plane cost: ~10 planes
-    // of per-CTA fixed work (tables, ring planes, pipeline fill), and a plane cost
+    // processing time first).  A chunk of c planes costs (c + 14) x plane cost: ~14 planes
+    // of per-CTA fixed work (tables, ring planes, pipeline fill; fitted with
+    // NGF_CHUNK_OVERHEAD sweeps at 256^3 .. 512^3), and a plane cost
     // relative to variant 1 (tools/sweep.py at 128^3 .. 512^3: 32 x 16 tiles of 320
     // threads with the derivative ring in shared memory take 1.16x the time of 32 x 12
     // tiles of 256 threads per plane for 1.33x the voxels).  Every
@@ -173,6 +174,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         cand = {1, 2};
     }
     const int nzs = zhi - zlo;
+    const double ovh = std::getenv("NGF_CHUNK_OVERHEAD") ? std::atof(std::getenv("NGF_CHUNK_OVERHEAD")) : 14.0;
     const int forced_cz = std::getenv("NGF_FUSED_CZ") ? std::atoi(std::getenv("NGF_FUSED_CZ")) : 0;
     struct Choice {
         double cost;
@@ -192,7 +194,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         const int64_t cols = (int64_t)ntx * nty, slots = (int64_t)kSMs * kMinBlocks[v];
         auto add = [&](std::vector<int> sizes) {
             std::vector<std::pair<int64_t, double>> cls;
-            for (int s : sizes) cls.push_back({cols, (s + 10) * kPlaneCost[v]});
+            for (int s : sizes) cls.push_back({cols, (s + ovh) * kPlaneCost[v]});
             choices.push_back({list_schedule(cls, slots), v, std::move(sizes)});
         };
         for (int B = std::min(nzs, kCzMax); B >= 1; --B) {
