@@ -126,13 +126,13 @@ static double list_schedule(const std::vector<std::pair<int64_t, double>>& class
 }
 
 static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, int nd,
-                        std::vector<int32_t>& cov) {
+                        std::vector<int32_t>& cov, int limit = kCover) {
     cov.assign((size_t)nd * kCover * 2, -1);
     for (int d = 0; d < nd; ++d) {
         int k = 0;
         for (int t = 0; t < (int)lo.size(); ++t) {
             if (d >= lo[t] && d <= hi[t]) {
-                if (k >= kCover) return false;
+                if (k >= limit) return false;
                 cov[((size_t)d * kCover + k) * 2] = t;
                 cov[((size_t)d * kCover + k) * 2 + 1] = d - lo[t];
                 ++k;
@@ -229,16 +229,22 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
                      [](const Choice& x, const Choice& y) { return x.cost < y.cost; });
     std::vector<int> bounds;
     int variant = -1;
-    for (const Choice& ch : choices) {  // cheapest valid chunking
-        std::vector<int> bd(1, zlo), a, b;
-        for (int s : ch.sizes) bd.push_back(bd.back() + s);
-        chunk_windows(p->h_i0[2], nz, ndz, bd, a, b);
-        std::vector<int32_t> cov;
-        if (build_cover(a, b, ndz, cov)) {
-            bounds = bd;
-            variant = ch.variant;
-            break;
+    // cheapest valid chunking; first among those whose def planes are covered by at most 4
+    // chunks (k_post's unrolled partial sum -- more covers take its serial loop, which at
+    // small sizes costs more than the march gains from the extra chunks)
+    for (const int limit : {4, kCover}) {
+        for (const Choice& ch : choices) {
+            std::vector<int> bd(1, zlo), a, b;
+            for (int s : ch.sizes) bd.push_back(bd.back() + s);
+            chunk_windows(p->h_i0[2], nz, ndz, bd, a, b);
+            std::vector<int32_t> cov;
+            if (build_cover(a, b, ndz, cov, limit)) {
+                bounds = bd;
+                variant = ch.variant;
+                break;
+            }
         }
+        if (variant >= 0) break;
     }
     if (variant < 0) return NGF_EARG;
     fp.variant = variant;
