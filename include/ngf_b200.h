@@ -182,6 +182,33 @@ int ngf_lbfgs_two_loop(int dtype, const void* const* S, const void* const* Y, co
                        double gamma, int m, const void* g, void* d, int64_t n, double* slope_dev,
                        void* stream);
 
+/* ---------------------------------------------------------------- native L-BFGS driver
+ * lbfgs_minimize (lbfgs.py:94-181) for a level's device objective: the reference's
+ * decisions (two-loop direction, steepest-descent safeguard, Armijo backtracking with
+ * forward expansion at t == 1, curvature-filtered history with ageing, relative stopping
+ * tests after min_iterations) with one pinned host round trip per scalar read.          */
+typedef struct {
+    int memory, max_iterations, max_ls_steps, min_iterations;
+    double c1, initial_step, step_shrink;       /* LbfgsConfig */
+    double tol_J, tol_grad, tol_step;           /* StoppingRules */
+} ngf_lbfgs_cfg_t;
+#define NGF_STOP_OBJECTIVE 0
+#define NGF_STOP_GRADIENT 1
+#define NGF_STOP_STEP 2
+#define NGF_STOP_MAX_ITER 3
+#define NGF_STOP_LINE_SEARCH 4
+#define NGF_STOP_STATIONARY 5
+typedef struct {
+    int iterations, evaluations, stop, line_search_failed, rows;
+} ngf_lbfgs_result_t;
+/* Minimise the level objective from the device vector x (n values of dtype, updated in
+ * place with the final iterate); exact selects the bit-exact evaluation.  rec[4 * it] =
+ * (J, max|g|, step, line-search evaluations) per iteration (room for max_iterations);
+ * rows[3 * k] = (J, D, S) per evaluation, up to max_rows (res->rows counts them all). */
+int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, void* x, int64_t n,
+                        const ngf_lbfgs_cfg_t* cfg, ngf_lbfgs_result_t* res, double* rec, double* rows,
+                        int max_rows, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -47,6 +47,7 @@ _PROTOS = {
     "ngf_apply_Pt": (_i, [_vp, _i, _vp, _vp, _vp]),
     "ngf_apply_Pt_variant": (_i, [_vp, _i, _i, _vp, _vp, _vp]),
     "ngf_sample_field": (_i, [_vp, _i, _vp, _vp, ctypes.c_int64, _vp, _vp]),
+    "ngf_lbfgs_run_level": (_i, [_vp, _i, _i, _vp, ctypes.c_int64, _vp, _vp, _vp, _vp, _i, _vp]),
     "ngf_warp": (_i, [_pg, _i, _vp, _vp, _i64, _vp, _vp, _vp]),
     "ngf_warp_jt": (_i, [_pg, _i, _vp, _vp, _vp, _i64, _vp, _vp]),
     "ngf_gradient": (_i, [_pg, _i, _vp, _vp, _vp]),

@@ -64,6 +64,32 @@ __device__ __forceinline__ void block_sum(double (&v)[K], double (&red)[K][kRedT
     }
 }
 
+// Final reduction of the block partials by warp 0 of the last block: NS sums (k < NS)
+// and a max (k == NS), lane-strided over the blocks in order, then a butterfly (fixed order).
+template <int NS>
+__device__ __forceinline__ void final_reduce(const double* parts, int nblocks, double* out) {
+    if (threadIdx.x >= 32) return;
+    double acc[NS], m = 0.0;
+#pragma unroll
+    for (int k = 0; k < NS; ++k) acc[k] = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 32) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) acc[k] += __ldcg(parts + b * kNStat + k);
+        m = fmax(m, __ldcg(parts + b * kNStat + NS));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) acc[k] += __shfl_xor_sync(0xffffffffu, acc[k], o);
+        m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    }
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int k = 0; k < NS; ++k) out[k] = acc[k];
+        out[NS] = m;
+    }
+}
+
 // stats: [0] g.d  [1] s.y  [2] s.s  [3] y.y  [4] max|g|
 template <typename T>
 __global__ void __launch_bounds__(kRedThreads) k_stats(const T* __restrict__ g, const T* __restrict__ d,
@@ -106,15 +132,10 @@ __global__ void __launch_bounds__(kRedThreads) k_stats(const T* __restrict__ g, 
         last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
         __threadfence();
-        double acc[kNStat] = {0.0, 0.0, 0.0, 0.0, 0.0};
-        for (int b = 0; b < (int)gridDim.x; ++b) {
-            for (int k = 0; k < 4; ++k) acc[k] += ((volatile double*)parts)[b * kNStat + k];
-            acc[4] = fmax(acc[4], ((volatile double*)parts)[b * kNStat + 4]);
-        }
-        for (int k = 0; k < kNStat; ++k) out[k] = acc[k];
-        *counter = 0u;
+        final_reduce<4>(parts, gridDim.x, out);
+        if (threadIdx.x == 0) *counter = 0u;
     }
 }
 
@@ -172,15 +193,10 @@ __global__ void __launch_bounds__(kRedThreads) k_pair(const T* __restrict__ xn, 
         last = (t == gridDim.x - 1);
     }
     __syncthreads();
-    if (last && threadIdx.x == 0) {
+    if (last) {
         __threadfence();
-        double acc[4] = {0.0, 0.0, 0.0, 0.0};
-        for (int b = 0; b < (int)gridDim.x; ++b) {
-            for (int k = 0; k < 3; ++k) acc[k] += ((volatile double*)parts)[b * kNStat + k];
-            acc[3] = fmax(acc[3], ((volatile double*)parts)[b * kNStat + 3]);
-        }
-        for (int k = 0; k < 4; ++k) out[k] = acc[k];
-        *counter = 0u;
+        final_reduce<3>(parts, gridDim.x, out);
+        if (threadIdx.x == 0) *counter = 0u;
     }
 }
 
@@ -214,8 +230,17 @@ __device__ __forceinline__ double grid_dot(cg::grid_group& grid, double v, doubl
         parts[buf * kRedBlocks + blockIdx.x] = s;
     }
     grid.sync();
-    double tot = 0.0;
-    for (int b = 0; b < (int)gridDim.x; ++b) tot += ((volatile double*)parts)[buf * kRedBlocks + b];
+    // one warp per block sums the block partials: lane-strided in block order, then a
+    // butterfly -- the same fixed order in every block, so all blocks agree bit for bit
+    if (threadIdx.x < 32) {
+        double t = 0.0;
+        for (int b = threadIdx.x; b < (int)gridDim.x; b += 32) t += __ldcg(parts + buf * kRedBlocks + b);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) red[0] = t;
+    }
+    __syncthreads();
+    const double tot = red[0];
     __syncthreads();  // red reused by the next call
     return tot;
 }

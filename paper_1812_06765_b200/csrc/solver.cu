@@ -1,0 +1,269 @@
+// The L-BFGS driver of one level in native code (lbfgs.py:94-181), for the device
+// objective: the same decisions as the Python driver (paper_1812_06765_b200/lbfgs.py) --
+// two-loop direction, steepest-descent safeguard, Armijo backtracking with forward
+// expansion at t == 1, curvature-filtered history with ageing, the three relative stopping
+// tests -- with the scalars it branches on read through one pinned buffer per host round
+// trip.  Used by `register` for LevelObjective levels; any other callable runs the Python
+// driver.
+
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ngf {
+
+namespace {
+
+struct PinnedScalars {
+    double* host = nullptr;
+    ~PinnedScalars() {
+        if (host) cudaFreeHost(host);
+    }
+};
+
+thread_local PinnedScalars t_pin;
+
+int read_scalars(const double* dev_src, int k, double* out, cudaStream_t s) {
+    if (!t_pin.host && cudaMallocHost((void**)&t_pin.host, 16 * sizeof(double)) != cudaSuccess)
+        return NGF_ENOMEM;
+    NGF_CUDA(cudaMemcpyAsync(t_pin.host, dev_src, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NGF_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(out, t_pin.host, k * sizeof(double));
+    return 0;
+}
+
+struct Pair {
+    void* s;
+    void* y;
+    double sy, yy;
+};
+
+}  // namespace
+}  // namespace ngf
+
+using namespace ngf;
+
+extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, void* x_io, int64_t n,
+                                   const ngf_lbfgs_cfg_t* cfg, ngf_lbfgs_result_t* res, double* rec,
+                                   double* rows, int max_rows, void* stream) {
+    if (!level || !x_io || !cfg || !res || n <= 0 || (dtype != NGF_F32 && dtype != NGF_F64) ||
+        cfg->memory < 1 || cfg->max_iterations < 0 || max_rows < 1)
+        return NGF_EARG;
+    cudaStream_t s = as_stream(stream);
+    const size_t vb = (size_t)n * (dtype == NGF_F32 ? 4 : 8);
+    std::memset(res, 0, sizeof(*res));
+
+    // workspace: g, d, xn, gn, xt, gt, a copy of x, the pair pool, scalars
+    std::vector<void*> owned;
+    auto alloc = [&](size_t bytes) -> void* {
+        void* p = nullptr;
+        if (dev_alloc(&p, bytes)) return nullptr;
+        owned.push_back(p);
+        return p;
+    };
+    void *x = alloc(vb), *g = alloc(vb), *d = alloc(vb), *xn = alloc(vb), *gn = alloc(vb), *xt = alloc(vb),
+         *gt = alloc(vb);
+    double* scal = (double*)alloc(4 * sizeof(double));   // J, D, S, slope
+    double* stats = (double*)alloc(5 * sizeof(double));  // see ngf_vec_stats / ngf_lbfgs_pair
+    std::vector<Pair> free_pairs;
+    int rc = (x && g && d && xn && gn && xt && gt && scal && stats) ? 0 : NGF_ENOMEM;
+    auto cleanup = [&]() {
+        cudaStreamSynchronize(s);
+        for (void* p : owned) dev_free(p);
+    };
+    if (rc) {
+        cleanup();
+        return rc;
+    }
+    cudaMemcpyAsync(x, x_io, vb, cudaMemcpyDeviceToDevice, s);
+
+    int nrows = 0;
+    auto row = [&](const double* v) {
+        if (nrows < max_rows) {
+            rows[3 * nrows] = v[0];
+            rows[3 * nrows + 1] = v[1];
+            rows[3 * nrows + 2] = v[2];
+        }
+        ++nrows;
+    };
+    double sc[5];
+#define RUN(call)               \
+    do {                        \
+        rc = (call);            \
+        if (rc) goto done;      \
+    } while (0)
+
+    {
+        int evals = 0;
+        RUN(ngf_level_eval(level, x, g, scal, exact, s));
+        ++evals;
+        RUN(read_scalars(scal, 3, sc, s));
+        double J = sc[0];
+        row(sc);
+        RUN(ngf_vec_stats(dtype, g, nullptr, x, nullptr, n, stats, s));
+        double st[5];
+        RUN(read_scalars(stats, 5, st, s));
+        const double g0_inf = st[4];
+        if (g0_inf <= 0.0) {
+            res->stop = NGF_STOP_STATIONARY;  // (the reference reports no evaluations here)
+            goto done;
+        }
+        std::vector<Pair> history;
+        const double x_scale = std::max(std::sqrt(st[2]), 1.0);
+        int rejected = 0;
+        auto two_loop = [&]() {
+            const int m = (int)history.size();
+            std::vector<const void*> S(std::max(m, 1)), Y(std::max(m, 1));
+            std::vector<double> rho(std::max(m, 1));
+            for (int k = 0; k < m; ++k) {
+                S[k] = history[k].s;
+                Y[k] = history[k].y;
+                rho[k] = 1.0 / history[k].sy;
+            }
+            const double gamma = m ? history[m - 1].sy / history[m - 1].yy : 1.0;
+            return ngf_lbfgs_two_loop(dtype, S.data(), Y.data(), rho.data(), gamma, m, g, d, n, scal + 3, s);
+        };
+        for (int it = 0; it < cfg->max_iterations; ++it) {
+            // direction and (optimistically) the first trial point, one host round trip
+            RUN(two_loop());
+            double t = cfg->initial_step;
+            RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
+            RUN(ngf_level_eval(level, xn, gn, scal, exact, s));
+            ++evals;
+            double v[4];
+            RUN(read_scalars(scal, 4, v, s));
+            double Jn = v[0], slope = v[3];
+            int ls_evals = 1;
+            if (slope >= 0) {  // safeguard: steepest descent (lbfgs.py:113-116)
+                --evals;       // the optimistic trial above is discarded
+                for (const Pair& p : history) free_pairs.push_back(p);
+                history.clear();
+                RUN(two_loop());
+                RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
+                RUN(ngf_level_eval(level, xn, gn, scal, exact, s));
+                ++evals;
+                RUN(read_scalars(scal, 4, v, s));
+                Jn = v[0];
+                slope = v[3];
+            }
+            row(v);
+            bool accepted = false;
+            while (true) {
+                if (std::isfinite(Jn) && Jn <= J + cfg->c1 * t * slope) {
+                    accepted = true;
+                    break;
+                }
+                if (ls_evals >= cfg->max_ls_steps) break;
+                t *= cfg->step_shrink;
+                RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
+                RUN(ngf_level_eval(level, xn, gn, scal, exact, s));
+                ++evals;
+                RUN(read_scalars(scal, 3, v, s));
+                Jn = v[0];
+                row(v);
+                ++ls_evals;
+            }
+            if (!accepted) {
+                res->stop = NGF_STOP_LINE_SEARCH;
+                res->line_search_failed = 1;
+                res->evaluations = evals;
+                goto done;
+            }
+            if (t == cfg->initial_step) {
+                // forward expansion while Armijo holds and J decreases (lbfgs.py:133-143)
+                while (ls_evals < cfg->max_ls_steps) {
+                    const double t_try = t / cfg->step_shrink;
+                    RUN(ngf_vec_axpy_step(dtype, x, t_try, d, xt, n, s));
+                    RUN(ngf_level_eval(level, xt, gt, scal, exact, s));
+                    ++evals;
+                    RUN(read_scalars(scal, 3, v, s));
+                    const double Jt = v[0];
+                    row(v);
+                    ++ls_evals;
+                    if (std::isfinite(Jt) && Jt <= J + cfg->c1 * t_try * slope && Jt < Jn) {
+                        t = t_try;
+                        Jn = Jt;
+                        std::swap(xn, xt);
+                        std::swap(gn, gt);
+                    } else {
+                        break;
+                    }
+                }
+            }
+            // history pair and stopping statistics in one pass (lbfgs.py:145-164)
+            Pair pair;
+            if (!free_pairs.empty()) {
+                pair = free_pairs.back();
+                free_pairs.pop_back();
+            } else {
+                pair.s = alloc(vb);
+                pair.y = alloc(vb);
+                if (!pair.s || !pair.y) {
+                    rc = NGF_ENOMEM;
+                    goto done;
+                }
+            }
+            RUN(ngf_lbfgs_pair(dtype, xn, x, gn, g, pair.s, pair.y, n, stats, s));
+            RUN(read_scalars(stats, 4, st, s));
+            const double sy = st[0], ss = st[1], yy = st[2], g_inf = st[3];
+            pair.sy = sy;
+            pair.yy = yy;
+            if (sy > 1e-10 * std::sqrt(ss) * std::sqrt(yy)) {
+                history.push_back(pair);
+                if ((int)history.size() > cfg->memory) {
+                    free_pairs.push_back(history.front());
+                    history.erase(history.begin());
+                }
+                rejected = 0;
+            } else {
+                free_pairs.push_back(pair);
+                ++rejected;
+                if (!history.empty()) {
+                    free_pairs.push_back(history.front());
+                    history.erase(history.begin());
+                }
+                if (rejected >= cfg->memory) {
+                    for (const Pair& p : history) free_pairs.push_back(p);
+                    history.clear();
+                }
+            }
+            const double step_norm = std::sqrt(ss);
+            const double J_prev = J;
+            std::swap(x, xn);
+            std::swap(g, gn);
+            J = Jn;
+            if (rec) {
+                rec[4 * it] = J;
+                rec[4 * it + 1] = g_inf;
+                rec[4 * it + 2] = t;
+                rec[4 * it + 3] = ls_evals;
+            }
+            res->iterations = it + 1;
+            if (it + 1 >= cfg->min_iterations) {
+                if (std::fabs(J_prev - J) <= cfg->tol_J * std::max(std::fabs(J_prev), 1e-30)) {
+                    res->stop = NGF_STOP_OBJECTIVE;
+                    break;
+                }
+                if (g_inf <= cfg->tol_grad * g0_inf) {
+                    res->stop = NGF_STOP_GRADIENT;
+                    break;
+                }
+                if (step_norm <= cfg->tol_step * x_scale) {
+                    res->stop = NGF_STOP_STEP;
+                    break;
+                }
+            }
+            if (it + 1 == cfg->max_iterations) res->stop = NGF_STOP_MAX_ITER;
+        }
+        if (cfg->max_iterations == 0) res->stop = NGF_STOP_MAX_ITER;
+        res->evaluations = evals;
+    }
+done:
+#undef RUN
+    res->rows = nrows;
+    if (!rc) cudaMemcpyAsync(x_io, x, vb, cudaMemcpyDeviceToDevice, s);  // the final (accepted) x
+    cleanup();
+    return rc;
+}

@@ -13,6 +13,7 @@ from __future__ import annotations
 
 import ctypes
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -283,12 +284,59 @@ class _Solver:
         return x, trace
 
 
+class _NativeCfg(ctypes.Structure):
+    _fields_ = [("memory", ctypes.c_int), ("max_iterations", ctypes.c_int), ("max_ls_steps", ctypes.c_int),
+                ("min_iterations", ctypes.c_int), ("c1", ctypes.c_double), ("initial_step", ctypes.c_double),
+                ("step_shrink", ctypes.c_double), ("tol_J", ctypes.c_double), ("tol_grad", ctypes.c_double),
+                ("tol_step", ctypes.c_double)]
+
+
+class _NativeRes(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int), ("evaluations", ctypes.c_int), ("stop", ctypes.c_int),
+                ("line_search_failed", ctypes.c_int), ("rows", ctypes.c_int)]
+
+
+_STOP_REASONS = ("objective change below tolerance", "gradient below tolerance", "step below tolerance",
+                 "max iterations", "line search failed", "stationary start")
+
+
+def _native_minimize(f, x0, cfg: LbfgsConfig, stop: StoppingRules):
+    """The driver loop in native code (ngf_lbfgs_run_level) for a level objective: the
+    same decisions as _Solver.run, without a Python round trip per vector operation."""
+    np_in = not dev.is_tensor(x0)
+    shape = tuple(x0.shape)
+    x = dev.to_device(x0).reshape(-1).clone()
+    n = x.numel()
+    c = _NativeCfg(cfg.memory, cfg.max_iterations, cfg.max_ls_steps, stop.min_iterations, cfg.c1,
+                   cfg.initial_step, cfg.step_shrink, stop.tol_J, stop.tol_grad, stop.tol_step)
+    res = _NativeRes()
+    rec = (ctypes.c_double * (4 * max(cfg.max_iterations, 1)))()
+    max_rows = 2 + cfg.max_iterations * (cfg.max_ls_steps + 1)
+    rows = (ctypes.c_double * (3 * max_rows))()
+    check(lib().ngf_lbfgs_run_level(f.level.handle, dtype_code(x.dtype), 1 if f.exact else 0, dev.ptr(x), n,
+                                    ctypes.byref(c), ctypes.byref(res), rec, rows, max_rows, dev.stream()),
+          "ngf_lbfgs_run_level")
+    trace = OptimizeTrace()
+    trace.records = [IterationRecord(it, rec[4 * it], rec[4 * it + 1], rec[4 * it + 2], int(rec[4 * it + 3]))
+                     for it in range(res.iterations)]
+    trace.stop_reason = _STOP_REASONS[res.stop]
+    trace.line_search_failed = bool(res.line_search_failed)
+    trace.evaluations = res.evaluations
+    trace.J_rows = [(rows[3 * k], rows[3 * k + 1], rows[3 * k + 2]) for k in range(min(res.rows, max_rows))]
+    f.evals += res.evaluations
+    x = x.reshape(shape)
+    return (dev.to_host(x) if np_in else x), trace
+
+
 def lbfgs_minimize(f, x0, cfg: LbfgsConfig = LbfgsConfig(), stop: StoppingRules = StoppingRules()):
     """Minimize f(x) -> (J, grad); returns (best x, OptimizeTrace) (lbfgs.py:94-181).
 
-    `f` may be a LevelObjective (device-resident evaluation) or any numpy callable.
+    `f` may be a LevelObjective (device-resident evaluation; its driver loop runs in
+    native code, NGF_PY_LBFGS=1 selects the Python loop) or any numpy callable.
     numpy x0 -> numpy x; a CUDA tensor x0 -> CUDA tensor x.
     """
+    if hasattr(f, "level") and hasattr(f, "exact") and not os.environ.get("NGF_PY_LBFGS"):
+        return _native_minimize(f, x0, cfg, stop)
     solver = _Solver(f, x0, cfg, stop)
     x, trace = solver.run()
     trace.J_rows = solver.trace_rows

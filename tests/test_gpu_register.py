@@ -115,3 +115,33 @@ def test_register_rejects_mismatched_grids():
     T = ngf.smooth_random_volume(ngf.Grid3((9, 8, 8), (1, 1, 1), (0, 0, 0)), seed=2)
     with pytest.raises(ngf.GridError):
         ngf.register(R, T)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_native_driver_matches_python_driver(monkeypatch, exact):
+    """ngf_lbfgs_run_level (native loop) takes the Python driver's decisions: identical
+    iteration records, (J, D, S) rows, stop reason, evaluation count and final field."""
+    import torch
+
+    gi = ngf.Grid3((40, 36, 32), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    gd = ngf.deformation_grid_for(gi, 4)
+    R = ngf.smooth_random_volume(gi, seed=11).values.astype(np.float32)
+    T = ngf.smooth_random_volume(gi, seed=12).values.astype(np.float32)
+    x0 = ngf.make_identity(gd).field.astype(np.float32).ravel()
+    plan = ngf.build_gather_plan(gd, gi)
+    out = []
+    for py in (True, False):
+        if py:
+            monkeypatch.setenv("NGF_PY_LBFGS", "1")
+        else:
+            monkeypatch.delenv("NGF_PY_LBFGS", raising=False)
+        obj = ngf.LevelObjective.from_device(torch.from_numpy(T).cuda(), torch.from_numpy(R).cuda(), plan,
+                                             ngf.NgfParams(), 1.0, exact=exact)
+        x, tr = ngf.lbfgs_minimize(obj, x0.copy(), ngf.LbfgsConfig(max_iterations=25))
+        out.append((x, tr))
+    (xp, tp), (xn, tn) = out
+    assert tn.stop_reason == tp.stop_reason and tn.evaluations == tp.evaluations
+    assert [(r.J, r.grad_inf, r.step, r.ls_evals) for r in tn.records] == \
+           [(r.J, r.grad_inf, r.step, r.ls_evals) for r in tp.records]
+    assert tn.J_rows == tp.J_rows
+    assert np.array_equal(xn, xp)
