@@ -245,10 +245,41 @@ __device__ __forceinline__ double grid_dot(cg::grid_group& grid, double v, doubl
     return tot;
 }
 
-template <typename T>
-__global__ void __launch_bounds__(kRedThreads) k_two_loop(const TwoLoopArgs<T> a) {
-    cg::grid_group grid = cg::this_grid();
-    __shared__ double red[kRedThreads / 32];
+// one-block variant for short vectors: the same fixed-order sum within the block
+__device__ __forceinline__ double block_dot(double v, double* red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double t = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        if (threadIdx.x == 0) red[32] = t;
+    }
+    __syncthreads();
+    const double tot = red[32];
+    __syncthreads();
+    return tot;
+}
+
+// GRID: cooperative launch over kRedBlocks blocks (long vectors); else one block of
+// kSmallThreads threads (no grid synchronisation; vectors up to kSmallN values)
+constexpr int kSmallThreads = 1024;
+constexpr int64_t kSmallN = 1 << 16;
+
+template <typename T, bool GRID>
+__global__ void __launch_bounds__(GRID ? kRedThreads : kSmallThreads) k_two_loop(const TwoLoopArgs<T> a) {
+    __shared__ double red[33];
+    auto dot = [&](double v, int buf) {
+        if constexpr (GRID) {
+            cg::grid_group grid = cg::this_grid();
+            return grid_dot(grid, v, a.parts, buf, red);
+        } else {
+            (void)buf;
+            return block_dot(v, red);
+        }
+    };
     const int64_t i0 = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int64_t st = (int64_t)gridDim.x * blockDim.x;
     int buf = 0;
@@ -262,9 +293,9 @@ __global__ void __launch_bounds__(kRedThreads) k_two_loop(const TwoLoopArgs<T> a
     }
     // first loop, newest pair first: alpha = rho * (s . q); q -= dtype(alpha) * y
     for (int k = a.m - 1; k >= 0; --k) {
-        const double dot = grid_dot(grid, v, a.parts, buf, red);
+        const double dt = dot(v, buf);
         buf ^= 1;
-        alpha[k] = a.rho[k] * dot;
+        alpha[k] = a.rho[k] * dt;
         const T al = (T)alpha[k];
         v = 0.0;
         const bool last = (k == 0);
@@ -282,9 +313,9 @@ __global__ void __launch_bounds__(kRedThreads) k_two_loop(const TwoLoopArgs<T> a
     }
     // second loop, oldest pair first: beta = rho * (y . q); q += dtype(alpha - beta) * s
     for (int k = 0; k < a.m; ++k) {
-        const double dot = grid_dot(grid, v, a.parts, buf, red);
+        const double dt = dot(v, buf);
         buf ^= 1;
-        const double beta = a.rho[k] * dot;
+        const double beta = a.rho[k] * dt;
         const T c = (T)(alpha[k] - beta);
         v = 0.0;
         const bool last = (k == a.m - 1);
@@ -308,7 +339,7 @@ __global__ void __launch_bounds__(kRedThreads) k_two_loop(const TwoLoopArgs<T> a
             v += (double)a.g[i] * (double)q;
         }
     }
-    const double slope = grid_dot(grid, v, a.parts, buf, red);
+    const double slope = dot(v, buf);
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.slope = slope;
 }
 
@@ -331,9 +362,14 @@ int two_loop_impl(const void* const* S, const void* const* Y, const double* rho,
     a.n = n;
     a.parts = sc->parts;
     a.slope = slope;
+    if (n <= kSmallN) {
+        NGF_LAUNCH((k_two_loop<T, false>), 1, kSmallThreads, 0, s, a);
+        NGF_CHECK_LAUNCH();
+        return 0;
+    }
     void* args[] = {&a};
     g_launches.fetch_add(1, std::memory_order_relaxed);
-    NGF_CUDA(cudaLaunchCooperativeKernel((const void*)k_two_loop<T>, dim3(kRedBlocks), dim3(kRedThreads),
+    NGF_CUDA(cudaLaunchCooperativeKernel((const void*)k_two_loop<T, true>, dim3(kRedBlocks), dim3(kRedThreads),
                                          args, 0, s));
     return 0;
 }
