@@ -141,26 +141,29 @@ class LevelObjective:
         return J, D, S, (dev.to_host(g) if np_out else g)
 
     def _host_call(self, x: np.ndarray):
-        """numpy in / out through pinned staging buffers: one H2D of x, one evaluation,
-        one D2H of (grad, J, D, S), one stream sync."""
+        """numpy in / out through pinned buffers: one H2D of x, one evaluation, one D2H of
+        (grad, J, D, S), one stream sync."""
         t = dev.torch()
         n = x.size
         st = getattr(self, "_stage", None)
         if st is None or st[0].numel() != n or st[0].dtype != dev.torch_dtype(x.dtype):
             tdt = dev.torch_dtype(x.dtype)
             st = (t.empty(n, dtype=tdt, pin_memory=True), dev.empty((n,), tdt), dev.empty((n,), tdt),
-                  t.empty(n, dtype=tdt, pin_memory=True), dev.zeros((3,), "float64"),
-                  t.empty(3, dtype=t.float64, pin_memory=True))
+                  None, dev.zeros((3,), "float64"), t.empty(3, dtype=t.float64, pin_memory=True))
             self._stage = st
-        x_pin, x_dev, g_dev, g_pin, sc_dev, sc_pin = st
+        x_pin, x_dev, g_dev, _, sc_dev, sc_pin = st
         x_pin.numpy()[:] = x.reshape(-1)
         x_dev.copy_(x_pin, non_blocking=True)
         self.eval_device(x_dev, g_dev, sc_dev)
-        g_pin.copy_(g_dev, non_blocking=True)
+        # the gradient lands in a fresh page-locked buffer from torch's caching host
+        # allocator and is returned without a host copy; the caller owns it (the
+        # reference returns a new array per call), and it is recycled once released
+        g_out = t.empty(n, dtype=g_dev.dtype, pin_memory=True)
+        g_out.copy_(g_dev, non_blocking=True)
         sc_pin.copy_(sc_dev, non_blocking=True)
         t.cuda.current_stream().synchronize()
         J, D, S = (float(v) for v in sc_pin.numpy())
-        return J, D, S, g_pin.numpy().copy()
+        return J, D, S, g_out.numpy()
 
     def __call__(self, x):
         if dev.is_tensor(x):
