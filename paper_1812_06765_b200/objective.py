@@ -145,13 +145,13 @@ class LevelObjective:
         (grad, J, D, S), one stream sync."""
         t = dev.torch()
         n = x.size
+        tdt = dev.torch_dtype(x.dtype)
         st = getattr(self, "_stage", None)
-        if st is None or st[0].numel() != n or st[0].dtype != dev.torch_dtype(x.dtype):
-            tdt = dev.torch_dtype(x.dtype)
-            st = (t.empty(n, dtype=tdt, pin_memory=True), dev.empty((n,), tdt), dev.empty((n,), tdt),
-                  None, dev.zeros((3,), "float64"), t.empty(3, dtype=t.float64, pin_memory=True))
+        if st is None or st[0].numel() != n or st[0].dtype != tdt:
+            st = (dev.empty((n,), tdt), dev.empty((n,), tdt), dev.zeros((3,), "float64"),
+                  t.empty(3, dtype=t.float64, pin_memory=True), t.empty(n, dtype=tdt, pin_memory=True))
             self._stage = st
-        x_pin, x_dev, g_dev, _, sc_dev, sc_pin = st
+        x_dev, g_dev, sc_dev, sc_pin, x_pin = st
         x_pin.numpy()[:] = x.reshape(-1)
         x_dev.copy_(x_pin, non_blocking=True)
         self.eval_device(x_dev, g_dev, sc_dev)

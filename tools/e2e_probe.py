@@ -31,7 +31,8 @@ y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=2.0).field.astype(np.float3
 obj = ngf.LevelObjective.from_device(torch.from_numpy(T.values).cuda(), torch.from_numpy(R.values).cuda(),
                                      ngf.build_gather_plan(gd, R.grid), ngf.NgfParams(), 1.0)
 obj(y)
-x_pin, x_dev, g_dev, g_pin, sc_dev, sc_pin = obj._stage
+x_dev, g_dev, sc_dev, sc_pin, x_pin = obj._stage
+g_pin = torch.empty(y.size, dtype=torch.float32, pin_memory=True)
 print(f"full __call__          {t(lambda: obj(y)):.3f} ms")
 print(f"memcpy x -> pinned     {t(lambda: x_pin.numpy().__setitem__(slice(None), y)):.3f} ms")
 print(f"H2D 3 MB               {t(lambda: x_dev.copy_(x_pin, non_blocking=True)):.3f} ms")
@@ -39,3 +40,6 @@ print(f"eval (device)          {t(lambda: obj.eval_device(x_dev, g_dev, sc_dev))
 print(f"D2H 3 MB               {t(lambda: g_pin.copy_(g_dev, non_blocking=True)):.3f} ms")
 print(f"pinned -> new array    {t(lambda: g_pin.numpy().copy()):.3f} ms")
 print(f"scalars D2H + sync     {t(lambda: (sc_pin.copy_(sc_dev, non_blocking=True), torch.cuda.current_stream().synchronize())):.3f} ms")
+xs = torch.from_numpy(y)
+print(f"pageable H2D 3 MB      {t(lambda: x_dev.copy_(xs, non_blocking=False)):.3f} ms")
+print(f"pinned alloc+D2H 3 MB  {t(lambda: torch.empty(y.size, dtype=torch.float32, pin_memory=True).copy_(g_dev, non_blocking=True)):.3f} ms")
