@@ -145,3 +145,33 @@ def test_native_driver_matches_python_driver(monkeypatch, exact):
            [(r.J, r.grad_inf, r.step, r.ls_evals) for r in tp.records]
     assert tn.J_rows == tp.J_rows
     assert np.array_equal(xn, xp)
+
+
+def test_native_driver_edge_cases(monkeypatch):
+    """Stationary start (constant images at the identity: grad J = 0 exactly) and a zero
+    iteration budget give the same traces from the native and the Python drivers."""
+    import torch
+
+    gi = ngf.Grid3((24, 20, 16), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    gd = ngf.deformation_grid_for(gi, 4)
+    x0 = ngf.make_identity(gd).field.astype(np.float32).ravel()
+    plan = ngf.build_gather_plan(gd, gi)
+    flat = np.full(gi.shape, 100.0, dtype=np.float32)
+    cases = ((flat, flat, ngf.LbfgsConfig(), "stationary start"),
+             (ngf.smooth_random_volume(gi, seed=4).values.astype(np.float32),
+              ngf.smooth_random_volume(gi, seed=3).values.astype(np.float32), ngf.LbfgsConfig(max_iterations=0),
+              "max iterations"))
+    for T, R, cfg, reason in cases:
+        out = []
+        for py in (True, False):
+            if py:
+                monkeypatch.setenv("NGF_PY_LBFGS", "1")
+            else:
+                monkeypatch.delenv("NGF_PY_LBFGS", raising=False)
+            obj = ngf.LevelObjective.from_device(torch.from_numpy(T).cuda(), torch.from_numpy(R).cuda(), plan,
+                                                 ngf.NgfParams(), 1.0)
+            out.append(ngf.lbfgs_minimize(obj, x0.copy(), cfg))
+        (xp, tp), (xn, tn) = out
+        assert tn.stop_reason == tp.stop_reason == reason and tn.evaluations == tp.evaluations
+        assert tn.iterations == tp.iterations == 0 and tn.J_rows == tp.J_rows
+        assert np.array_equal(xn, xp) and np.array_equal(xn, x0)
