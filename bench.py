@@ -51,6 +51,9 @@ def parse():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-register", action="store_true", help="skip the full-registration leg")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU baseline work")
+    ap.add_argument("--pairs", type=int, default=0,
+                    help="config 4: also register this many independent pairs, split over the ranks "
+                         "(distributed.weak_scaling_pairs), and report pairs/s")
     return ap.parse_args()
 
 
@@ -329,6 +332,20 @@ def run_ours(args):
                              for lv in rep.levels],
                "paper_gtx1080ti_s": 1.99,
                "pairs_per_s": ws / reg_s}
+        if args.pairs > 0:
+            # config 4: a batch of independent pairs (seeds = pair ids), one process per GPU,
+            # no collective; inputs generated on the host before the clock starts
+            from paper_1812_06765_b200.distributed import weak_scaling_pairs
+            mine = weak_scaling_pairs(args.pairs, ws, rank)
+            batch = [make_inputs(n, ratio, seed=1000 + p)[:2] for p in mine]
+            barrier()
+            t0 = time.perf_counter()
+            for Rp, Tp in batch:
+                ngf.register(Rp, Tp, cfg)
+            barrier()
+            batch_s = max_over_ranks(time.perf_counter() - t0)
+            reg["batch"] = {"pairs": args.pairs, "per_rank": len(mine), "seconds": batch_s,
+                            "pairs_per_s": args.pairs / batch_s}
 
     cpu = None
     if rank == 0 and ws == 1:
