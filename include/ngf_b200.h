@@ -20,6 +20,7 @@
 #ifndef NGF_B200_H
 #define NGF_B200_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -135,6 +136,19 @@ void ngf_level_destroy(ngf_level_t* level);
  * mode 1 = exact path (reference operation order, bit-exact D and grad D). */
 int ngf_level_eval(ngf_level_t* level, const void* y, void* grad, double* scalars_dev, int mode,
                    void* stream);
+/* The same evaluation with host arrays, synchronous: y_host (3M values, pageable or
+ * page-locked) is uploaded through the library's staging threads, grad_host receives the
+ * gradient and scalars_host[0..2] = (J, D, S).  mode 0 or 1 as above.  This is the
+ * reference's LevelObjective.__call__(x) -> (J, grad) (objective.py:48-60) for callers
+ * that hold numpy / host memory. */
+int ngf_level_eval_host(ngf_level_t* level, const void* y_host, void* grad_host,
+                        double* scalars_host, int mode, void* stream);
+/* Host <-> device copies staged through page-locked memory by the library's copy threads
+ * (a pageable cudaMemcpy runs at a fraction of the PCIe bandwidth).  ngf_host_upload is
+ * stream-ordered and returns once src_host may be reused; ngf_host_download returns once
+ * dst_host holds the data (it synchronises the stream). */
+int ngf_host_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
+int ngf_host_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 /* Config-5 z-slab decomposition: restrict the fused evaluation to image
  * planes [zlo, zhi).  mode 2 of ngf_level_eval then writes the slab's NGF partial
  * (grad <- grad D_slab, scalars[1] <- D_slab, no curvature); after summing grad and

@@ -65,6 +65,9 @@ _PROTOS = {
                                     ctypes.POINTER(_vp)]),
     "ngf_level_destroy": (None, [_vp]),
     "ngf_level_eval": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "ngf_level_eval_host": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "ngf_host_upload": (_i, [_vp, _vp, ctypes.c_size_t, _vp]),
+    "ngf_host_download": (_i, [_vp, _vp, ctypes.c_size_t, _vp]),
     "ngf_level_ref_terms": (_vp, [_vp]),
     "ngf_level_set_timing": (_i, [_vp, _i]),
     "ngf_level_set_pt_variant": (_i, [_vp, _i]),

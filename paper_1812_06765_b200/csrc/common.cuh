@@ -16,6 +16,13 @@ extern std::atomic<int64_t> g_launches;
 int dev_alloc(void** ptr, size_t bytes);
 void dev_free(void* ptr);
 
+// Host-buffer transfers (hostio.cu): staged through page-locked memory by the copy
+// threads unless the host side is already page-locked.  host_upload is asynchronous
+// (the source may be reused on return); host_download returns once dst holds the data.
+bool host_is_pinned(const void* p);
+int host_upload(void* dst_dev, const void* src, size_t bytes, cudaStream_t s);
+int host_download(void* dst, const void* src_dev, size_t bytes, cudaStream_t s);
+
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // Count every kernel launch issued by the library (bench.py reports them).

@@ -50,6 +50,11 @@ struct ngf_level {
     int pt_variant;  // P^T variant of the exact path (0 gather, 1 scatter, 2 red-black)
     cudaEvent_t ev[2];
     ngf::LevelWork ex;
+    // ngf_level_eval_host: device copies of x and the gradient, scalars (device, pinned)
+    void* hx;
+    void* hg;
+    double* hsc;
+    double* hsc_pin;
 };
 
 namespace ngf {
@@ -552,9 +557,10 @@ void ngf_level_destroy(ngf_level_t* L) {
     if (L->plan) ngf_plan_destroy(L->plan);
     void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart,
                     L->ex.yhat, L->ex.W, L->ex.terms, L->ex.q, L->ex.s, L->ex.ghat, L->ex.gD,
-                    L->ex.cws, L->ex.dws};
+                    L->ex.cws, L->ex.dws, L->hx, L->hg, L->hsc};
     cudaDeviceSynchronize();  // no kernel may still use them
     for (void* b : bufs) dev_free(b);
+    if (L->hsc_pin) cudaFreeHost(L->hsc_pin);
     for (int k = 0; k < 2; ++k)
         if (L->ev[k]) cudaEventDestroy(L->ev[k]);
     std::free(L);
@@ -570,6 +576,26 @@ int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_de
     }
     if (mode != 0 && mode != 2) return NGF_EARG;
     return fused_part(L, y, grad, scalars_dev, s, mode == 2 ? 1 : 0);
+}
+
+int ngf_level_eval_host(ngf_level_t* L, const void* y_host, void* grad_host, double* scalars_host,
+                        int mode, void* stream) {
+    if (!L || !y_host || !grad_host || !scalars_host || (mode != 0 && mode != 1)) return NGF_EARG;
+    cudaStream_t s = as_stream(stream);
+    const size_t vb = (size_t)3 * L->def.dims[0] * L->def.dims[1] * L->def.dims[2] *
+                      (L->dtype == NGF_F32 ? 4 : 8);
+    if (!L->hx) {
+        if (dev_alloc(&L->hx, vb) || dev_alloc(&L->hg, vb) || dev_alloc((void**)&L->hsc, 4 * sizeof(double)))
+            return NGF_ENOMEM;
+        NGF_CUDA(cudaHostAlloc((void**)&L->hsc_pin, 4 * sizeof(double), cudaHostAllocDefault));
+    }
+    if (int rc = host_upload(L->hx, y_host, vb, s)) return rc;
+    if (int rc = ngf_level_eval(L, L->hx, L->hg, L->hsc, mode, stream)) return rc;
+    // the scalars go first: the gradient download waits for everything before it
+    NGF_CUDA(cudaMemcpyAsync(L->hsc_pin, L->hsc, 3 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    if (int rc = host_download(grad_host, L->hg, vb, s)) return rc;
+    std::memcpy(scalars_host, L->hsc_pin, 3 * sizeof(double));
+    return 0;
 }
 
 int ngf_level_add_curvature(ngf_level_t* L, const void* y, void* grad, double* scalars_dev,

@@ -85,6 +85,7 @@ class LevelObjective:
     evals: int = 0
     _level: DeviceLevel | None = field(default=None, repr=False)
     _R_dev: object = field(default=None, repr=False)
+    _sc_host: np.ndarray = field(default_factory=lambda: np.zeros(3), repr=False)
 
     def __post_init__(self):
         if self.pt_variant not in PT_VARIANTS:
@@ -141,29 +142,25 @@ class LevelObjective:
         return J, D, S, (dev.to_host(g) if np_out else g)
 
     def _host_call(self, x: np.ndarray):
-        """numpy in / out through pinned buffers: one H2D of x, one evaluation, one D2H of
-        (grad, J, D, S), one stream sync."""
+        """numpy in / out through ngf_level_eval_host: the library stages x through
+        page-locked memory with its copy threads (overlapping the upload DMA), evaluates,
+        and downloads the gradient; one stream sync."""
         t = dev.torch()
-        n = x.size
-        tdt = dev.torch_dtype(x.dtype)
-        st = getattr(self, "_stage", None)
-        if st is None or st[0].numel() != n or st[0].dtype != tdt:
-            st = (dev.empty((n,), tdt), dev.empty((n,), tdt), dev.zeros((3,), "float64"),
-                  t.empty(3, dtype=t.float64, pin_memory=True), t.empty(n, dtype=tdt, pin_memory=True))
-            self._stage = st
-        x_dev, g_dev, sc_dev, sc_pin, x_pin = st
-        x_pin.numpy()[:] = x.reshape(-1)
-        x_dev.copy_(x_pin, non_blocking=True)
-        self.eval_device(x_dev, g_dev, sc_dev)
+        lvl = self.level
+        ndt = dev.np_dtype(lvl.dtype)
+        x = np.ascontiguousarray(x.reshape(-1), dtype=ndt)
+        if x.size != lvl.n:
+            raise ValueError(f"x has {x.size} values, the level's deformation has {lvl.n}")
         # the gradient lands in a fresh page-locked buffer from torch's caching host
-        # allocator and is returned without a host copy; the caller owns it (the
-        # reference returns a new array per call), and it is recycled once released
-        g_out = t.empty(n, dtype=g_dev.dtype, pin_memory=True)
-        g_out.copy_(g_dev, non_blocking=True)
-        sc_pin.copy_(sc_dev, non_blocking=True)
-        t.cuda.current_stream().synchronize()
-        J, D, S = (float(v) for v in sc_pin.numpy())
-        return J, D, S, g_out.numpy()
+        # allocator (a direct DMA) and is returned without a host copy; the caller owns it
+        # (the reference returns a new array per call), and it is recycled once released
+        g_out = t.empty(lvl.n, dtype=lvl.dtype, pin_memory=True)
+        sc = self._sc_host
+        check(lib().ngf_level_eval_host(lvl.handle, x.ctypes.data, g_out.data_ptr(),
+                                        sc.ctypes.data, 1 if self.exact else 0, dev.stream()),
+              "ngf_level_eval_host")
+        self.evals += 1
+        return float(sc[0]), float(sc[1]), float(sc[2]), g_out.numpy()
 
     def __call__(self, x):
         if dev.is_tensor(x):
