@@ -9,6 +9,7 @@
 
 #include <cooperative_groups.h>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -343,6 +344,207 @@ __global__ void __launch_bounds__(GRID ? kRedThreads : kSmallThreads) k_two_loop
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.slope = slope;
 }
 
+// Register-resident two-loop (the path used whenever q fits in registers): q stays in
+// registers for the whole recursion, and the loads of the next pair's vectors are issued
+// before the current reduction, so each of the 2m + 1 sequential steps costs one
+// reduction latency instead of a dependent L2 round trip per element.  The reduction
+// group is a thread-block cluster (C <= 16 CTAs, partials exchanged through distributed
+// shared memory) or, for long vectors, the whole grid of a cooperative launch.  Element
+// updates are the same dtype operations as k_two_loop; the dot products are summed in a
+// fixed order (warp butterflies, then CTAs in rank order), identical in every CTA.
+constexpr int kRvThreads = 512;
+constexpr int kRvWarps = kRvThreads / 32;
+
+template <bool GRIDSYNC>
+struct RvReducer {
+    double* parts;  // grid mode: [2][gridDim.x] block partials
+    int C;          // cluster mode: CTAs per cluster
+    __device__ __forceinline__ double operator()(double v, int parity, double* wred, double (*cslot)[16],
+                                                 double* bcast) const {
+        const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) wred[warp] = v;
+        __syncthreads();
+        double t = 0.0;
+        if (warp == 0) {
+            t = lane < kRvWarps ? wred[lane] : 0.0;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+        }
+        if constexpr (GRIDSYNC) {
+            if (threadIdx.x == 0) parts[parity * gridDim.x + blockIdx.x] = t;
+            cg::this_grid().sync();
+            if (warp == 0) {
+                double u = 0.0;
+                for (int b = lane; b < (int)gridDim.x; b += 32) u += __ldcg(parts + parity * gridDim.x + b);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+                if (lane == 0) *bcast = u;
+            }
+        } else {
+            if (C == 1) {
+                if (threadIdx.x == 0) *bcast = t;
+            } else {
+                cg::cluster_group cl = cg::this_cluster();
+                const unsigned me = cl.block_rank();
+                if (warp == 0 && lane < C) *cl.map_shared_rank(&cslot[parity][me], lane) = t;
+                cl.sync();
+                if (warp == 0) {
+                    double u = lane < C ? cslot[parity][lane] : 0.0;
+#pragma unroll
+                    for (int o = 8; o > 0; o >>= 1) u += __shfl_xor_sync(0xffffffffu, u, o);
+                    if (lane == 0) *bcast = u;
+                }
+            }
+        }
+        __syncthreads();
+        return *bcast;
+    }
+};
+
+template <typename T, int VPT, bool GRIDSYNC>
+__global__ void __launch_bounds__(kRvThreads) k_two_loop_rv(const TwoLoopArgs<T> a, int C) {
+    __shared__ double wred[32];
+    __shared__ double cslot[2][16];
+    __shared__ double bcast;
+    const RvReducer<GRIDSYNC> red{a.parts, C};
+    const int64_t i0 = blockIdx.x * (int64_t)kRvThreads + threadIdx.x;
+    const int64_t st = (int64_t)gridDim.x * kRvThreads;
+    const int64_t n = a.n;
+    T q[VPT], u[VPT], w[VPT];
+    auto load = [&](T(&r)[VPT], const T* __restrict__ src) {
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const int64_t i = i0 + j * st;
+            r[j] = i < n ? __ldcg(src + i) : T(0);
+        }
+    };
+    int parity = 0;
+    double alpha[kMaxMem];
+    load(q, a.g);
+    double v = 0.0;
+    if (a.m > 0) {
+        load(w, a.S[a.m - 1]);
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) v += (double)w[j] * (double)q[j];
+    }
+    // first loop, newest pair first: alpha = rho * (s . q); q -= dtype(alpha) * y
+    for (int k = a.m - 1; k >= 0; --k) {
+        load(u, a.Y[k]);
+        load(w, k > 0 ? a.S[k - 1] : a.Y[0]);  // in flight during the reduction
+        const double dt = red(v, parity, wred, cslot, &bcast);
+        parity ^= 1;
+        alpha[k] = a.rho[k] * dt;
+        const T al = (T)alpha[k];
+        const T tg = (T)a.gamma;
+        v = 0.0;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            T x = __fsub_rn_t(q[j], __fmul_rn_t(al, u[j]));
+            if (k == 0) x = __fmul_rn_t(x, tg);  // q *= dtype(gamma)
+            q[j] = x;
+            v += (double)w[j] * (double)x;
+        }
+    }
+    // second loop, oldest pair first: beta = rho * (y . q); q += dtype(alpha - beta) * s
+    for (int k = 0; k < a.m; ++k) {
+        load(u, a.S[k]);
+        load(w, k < a.m - 1 ? a.Y[k + 1] : a.g);
+        const double dt = red(v, parity, wred, cslot, &bcast);
+        parity ^= 1;
+        const double beta = a.rho[k] * dt;
+        const T c = (T)(alpha[k] - beta);
+        const bool last = (k == a.m - 1);
+        v = 0.0;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            T x = __fadd_rn_t(q[j], __fmul_rn_t(c, u[j]));
+            if (last) x = -x;
+            q[j] = x;
+            v += (double)w[j] * (double)x;
+        }
+    }
+    if (a.m == 0) {  // d = -g
+        v = 0.0;
+#pragma unroll
+        for (int j = 0; j < VPT; ++j) {
+            const T g = q[j];
+            q[j] = -g;
+            v += (double)g * (double)q[j];
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+        const int64_t i = i0 + j * st;
+        if (i < n) a.d[i] = q[j];
+    }
+    const double slope = red(v, parity, wred, cslot, &bcast);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *a.slope = slope;
+}
+
+template <typename T, int VPT>
+int launch_rv(const TwoLoopArgs<T>& a, int C, bool grid, cudaStream_t s) {
+    if (grid) {
+        TwoLoopArgs<T> aa = a;
+        int cc = 1;
+        void* args[] = {&aa, &cc};
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        NGF_CUDA(cudaLaunchCooperativeKernel((const void*)k_two_loop_rv<T, VPT, true>, dim3(kRedBlocks),
+                                             dim3(kRvThreads), args, 0, s));
+        return 0;
+    }
+    static bool attr = false;
+    if (!attr) {
+        NGF_CUDA(cudaFuncSetAttribute(k_two_loop_rv<T, VPT, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kRvThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    NGF_CUDA(cudaLaunchKernelEx(&cfg, k_two_loop_rv<T, VPT, false>, a, C));
+    return 0;
+}
+
+// Register-resident path if q fits (<= 16 values per thread: more spills); -1 if not.
+template <typename T>
+int two_loop_rv(const TwoLoopArgs<T>& a, cudaStream_t s) {
+    const int64_t n = a.n;
+    constexpr int kVmax = 16;
+    const char* env = std::getenv("NGF_TWO_LOOP");
+    if (env && std::atoi(env) == 0) return -1;
+    // smallest cluster giving <= 8 values per thread, else 16 CTAs, else the whole grid
+    int C = 1;
+    while (C < 16 && (int64_t)C * kRvThreads * 8 < n) C *= 2;
+    bool grid = false;
+    int64_t threads = (int64_t)C * kRvThreads;
+    if ((n + threads - 1) / threads > kVmax) {
+        grid = true;
+        threads = (int64_t)kRedBlocks * kRvThreads;
+        if ((n + threads - 1) / threads > kVmax) return -1;
+    }
+    const int64_t need = (n + threads - 1) / threads;
+    int vpt = 1;
+    while (vpt < need) vpt *= 2;
+    switch (vpt) {
+        case 1: return launch_rv<T, 1>(a, C, grid, s);
+        case 2: return launch_rv<T, 2>(a, C, grid, s);
+        case 4: return launch_rv<T, 4>(a, C, grid, s);
+        case 8: return launch_rv<T, 8>(a, C, grid, s);
+        case 16: return launch_rv<T, 16>(a, C, grid, s);
+        default: return -1;
+    }
+}
+
 template <typename T>
 int two_loop_impl(const void* const* S, const void* const* Y, const double* rho, double gamma, int m,
                   const void* g, void* d, int64_t n, double* slope, cudaStream_t s) {
@@ -362,6 +564,8 @@ int two_loop_impl(const void* const* S, const void* const* Y, const double* rho,
     a.n = n;
     a.parts = sc->parts;
     a.slope = slope;
+    const int rv = two_loop_rv<T>(a, s);
+    if (rv >= 0) return rv;
     if (n <= kSmallN) {
         NGF_LAUNCH((k_two_loop<T, false>), 1, kSmallThreads, 0, s, a);
         NGF_CHECK_LAUNCH();
