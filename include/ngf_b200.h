@@ -222,6 +222,14 @@ typedef struct {
 int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, void* x, int64_t n,
                         const ngf_lbfgs_cfg_t* cfg, ngf_lbfgs_result_t* res, double* rec, double* rows,
                         int max_rows, void* stream);
+/* Levels whose vectors fit the cluster two-loop (n <= 131072: deformation grids up to
+ * ~35^3) can run the whole iteration loop as ONE CUDA graph with device-side control
+ * (conditional nodes; csrc/solver_graph.cu) -- the same decisions, no host round trips --
+ * when ngf_lbfgs_set_graph(1) (or NGF_LBFGS_GRAPH=1) selects it; the default is the
+ * host-driven loop.  Returns the previous setting. */
+int ngf_lbfgs_set_graph(int on);
+/* Number of level loops that ran as a graph in this process (tests, bench). */
+int64_t ngf_lbfgs_graph_runs(void);
 
 #ifdef __cplusplus
 }

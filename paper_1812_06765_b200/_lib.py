@@ -66,6 +66,8 @@ _PROTOS = {
     "ngf_level_destroy": (None, [_vp]),
     "ngf_level_eval": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
     "ngf_level_eval_host": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
+    "ngf_lbfgs_set_graph": (_i, [_i]),
+    "ngf_lbfgs_graph_runs": (_i64, []),
     "ngf_host_upload": (_i, [_vp, _vp, ctypes.c_size_t, _vp]),
     "ngf_host_download": (_i, [_vp, _vp, ctypes.c_size_t, _vp]),
     "ngf_level_ref_terms": (_vp, [_vp]),

@@ -476,7 +476,12 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
     p.ihx2 = (T)1 / (p.g.hx * p.g.hx);
     p.ihy2 = (T)1 / (p.g.hy * p.g.hy);
     p.ihz2 = (T)1 / (p.g.hz * p.g.hz);
-    if (part == 2) {
+    // programmatic dependent launch edges inside conditional graph bodies are opt-in
+    // (NGF_GRAPH_PDL=1); a captured evaluation launches k_post plainly by default
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    static const bool graph_pdl = std::getenv("NGF_GRAPH_PDL") != nullptr;
+    if (part == 2 || (cap != cudaStreamCaptureStatusNone && !graph_pdl)) {
         NGF_LAUNCH(k_post<T>, cgrid, dim3(32, 8), 0, s, p);
     } else {
         // programmatic dependent launch after the march

@@ -13,6 +13,7 @@
 #include <mutex>
 
 #include "common.cuh"
+#include "lbfgs.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -158,11 +159,10 @@ __global__ void k_sub(const T* __restrict__ a, const T* __restrict__ b, T* __res
 
 // s = x_new - x, y = g_new - g and their stats in one pass (lbfgs.py:145-148, :161-164)
 template <typename T>
-__global__ void __launch_bounds__(kRedThreads) k_pair(const T* __restrict__ xn, const T* __restrict__ x,
-                                                      const T* __restrict__ gn, const T* __restrict__ g,
-                                                      T* __restrict__ s_out, T* __restrict__ y_out,
-                                                      int64_t n, double* parts, unsigned int* counter,
-                                                      double* out) {
+__device__ __forceinline__ void pair_body(const T* __restrict__ xn, const T* __restrict__ x,
+                                          const T* __restrict__ gn, const T* __restrict__ g,
+                                          T* __restrict__ s_out, T* __restrict__ y_out, int64_t n,
+                                          double* parts, unsigned int* counter, double* out) {
     __shared__ double red[4][kRedThreads / 32];
     __shared__ double redm[kRedThreads / 32];
     __shared__ bool last;
@@ -201,21 +201,32 @@ __global__ void __launch_bounds__(kRedThreads) k_pair(const T* __restrict__ xn, 
     }
 }
 
-constexpr int kMaxMem = 32;
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_pair(const T* __restrict__ xn, const T* __restrict__ x,
+                                                      const T* __restrict__ gn, const T* __restrict__ g,
+                                                      T* __restrict__ s_out, T* __restrict__ y_out,
+                                                      int64_t n, double* parts, unsigned int* counter,
+                                                      double* out) {
+    pair_body(xn, x, gn, g, s_out, y_out, n, parts, counter, out);
+}
+
+// the same with the output pair chosen on the device (graph-driven solver)
+template <typename T>
+__global__ void __launch_bounds__(kRedThreads) k_pair_ind(const T* __restrict__ xn, const T* __restrict__ x,
+                                                          const T* __restrict__ gn, const T* __restrict__ g,
+                                                          T* const* s_ptr, T* const* y_ptr, int64_t n,
+                                                          double* parts, unsigned int* counter, double* out) {
+    pair_body(xn, x, gn, g, *s_ptr, *y_ptr, n, parts, counter, out);
+}
 
 template <typename T>
-struct TwoLoopArgs {
-    const T* S[kMaxMem];
-    const T* Y[kMaxMem];
-    double rho[kMaxMem];
-    double gamma;
-    int m;
-    const T* g;
-    T* d;  // holds q during the recursion, -q at the end
-    int64_t n;
-    double* parts;  // [2][kRedBlocks]
-    double* slope;
-};
+__global__ void k_axpy_ind(const T* __restrict__ x, const double* t, const T* __restrict__ d,
+                           T* __restrict__ out, int64_t n) {
+    const T tt = (T)*t;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __fadd_rn_t(x[i], __fmul_rn_t(tt, d[i]));
+}
 
 // grid-wide deterministic sum of one value per thread: block partial -> parts[buf][b],
 // grid sync, every block sums the partials in block order (identical result everywhere)
@@ -404,7 +415,7 @@ struct RvReducer {
 };
 
 template <typename T, int VPT, bool GRIDSYNC>
-__global__ void __launch_bounds__(kRvThreads) k_two_loop_rv(const TwoLoopArgs<T> a, int C) {
+__device__ __forceinline__ void two_loop_rv_body(const TwoLoopArgs<T>& a, int C) {
     __shared__ double wred[32];
     __shared__ double cslot[2][16];
     __shared__ double bcast;
@@ -481,6 +492,17 @@ __global__ void __launch_bounds__(kRvThreads) k_two_loop_rv(const TwoLoopArgs<T>
     }
     const double slope = red(v, parity, wred, cslot, &bcast);
     if (blockIdx.x == 0 && threadIdx.x == 0) *a.slope = slope;
+}
+
+template <typename T, int VPT, bool GRIDSYNC>
+__global__ void __launch_bounds__(kRvThreads) k_two_loop_rv(const TwoLoopArgs<T> a, int C) {
+    two_loop_rv_body<T, VPT, GRIDSYNC>(a, C);
+}
+
+// arguments in device memory, rewritten by the graph-driven solver between launches
+template <typename T, int VPT>
+__global__ void __launch_bounds__(kRvThreads) k_two_loop_rv_ind(const TwoLoopArgs<T>* __restrict__ ap, int C) {
+    two_loop_rv_body<T, VPT, false>(*ap, C);
 }
 
 template <typename T, int VPT>
@@ -577,6 +599,88 @@ int two_loop_impl(const void* const* S, const void* const* Y, const double* rho,
                                          args, 0, s));
     return 0;
 }
+
+// ---- device-argument launchers for the graph-driven solver (solver_graph.cu)
+
+static void rv_shape(int64_t n, int& C, int& vpt) {
+    C = 1;
+    while (C < 16 && (int64_t)C * kRvThreads * 8 < n) C *= 2;
+    const int64_t threads = (int64_t)C * kRvThreads;
+    const int64_t need = (n + threads - 1) / threads;
+    vpt = 1;
+    while (vpt < need) vpt *= 2;
+}
+
+template <typename T, int VPT>
+static int launch_rv_ind(const TwoLoopArgs<T>* ap, int C, cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        NGF_CUDA(cudaFuncSetAttribute(k_two_loop_rv_ind<T, VPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        attr = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(C);
+    cfg.blockDim = dim3(kRvThreads);
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    g_launches.fetch_add(1, std::memory_order_relaxed);
+    NGF_CUDA(cudaLaunchKernelEx(&cfg, k_two_loop_rv_ind<T, VPT>, ap, C));
+    return 0;
+}
+
+template <typename T>
+int two_loop_dev_launch(const TwoLoopArgs<T>* ap, int64_t n, cudaStream_t s) {
+    if (n > kTwoLoopClusterMaxN) return NGF_EARG;
+    int C, vpt;
+    rv_shape(n, C, vpt);
+    switch (vpt) {
+        case 1: return launch_rv_ind<T, 1>(ap, C, s);
+        case 2: return launch_rv_ind<T, 2>(ap, C, s);
+        case 4: return launch_rv_ind<T, 4>(ap, C, s);
+        case 8: return launch_rv_ind<T, 8>(ap, C, s);
+        case 16: return launch_rv_ind<T, 16>(ap, C, s);
+        default: return NGF_EARG;
+    }
+}
+
+template <typename T>
+int pair_dev_launch(const T* xn, const T* x, const T* gn, const T* g, T* const* s_ptr, T* const* y_ptr,
+                    int64_t n, double* out, cudaStream_t s) {
+    Scratch* sc = scratch();
+    if (!sc) return NGF_ENOMEM;
+    NGF_LAUNCH(k_pair_ind<T>, kRedBlocks, kRedThreads, 0, s, xn, x, gn, g, s_ptr, y_ptr, n, sc->parts,
+               sc->counter, out);
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+template <typename T>
+int axpy_dev_launch(const T* x, const double* t, const T* d, T* out, int64_t n, cudaStream_t s) {
+    NGF_LAUNCH(k_axpy_ind<T>, blocks_for(n, 256), 256, 0, s, x, t, d, out, n);
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+double* lbfgs_parts() {
+    Scratch* sc = scratch();
+    return sc ? sc->parts : nullptr;
+}
+
+template int two_loop_dev_launch<float>(const TwoLoopArgs<float>*, int64_t, cudaStream_t);
+template int two_loop_dev_launch<double>(const TwoLoopArgs<double>*, int64_t, cudaStream_t);
+template int pair_dev_launch<float>(const float*, const float*, const float*, const float*, float* const*,
+                                    float* const*, int64_t, double*, cudaStream_t);
+template int pair_dev_launch<double>(const double*, const double*, const double*, const double*,
+                                     double* const*, double* const*, int64_t, double*, cudaStream_t);
+template int axpy_dev_launch<float>(const float*, const double*, const float*, float*, int64_t, cudaStream_t);
+template int axpy_dev_launch<double>(const double*, const double*, const double*, double*, int64_t,
+                                     cudaStream_t);
 
 }  // namespace ngf
 

@@ -147,6 +147,50 @@ def test_native_driver_matches_python_driver(monkeypatch, exact):
     assert np.array_equal(xn, xp)
 
 
+@pytest.mark.parametrize("cfg", [
+    ngf.LbfgsConfig(max_iterations=30),
+    ngf.LbfgsConfig(memory=1, max_iterations=20),                        # history ageing
+    ngf.LbfgsConfig(initial_step=40.0, max_ls_steps=3, max_iterations=20),  # backtracking, failure
+    ngf.LbfgsConfig(initial_step=0.05, step_shrink=0.7, max_iterations=12),  # long forward expansions
+], ids=["default", "memory1", "backtrack", "expand"])
+def test_graph_driver_matches_host_and_python(monkeypatch, cfg):
+    """The graph-driven level loop (csrc/solver_graph.cu: one CUDA graph, device-side
+    decisions) and the host-driven native loop take exactly the Python driver's decisions."""
+    import torch
+
+    from paper_1812_06765_b200._lib import lib
+
+    gi = ngf.Grid3((40, 36, 32), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    gd = ngf.deformation_grid_for(gi, 4)
+    R = ngf.smooth_random_volume(gi, seed=21).values.astype(np.float32)
+    T = ngf.smooth_random_volume(gi, seed=22).values.astype(np.float32)
+    x0 = ngf.make_identity(gd).field.astype(np.float32).ravel()
+    plan = ngf.build_gather_plan(gd, gi)
+    out = []
+    try:
+        for mode in ("python", "host", "graph"):
+            if mode == "python":
+                monkeypatch.setenv("NGF_PY_LBFGS", "1")
+            else:
+                monkeypatch.delenv("NGF_PY_LBFGS", raising=False)
+                lib().ngf_lbfgs_set_graph(1 if mode == "graph" else 0)
+            obj = ngf.LevelObjective.from_device(torch.from_numpy(T).cuda(), torch.from_numpy(R).cuda(), plan,
+                                                 ngf.NgfParams(), 1.0)
+            runs = lib().ngf_lbfgs_graph_runs()
+            out.append(ngf.lbfgs_minimize(obj, x0.copy(), cfg))
+            assert lib().ngf_lbfgs_graph_runs() - runs == (1 if mode == "graph" else 0), mode
+    finally:
+        lib().ngf_lbfgs_set_graph(0)
+    xp, tp = out[0]
+    for x, t in out[1:]:
+        assert (t.stop_reason, t.evaluations, t.iterations, t.line_search_failed) == \
+               (tp.stop_reason, tp.evaluations, tp.iterations, tp.line_search_failed)
+        assert [(r.J, r.grad_inf, r.step, r.ls_evals) for r in t.records] == \
+               [(r.J, r.grad_inf, r.step, r.ls_evals) for r in tp.records]
+        assert t.J_rows == tp.J_rows
+        assert np.array_equal(x, xp)
+
+
 def test_native_driver_edge_cases(monkeypatch):
     """Stationary start (constant images at the identity: grad J = 0 exactly) and a zero
     iteration budget give the same traces from the native and the Python drivers."""
