@@ -36,7 +36,7 @@ METRIC = "256^3 full-registration time (s); obj+grad evals/s; HBM GB/s vs peak"
 WORKLOADS = {
     # name: (image n, grid ratio, levels for the full registration)
     "c1": (64, 4, 1),
-    "c2": (128, 4, 3),
+    "c2": (128, 2, 3),  # ratio 2: 64^3 deformation grid on the finest level (DIR-lab-like)
     "c3": (256, 4, 4),
     "c5": (512, 4, 4),  # z-slab decomposition over the ranks (strong scaling), evaluation only
 }

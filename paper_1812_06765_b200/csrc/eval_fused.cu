@@ -403,6 +403,8 @@ int fused_prepare<float>(int v, size_t smem) {
         case 1: return march_prepare<float, V1>(smem);
         case 2: return march_prepare<float, V2>(smem);
         case 3: return march_prepare<float, V3>(smem);
+        case 4: return march_prepare<float, V4>(smem);
+        case 5: return march_prepare<float, V5>(smem);
         default: return march_prepare<float, V0>(smem);
     }
 }
@@ -425,6 +427,8 @@ void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
         case 1: march_launch<float, V1>(a, s); return;
         case 2: march_launch<float, V2>(a, s); return;
         case 3: march_launch<float, V3>(a, s); return;
+        case 4: march_launch<float, V4>(a, s); return;
+        case 5: march_launch<float, V5>(a, s); return;
         default: march_launch<float, V0>(a, s); return;
     }
 }

@@ -173,7 +173,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         const int v = env ? std::atoi(env) : -1;
         cand = (v == 0 || v == 4 || v == 5) ? std::vector<int>{v} : std::vector<int>{4, 5};
     } else if (env) {
-        const int v = std::atoi(env) % 4;  // f32 shapes: 0 .. 3
+        const int v = std::atoi(env) % 6;  // f32 shapes: 0 .. 5
         cand = {v};
     } else {
         cand = {1, 2};

@@ -211,6 +211,7 @@ def test_packed_march_matches_scalar_march(monkeypatch, dims, spacing, ratio):
 
 
 @pytest.mark.parametrize("variant,prec", [("0", "f32"), ("1", "f32"), ("2", "f32"), ("3", "f32"),
+                                          ("4", "f32"), ("5", "f32"),
                                           ("0", "f64"), ("4", "f64"), ("5", "f64")])
 @pytest.mark.parametrize("dims,ratio", [((40, 40, 40), 1), ((70, 45, 33), 4)])
 def test_every_kernel_variant_within_tolerance(monkeypatch, variant, prec, dims, ratio):
