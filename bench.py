@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
+    ap.add_argument("--precision", default="f32", choices=["f32", "f64"],
+                    help="working dtype (the reference's default precision is f64, multilevel.py:55)")
     ap.add_argument("--no-register", action="store_true", help="skip the full-registration leg")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU baseline work")
     ap.add_argument("--pairs", type=int, default=0,
@@ -130,11 +132,11 @@ class ClockSampler:
                 "samples": len(self.rows)}
 
 
-def make_inputs(n: int, ratio: int, seed: int):
+def make_inputs(n: int, ratio: int, seed: int, dtype=np.float32):
     import paper_1812_06765_b200 as ngf
-    R, T, _ = ngf.ct_pair(n, seed=seed, dtype=np.float32)
+    R, T, _ = ngf.ct_pair(n, seed=seed, dtype=dtype)
     gd = ngf.deformation_grid_for(R.grid, ratio)
-    y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=2.0).field.astype(np.float32)
+    y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=2.0).field.astype(dtype)
     return R, T, gd, y
 
 
@@ -155,7 +157,8 @@ def cpu_baseline(R, T, gd, y, budget_s: float):
     dt = (time.perf_counter() - t0) / reps
     return {"value": 1.0 / dt, "unit": "evals/s", "cores": cores, "kind": "port",
             "sample": f"{reps} full evaluations of the same {R.grid.dims[0]}^3/{gd.dims[0]}^3 workload "
-                      f"(oracle/ngf_oracle.py, workers={cores}, f32) after 1 warm-up; {dt:.2f} s/eval"}
+                      f"(oracle/ngf_oracle.py, workers={cores}, {np.dtype(y.dtype).name}) after 1 warm-up; "
+                      f"{dt:.2f} s/eval"}
 
 
 def run_reference(args):
@@ -163,7 +166,7 @@ def run_reference(args):
     if rank != 0:
         return
     n, ratio, _ = WORKLOADS[args.workload]
-    R, T, gd, y = make_inputs(n, ratio, 0)
+    R, T, gd, y = make_inputs(n, ratio, 0, np.float32 if args.precision == "f32" else np.float64)
     from oracle import ngf_oracle as O
     cores = os.cpu_count() or 1
     og = O.grid(R.grid.dims, R.grid.spacing, R.grid.origin)
@@ -185,7 +188,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": warm + 1, "ms_per_step": 1000 * dt / steps,
             "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
-            "vs_baseline": None, "dtype": "f32", "data": "synthetic", "impl": "reference",
+            "vs_baseline": None, "dtype": args.precision, "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair, {gd.dims[0]}^3 def grid, "
                                    "one LevelObjective evaluation per step"},
             "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
@@ -214,7 +217,9 @@ def run_ours(args):
 
     n, ratio, levels = WORKLOADS[args.workload]
     strong = args.workload == "c5"  # one pair split in z-slabs over all ranks
-    R, T, gd, y = make_inputs(n, ratio, seed=0 if strong else rank)
+    npdt = np.float32 if args.precision == "f32" else np.float64
+    es = np.dtype(npdt).itemsize
+    R, T, gd, y = make_inputs(n, ratio, seed=0 if strong else rank, dtype=npdt)
     gi = R.grid
     plan = ngf.build_gather_plan(gd, gi)
     T_dev = torch.from_numpy(T.values).cuda()
@@ -245,6 +250,10 @@ def run_ours(args):
         return float(t.item())
 
     # ---------------- device-resident leg (value) ----------------
+    # inputs smaller than twice the 126 MB L2 are timed cold: an L2 flush (a 512 MB write)
+    # before every step, outside the per-step events
+    l2_cold = 20 * gi.dims[0] * gi.dims[1] * (gi.dims[2]) * es // 4 < 2 * 126 * 2**20
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if l2_cold else None
     for _ in range(max(3, args.warmup)):
         evaluator.eval_device(x, g, sc)
     barrier()
@@ -252,13 +261,25 @@ def run_ours(args):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(dev_index) as clk:
         barrier()
-        e0.record(stream)
-        for _ in range(args.steps):
-            evaluator.eval_device(x, g, sc)
-        e1.record(stream)
-        barrier()
+        if l2_cold:
+            evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                   for _ in range(args.steps)]
+            for a, b in evs:
+                flush.fill_(1)
+                a.record(stream)
+                evaluator.eval_device(x, g, sc)
+                b.record(stream)
+            barrier()
+            step_ms = sum(a.elapsed_time(b) for a, b in evs)
+        else:
+            e0.record(stream)
+            for _ in range(args.steps):
+                evaluator.eval_device(x, g, sc)
+            e1.record(stream)
+            barrier()
+            step_ms = e0.elapsed_time(e1)
     launches = _lib.launch_count() - launches0
-    t_ms = max_over_ranks(e0.elapsed_time(e1))
+    t_ms = max_over_ranks(step_ms)
     jobs = 1 if strong else ws  # evaluations completed per step, whole job
     value = jobs * args.steps / (t_ms / 1000.0)
 
@@ -275,8 +296,8 @@ def run_ours(args):
     info = (ctypes.c_int64 * 9)()
     _lib.check(_lib.lib().ngf_level_info(level.handle, info), "info")
     N, M = gi.dims[0] * gi.dims[1] * (zhi - zlo), gd.num_points  # this rank's slab
-    bytes_kernel = 20 * N + 12 * M          # T + packed reference terms + y
-    bytes_eval = 20 * N + 24 * M            # + grad J written (B_eval)
+    bytes_kernel = es * (5 * N + 3 * M)     # T + packed reference terms + y
+    bytes_eval = es * (5 * N + 6 * M)       # + grad J written (B_eval: 20N + 24M in f32)
     peak, peak_kind = peaks()
     achieved = bytes_kernel / (k_ms / 1000.0) / 1e9
     eval_ms = t_ms / args.steps
@@ -323,14 +344,14 @@ def run_ours(args):
     # ---------------- full coarse-to-fine registration (the paper's headline) -------------
     reg = None
     if not args.no_register and not strong:
-        cfg = ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision="f32")
+        cfg = ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision=args.precision)
         ngf.register(R, T, cfg)  # warm-up (allocations, first-touch)
         barrier()
         t0 = time.perf_counter()
         yr, rep = ngf.register(R, T, cfg)
         barrier()
         reg_s = max_over_ranks(time.perf_counter() - t0)
-        reg = {"seconds": reg_s, "levels": levels, "inputs": "host numpy f32 (H2D inside)",
+        reg = {"seconds": reg_s, "levels": levels, "inputs": f"host numpy {args.precision} (H2D inside)",
                "seconds_pyramid": round(rep.seconds_pyramid, 4),
                "per_level": [{"image": lv.image_dims[0], "def": lv.def_dims[0],
                               "iterations": lv.iterations, "evals": lv.evaluations,
@@ -344,7 +365,7 @@ def run_ours(args):
             # no collective; inputs generated on the host before the clock starts
             from paper_1812_06765_b200.distributed import weak_scaling_pairs
             mine = weak_scaling_pairs(args.pairs, ws, rank)
-            batch = [make_inputs(n, ratio, seed=1000 + p)[:2] for p in mine]
+            batch = [make_inputs(n, ratio, seed=1000 + p, dtype=npdt)[:2] for p in mine]
             barrier()
             t0 = time.perf_counter()
             for Rp, Tp in batch:
@@ -363,17 +384,21 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": ws,
             "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": eval_ms,
             "higher_is_better": True, "scaling": "strong" if strong else "weak", "vs_baseline": None,
-            "dtype": "f32",
+            "dtype": args.precision,
             "data": "synthetic",
             "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair (1 mm), "
                                    f"{gd.dims[0]}^3 def grid, NGF tau=rho=10, alpha=1; one "
                                    "LevelObjective evaluation per step",
-                       "l2": "inputs larger than L2 (T 4N + reference terms 16N = "
-                             f"{(20 * N) / 1e6:.0f} MB > 126 MB)",
+                       "l2": (f"inputs smaller than 2 x L2 (T + reference terms = {(5 * es * N) / 1e6:.0f} MB): "
+                              "L2 flushed (512 MB write) before every timed step, steps timed one by one"
+                              if l2_cold else
+                              f"inputs larger than L2 (T + reference terms = {(5 * es * N) / 1e6:.0f} MB "
+                              "> 126 MB), back-to-back steps"),
                        "parallelism": (f"z-slabs x{ws} (one pair; NCCL all-reduce of grad D and D)"
                                        if strong else f"replicas x{ws} (one independent pair per GPU)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": ncu_traffic(args.workload),
+                         "frac": achieved / peak,
+                         "traffic": ncu_traffic(args.workload + ("" if args.precision == "f32" else "_f64")),
                          "kernel": "k_eval_fused", "kernel_ms": k_ms,
                          "bytes_per_launch": bytes_kernel, "peak_kind": peak_kind,
                          "eval_frac": bytes_eval / (eval_ms / 1000.0) / 1e9 / peak,
