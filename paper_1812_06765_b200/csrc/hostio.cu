@@ -8,6 +8,7 @@
 // and destinations skip the staging.
 
 #include <immintrin.h>
+#include <unistd.h>
 
 #include <algorithm>
 #include <atomic>
@@ -30,8 +31,16 @@ namespace {
 class Team {
   public:
     static Team& get() {
-        static Team t;
-        return t;
+        // a forked child has none of the parent's threads: it builds its own team (the
+        // parent's object is leaked in the child, never joined)
+        static Team* t = nullptr;
+        static pid_t owner = 0;
+        const pid_t me = getpid();
+        if (!t || owner != me) {
+            t = new Team();
+            owner = me;
+        }
+        return *t;
     }
     int size() const { return (int)th_.size(); }
 
