@@ -32,6 +32,10 @@
 
 namespace ngf {
 
+#ifndef NGF_T_PREFETCH
+#define NGF_T_PREFETCH 0  // measured slower: 356 vs 340 us at 256^3
+#endif
+
 template <typename T>
 __host__ __device__ __forceinline__ void fd_coef(int i, int n, T ih, T& cm, T& c0, T& cp) {
     // derivative at index i as cm*v[i-1] + c0*v[i] + cp*v[i+1] (warp.py:130-143)
@@ -206,6 +210,7 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
         unsigned off[S];
         T fx[S], fy[S], fz[S];
         bool in[S];
+        bool pf[S];  // the template plane after this slot's corner planes exists
 #pragma unroll
         for (int s = 0; s < S; ++s) {
             // yhat = Ylo * (1 - w) + Yhi * w, each op rounded (transfer.py:126)
@@ -217,6 +222,7 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
             const int iy = cell_axis<T, POW2>(yh1, a.oy, a.hy, a.ihy, a.nm1y, a.hiy, inside, fy[s]);
             const int iz = cell_axis<T, POW2>(yh2, a.oz, a.hz, a.ihz, a.nm1z, a.hiz, inside, fz[s]);
             in[s] = inside;
+            pf[s] = iz + 2 < a.nz;
             off[s] = (unsigned)iz * nxy + (unsigned)iy * (unsigned)a.nx + (unsigned)ix;
         }
         T cv[S][8];
@@ -251,6 +257,14 @@ __device__ __forceinline__ void fused_step(const FusedArgs<T>& a, SmemL<T, C>& s
                 cv[s][5] = __ldg(bz + 1);
                 cv[s][6] = __ldg(byz);
                 cv[s][7] = __ldg(byz + 1);
+#if NGF_T_PREFETCH
+                // the next plane's new corner plane (y advances about one voxel per plane)
+                // towards L2, so its first gathers miss L1 but not DRAM
+                if (pf[s]) {
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(bz + nxy));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(byz + nxy));
+                }
+#endif
             }
         }
 #pragma unroll
