@@ -87,6 +87,7 @@ def test_objective_from_reference_terms_matches_from_R():
     ((70, 45, 33), 4, None),        # ragged, several partial tiles
     ((40, 40, 40), 1, None),        # def grid == image grid (ratio 1)
     ((50, 30, 20), 3, None),        # non power-of-two ratio
+    ((48, 40, 36), 2, None),        # ratio 2 (config 2: 64^3 def grid on 128^3)
     ((33, 33, 33), None, (17, 17, 17)),  # 65^3-on-128^3 style (width-5 gather)
     ((24, 20, 1), 4, None),         # degenerate z
     ((48, 36, 28), 16, None),       # very coarse def grid (wide windows)
