@@ -1,10 +1,14 @@
 // Level objective: reference terms, fused/exact evaluation (objective.py:22-60).
 
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <string>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -149,6 +153,7 @@ static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, 
 
 template <typename T>
 static int fused_setup(ngf_level* L, int zlo, int zhi) {
+    const auto t_start = std::chrono::steady_clock::now();
     const ngf_plan_t* p = L->plan;
     const int nx = (int)L->img.dims[0], ny = (int)L->img.dims[1], nz = (int)L->img.dims[2];
     const int ndx = (int)L->def.dims[0], ndy = (int)L->def.dims[1], ndz = (int)L->def.dims[2];
@@ -167,91 +172,126 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     // chunking must keep each def node covered by at most kCover chunks (k_post's sum).
     static const int kMinBlocks[] = {2, 2, 2, 2, 1, 1};
     static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5, 1.0, 1.14};  // f64 (4, 5) relative to 4
-    std::vector<int> cand;
-    const char* env = std::getenv("NGF_FUSED_VARIANT");
-    if (sizeof(T) == 8) {  // f64 shapes: 0, 4, 5
-        const int v = env ? std::atoi(env) : -1;
-        cand = (v == 0 || v == 4 || v == 5) ? std::vector<int>{v} : std::vector<int>{4, 5};
-    } else if (env) {
-        const int v = std::atoi(env) % 6;  // f32 shapes: 0 .. 5
-        cand = {v};
-    } else {
-        cand = {1, 2};
-    }
-    const int nzs = zhi - zlo;
-    const double ovh = std::getenv("NGF_CHUNK_OVERHEAD") ? std::atof(std::getenv("NGF_CHUNK_OVERHEAD")) : 14.0;
-    const int forced_cz = std::getenv("NGF_FUSED_CZ") ? std::atoi(std::getenv("NGF_FUSED_CZ")) : 0;
-    struct Choice {
-        double cost;
-        int variant;
-        std::vector<int> sizes;
-    };
-    std::vector<Choice> choices;
-    for (int v : cand) {
-        int ty, nth;
-        fused_variant_geom(v, &ty, &nth);
-        std::vector<int> a, b;
-        const int wx = tile_windows(p->h_i0[0], nx, ndx, kTX, 1, a, b);
-        const int ntx = (int)a.size();
-        const int wy = tile_windows(p->h_i0[1], ny, ndy, ty, 1, a, b);
-        const int nty = (int)a.size();
-        if (fused_smem<T>(v, wx, wy) > size_t(220) * 1024) continue;
-        const int64_t cols = (int64_t)ntx * nty, slots = (int64_t)kSMs * kMinBlocks[v];
-        auto add = [&](std::vector<int> sizes) {
-            std::vector<std::pair<int64_t, double>> cls;
-            for (int s : sizes) cls.push_back({cols, (s + ovh) * kPlaneCost[v]});
-            choices.push_back({list_schedule(cls, slots), v, std::move(sizes)});
-        };
-        for (int B = std::min(nzs, kCzMax); B >= 1; --B) {
-            if (forced_cz > 0 && B != std::min(forced_cz, nzs)) continue;
-            // big-chunk counts that leave less than ~3 big chunks for the remainder
-            for (int nb = std::max(1, nzs / B - 2); nb * B <= nzs; ++nb) {
-                const int r = nzs - nb * B;
-                std::vector<int> big(nb, B);
-                if (r == 0) {
-                    add(big);
-                    continue;
-                }
-                if (forced_cz > 0) {  // uniform chunks of the forced size
-                    if (nb == nzs / B) {
-                        big.push_back(r);
-                        add(big);
-                    }
-                    continue;
-                }
-                for (int div = 1; div <= 4; ++div) {  // remainder in m chunks of <= B / div
-                    const int cap = std::max(1, B / div);
-                    const int m = (r + cap - 1) / cap;
-                    std::vector<int> sizes = big;
-                    for (int i = 0; i < m; ++i) sizes.push_back(r / m + (i < r % m ? 1 : 0));
-                    std::sort(sizes.begin() + nb, sizes.end(), std::greater<int>());
-                    add(sizes);
-                }
-            }
+    // the search depends only on the geometry (dims, slab, index maps), the dtype and the
+    // tuning overrides: memoised per process, so repeated registrations of one size (a
+    // batch of pairs, config 4) skip it (1.4 ms at 256^3, 4.9 ms at 512^3)
+    std::string key;
+    {
+        const char* ev[] = {"NGF_FUSED_VARIANT", "NGF_FUSED_CZ", "NGF_CHUNK_OVERHEAD"};
+        key = std::to_string(sizeof(T)) + ":" + std::to_string(zlo) + ":" + std::to_string(zhi);
+        for (const char* e : ev) key += std::string(":") + (std::getenv(e) ? std::getenv(e) : "-");
+        const int nimg[3] = {nx, ny, nz}, ndef[3] = {ndx, ndy, ndz};
+        for (int ax = 0; ax < 3; ++ax) {
+            key += "|" + std::to_string(nimg[ax]) + "/" + std::to_string(ndef[ax]) + ":";
+            uint64_t h = 1469598103934665603ull;  // FNV-1a of the axis index map
+            for (int i = 0; i < nimg[ax]; ++i) h = (h ^ (uint32_t)p->h_i0[ax][i]) * 1099511628211ull;
+            key += std::to_string(h);
         }
     }
-    std::stable_sort(choices.begin(), choices.end(),
-                     [](const Choice& x, const Choice& y) { return x.cost < y.cost; });
     std::vector<int> bounds;
     int variant = -1;
-    // cheapest valid chunking; first among those whose def planes are covered by at most 4
-    // chunks (k_post's unrolled partial sum -- more covers take its serial loop, which at
-    // small sizes costs more than the march gains from the extra chunks)
-    for (const int limit : {4, kCover}) {
-        for (const Choice& ch : choices) {
-            std::vector<int> bd(1, zlo), a, b;
-            for (int s : ch.sizes) bd.push_back(bd.back() + s);
-            chunk_windows(p->h_i0[2], nz, ndz, bd, a, b);
-            std::vector<int32_t> cov;
-            if (build_cover(a, b, ndz, cov, limit)) {
-                bounds = bd;
-                variant = ch.variant;
-                break;
+    size_t n_choices = 0;
+    static std::mutex plan_mu;
+    static std::map<std::string, std::pair<int, std::vector<int>>> plan_cache;
+    {
+        std::lock_guard<std::mutex> lk(plan_mu);
+        auto it = plan_cache.find(key);
+        if (it != plan_cache.end()) {
+            variant = it->second.first;
+            bounds = it->second.second;
+        }
+    }
+    if (variant < 0) {
+        std::vector<int> cand;
+        const char* env = std::getenv("NGF_FUSED_VARIANT");
+        if (sizeof(T) == 8) {  // f64 shapes: 0, 4, 5
+            const int v = env ? std::atoi(env) : -1;
+            cand = (v == 0 || v == 4 || v == 5) ? std::vector<int>{v} : std::vector<int>{4, 5};
+        } else if (env) {
+            const int v = std::atoi(env) % 6;  // f32 shapes: 0 .. 5
+            cand = {v};
+        } else {
+            cand = {1, 2};
+        }
+        const int nzs = zhi - zlo;
+        const double ovh = std::getenv("NGF_CHUNK_OVERHEAD") ? std::atof(std::getenv("NGF_CHUNK_OVERHEAD")) : 14.0;
+        const int forced_cz = std::getenv("NGF_FUSED_CZ") ? std::atoi(std::getenv("NGF_FUSED_CZ")) : 0;
+        struct Choice {
+            double cost;
+            int variant;
+            std::vector<int> sizes;
+        };
+        std::vector<Choice> choices;
+        for (int v : cand) {
+            int ty, nth;
+            fused_variant_geom(v, &ty, &nth);
+            std::vector<int> a, b;
+            const int wx = tile_windows(p->h_i0[0], nx, ndx, kTX, 1, a, b);
+            const int ntx = (int)a.size();
+            const int wy = tile_windows(p->h_i0[1], ny, ndy, ty, 1, a, b);
+            const int nty = (int)a.size();
+            if (fused_smem<T>(v, wx, wy) > size_t(220) * 1024) continue;
+            const int64_t cols = (int64_t)ntx * nty, slots = (int64_t)kSMs * kMinBlocks[v];
+            auto add = [&](std::vector<int> sizes) {
+                std::vector<std::pair<int64_t, double>> cls;
+                for (int s : sizes) cls.push_back({cols, (s + ovh) * kPlaneCost[v]});
+                choices.push_back({list_schedule(cls, slots), v, std::move(sizes)});
+            };
+            for (int B = std::min(nzs, kCzMax); B >= 1; --B) {
+                if (forced_cz > 0 && B != std::min(forced_cz, nzs)) continue;
+                // big-chunk counts that leave less than ~3 big chunks for the remainder
+                for (int nb = std::max(1, nzs / B - 2); nb * B <= nzs; ++nb) {
+                    const int r = nzs - nb * B;
+                    std::vector<int> big(nb, B);
+                    if (r == 0) {
+                        add(big);
+                        continue;
+                    }
+                    if (forced_cz > 0) {  // uniform chunks of the forced size
+                        if (nb == nzs / B) {
+                            big.push_back(r);
+                            add(big);
+                        }
+                        continue;
+                    }
+                    for (int div = 1; div <= 4; ++div) {  // remainder in m chunks of <= B / div
+                        const int cap = std::max(1, B / div);
+                        const int m = (r + cap - 1) / cap;
+                        std::vector<int> sizes = big;
+                        for (int i = 0; i < m; ++i) sizes.push_back(r / m + (i < r % m ? 1 : 0));
+                        std::sort(sizes.begin() + nb, sizes.end(), std::greater<int>());
+                        add(sizes);
+                    }
+                }
             }
         }
-        if (variant >= 0) break;
+        std::stable_sort(choices.begin(), choices.end(),
+                         [](const Choice& x, const Choice& y) { return x.cost < y.cost; });
+        // cheapest valid chunking; first among those whose def planes are covered by at most 4
+        // chunks (k_post's unrolled partial sum -- more covers take its serial loop, which at
+        // small sizes costs more than the march gains from the extra chunks)
+        for (const int limit : {4, kCover}) {
+            for (const Choice& ch : choices) {
+                std::vector<int> bd(1, zlo), a, b;
+                for (int s : ch.sizes) bd.push_back(bd.back() + s);
+                chunk_windows(p->h_i0[2], nz, ndz, bd, a, b);
+                std::vector<int32_t> cov;
+                if (build_cover(a, b, ndz, cov, limit)) {
+                    bounds = bd;
+                    variant = ch.variant;
+                    break;
+                }
+            }
+            if (variant >= 0) break;
+        }
+        n_choices = choices.size();
+        if (variant >= 0) {
+            std::lock_guard<std::mutex> lk(plan_mu);
+            plan_cache[key] = {variant, bounds};
+        }
     }
     if (variant < 0) return NGF_EARG;
+    const auto t_plan = std::chrono::steady_clock::now();
     fp.variant = variant;
     // two-slot float2 march: opt-in (measured 388 us vs 375 us for the scalar march at
     // 256^3 -- the FP issue slots it saves are spent on pair formation and masking)
@@ -342,6 +382,12 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     NGF_CUDA((cudaError_t)dev_alloc((void**)&L->dpart, (size_t)fp.n_cta * sizeof(double)));
     L->ns = (int)(((L->def.dims[0] + 31) / 32) * ((L->def.dims[1] + 7) / 8) * 3 * L->def.dims[2]);
     NGF_CUDA((cudaError_t)dev_alloc((void**)&L->spart, (size_t)L->ns * sizeof(double)));
+    if (std::getenv("NGF_SETUP_DEBUG")) {
+        const auto t_end = std::chrono::steady_clock::now();
+        std::fprintf(stderr, "fused_setup %dx%dx%d: plan search %.3f ms (%zu choices; 0 = cached), tables+upload %.3f ms\n",
+                     nx, ny, nz, std::chrono::duration<double, std::milli>(t_plan - t_start).count(),
+                     n_choices, std::chrono::duration<double, std::milli>(t_end - t_plan).count());
+    }
     return fused_prepare<T>(variant, fp.smem_bytes);
 }
 
