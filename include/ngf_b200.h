@@ -145,8 +145,10 @@ int ngf_level_eval_host(ngf_level_t* level, const void* y_host, void* grad_host,
                         double* scalars_host, int mode, void* stream);
 /* Host <-> device copies staged through page-locked memory by the library's copy threads
  * (a pageable cudaMemcpy runs at a fraction of the PCIe bandwidth).  ngf_host_upload is
- * stream-ordered and returns once src_host may be reused; ngf_host_download returns once
- * dst_host holds the data (it synchronises the stream). */
+ * stream-ordered; a pageable src_host may be reused when it returns, a page-locked one is
+ * copied by a direct asynchronous DMA and must stay unchanged until the stream has passed
+ * the copy (cudaMemcpyAsync semantics).  ngf_host_download returns once dst_host holds
+ * the data (it synchronises the stream). */
 int ngf_host_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 int ngf_host_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
 /* Config-5 z-slab decomposition: restrict the fused evaluation to image

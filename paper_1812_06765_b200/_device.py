@@ -80,6 +80,15 @@ def _upload_staged(t, arr: np.ndarray):
     return out
 
 
+def pinned_empty(shape, dtype) -> np.ndarray:
+    """A numpy array in page-locked host memory (torch's caching host allocator) when a GPU
+    is present, so its uploads are direct DMAs; plain numpy memory otherwise."""
+    t = torch()
+    if t.cuda.is_available():
+        return t.empty(tuple(shape), dtype=torch_dtype(dtype), pin_memory=True).numpy()
+    return np.empty(shape, dtype)
+
+
 def empty(shape, dtype):
     t = require_cuda()
     return t.empty(tuple(shape), dtype=torch_dtype(dtype), device="cuda")
