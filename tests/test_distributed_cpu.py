@@ -35,6 +35,7 @@ class OracleSlab:
 
     def __init__(self, gi, gd, R, T, zlo, zhi, tau=10.0, rho=10.0, alpha=1.0):
         self.gi, self.gd, self.T, self.zlo, self.zhi = gi, gd, T, zlo, zhi
+        self.image_grid, self.def_grid = gi, gd
         self.tau, self.rho, self.alpha = tau, rho, alpha
         self.gR, self.nR = O.ref_terms(R, gi, rho)
 
@@ -63,14 +64,14 @@ class OracleSlab:
         scal[2] = S
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, exchange="planes"):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         gi, gd, R, T, y = _problem()
         zlo, zhi = slab_ranges(gi.dims[2], gd.dims[2], world)[rank]
-        obj = SlabObjective(OracleSlab(gi, gd, R, T, zlo, zhi))
+        obj = SlabObjective(OracleSlab(gi, gd, R, T, zlo, zhi), exchange=exchange)
         x = torch.from_numpy(y.ravel().copy())
         g = torch.zeros_like(x)
         sc = torch.zeros(3, dtype=torch.float64)
@@ -86,23 +87,43 @@ def _free_port():
         return s.getsockname()[1]
 
 
-def test_slab_decomposition_gloo_world2():
-    world = 2
+def _run(world, exchange):
     with mp.Manager() as mgr:
         out = mgr.dict()
-        mp.start_processes(_worker, args=(world, _free_port(), out), nprocs=world, join=True,
+        mp.start_processes(_worker, args=(world, _free_port(), out, exchange), nprocs=world, join=True,
                            start_method="spawn")
-        res = dict(out)
+        return dict(out)
+
+
+@pytest.mark.parametrize("world,exchange", [(2, "planes"), (2, "allreduce"), (3, "planes")])
+def test_slab_decomposition_gloo(world, exchange):
+    res = _run(world, exchange)
     gi, gd, R, T, y = _problem()
     J, g = O.Objective(T, R, gd, gi)(y.ravel())
     slabs = [res[r][2] for r in range(world)]
-    assert slabs[0][0] == 0 and slabs[-1][1] == gi.dims[2] and slabs[0][1] == slabs[1][0]
+    assert slabs[0][0] == 0 and slabs[-1][1] == gi.dims[2]
+    assert all(slabs[r][1] == slabs[r + 1][0] for r in range(world - 1))
     for r in range(world):
         sc, gr, _ = res[r]
         assert abs(sc[0] - J) <= 1e-12 * abs(J)
         assert np.max(np.abs(gr - g)) <= 1e-11 * np.abs(g).max()
     # every rank holds the same result (replicated L-BFGS stays in lock-step)
-    assert np.array_equal(res[0][1], res[1][1]) and np.array_equal(res[0][0], res[1][0])
+    for r in range(1, world):
+        assert np.array_equal(res[0][1], res[r][1]) and np.array_equal(res[0][0], res[r][0])
+
+
+def test_slab_plane_layout_partitions_and_covers():
+    from paper_1812_06765_b200.distributed import slab_plane_layout
+
+    gi = O.grid((64, 64, 512), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    gd = O.def_grid_for(gi, 4)
+    slabs = slab_ranges(512, gd.dims[2], 8)
+    windows, owned = slab_plane_layout(gi, gd, slabs)
+    assert owned[0][0] == 0 and owned[-1][1] == gd.dims[2]
+    assert all(owned[r][1] == owned[r + 1][0] for r in range(7))
+    for (lo, hi), (wlo, whi) in zip(owned, windows):
+        assert wlo <= lo and hi - 1 <= whi          # a rank's window covers its owned planes
+        assert whi - wlo + 1 <= (hi - lo) + 4       # plus at most a couple of halo planes
 
 
 def test_slab_ranges_align_to_deformation_cells():
