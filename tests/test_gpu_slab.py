@@ -9,7 +9,8 @@ pytestmark = pytest.mark.gpu
 
 import paper_1812_06765_b200 as ngf  # noqa: E402
 from oracle import ngf_oracle as O  # noqa: E402
-from paper_1812_06765_b200.distributed import DeviceSlab, SlabObjective, slab_ranges  # noqa: E402
+from paper_1812_06765_b200.distributed import (DeviceSlab, SlabObjective, slab_plane_layout,  # noqa: E402
+                                                slab_ranges)
 
 
 @pytest.mark.parametrize("dims,ratio,world", [((64, 48, 40), 4, 2), ((48, 40, 37), 4, 3),
@@ -31,12 +32,17 @@ def test_slab_partials_sum_to_full(dims, ratio, world):
     gsum = torch.zeros_like(x)
     dsum = 0.0
     last = None
-    for zlo, zhi in slab_ranges(gi.dims[2], gd.dims[2], world):
+    slabs = slab_ranges(gi.dims[2], gd.dims[2], world)
+    windows, _ = slab_plane_layout(gi, gd, slabs)
+    for (zlo, zhi), (wlo, whi) in zip(slabs, windows):
         obj = ngf.LevelObjective.from_device(Td, Rd, plan, ngf.NgfParams(), 1.0)
         slab = DeviceSlab(obj.level, zlo, zhi)
         g = torch.empty_like(x)
         sc = torch.zeros(3, dtype=torch.float64, device="cuda")
         slab.partial(x, g, sc)
+        # the plane exchange (SlabObjective) relies on the partial living in its window
+        gp = g.view(3, gd.dims[2], -1)
+        assert not torch.any(gp[:, :wlo]) and not torch.any(gp[:, whi + 1:]), (zlo, zhi, wlo, whi)
         gsum += g
         dsum += float(sc[1].item())
         last = slab
