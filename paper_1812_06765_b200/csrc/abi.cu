@@ -149,8 +149,17 @@ int ngf_downsample(const ngf_grid_t* g, int dtype, const void* in, void* out, vo
 
 int ngf_prolong(const ngf_plan_t* p, int dtype, const void* yc, void* yf, void* stream) {
     if (!p || !yc || !yf) return NGF_EARG;
-    NGF_DISPATCH(dtype, prolong_impl<float>(p, (const float*)yc, (float*)yf, as_stream(stream)),
-                 prolong_impl<double>(p, (const double*)yc, (double*)yf, as_stream(stream)));
+    ngf_plan_t* mp = const_cast<ngf_plan_t*>(p);
+    if (!mp->done) NGF_CUDA(cudaEventCreateWithFlags(&mp->done, cudaEventDisableTiming));
+    int rc;
+    if (dtype == NGF_F32)
+        rc = prolong_impl<float>(p, (const float*)yc, (float*)yf, as_stream(stream));
+    else if (dtype == NGF_F64)
+        rc = prolong_impl<double>(p, (const double*)yc, (double*)yf, as_stream(stream));
+    else
+        return NGF_EARG;
+    record_done(mp->done, as_stream(stream));
+    return rc;
 }
 
 }  // extern "C"

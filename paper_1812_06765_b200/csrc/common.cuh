@@ -150,4 +150,19 @@ struct ngf_plan {
     // workspace for P^T (x/y stage result, 3 * nz_img * ny_def * nx_def doubles)
     void* d_tmp;
     size_t tmp_bytes;
+    // completion of the plan's last launch (ngf_prolong), so destroying it waits for that
+    // work only, not the whole device (concurrent registrations); `idle` is set by an
+    // owner that has already waited (the level)
+    cudaEvent_t done;
+    int idle;
 };
+
+namespace ngf {
+// record `ev` on `s` unless `s` is being captured (event records are not allowed in
+// conditional graph bodies, and a captured launch completes with the graph)
+inline void record_done(cudaEvent_t ev, cudaStream_t s) {
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(s, &cap) == cudaSuccess && cap == cudaStreamCaptureStatusNone)
+        cudaEventRecord(ev, s);
+}
+}  // namespace ngf

@@ -10,6 +10,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdlib>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -28,14 +29,17 @@ struct Scratch {
     unsigned int* counter = nullptr;  // last-block counter
 };
 
+// One scratch (block partials + last-block counter) per (device, stream): the reductions'
+// last-block pattern shares it between launches, so launches on different streams (e.g.
+// concurrent registrations) must not share one.
 static std::mutex g_scr_mu;
-static Scratch g_scr[64];
+static std::map<std::pair<int, cudaStream_t>, Scratch> g_scr;
 
-static Scratch* scratch() {
+static Scratch* scratch(cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     std::lock_guard<std::mutex> lk(g_scr_mu);
-    Scratch& s = g_scr[dev & 63];
+    Scratch& s = g_scr[{dev, st}];
     if (!s.parts) {
         if (cudaMalloc(&s.parts, 2 * kRedBlocks * kNStat * sizeof(double)) != cudaSuccess) return nullptr;
         if (cudaMalloc(&s.counter, 64) != cudaSuccess) return nullptr;
@@ -571,7 +575,7 @@ template <typename T>
 int two_loop_impl(const void* const* S, const void* const* Y, const double* rho, double gamma, int m,
                   const void* g, void* d, int64_t n, double* slope, cudaStream_t s) {
     if (m < 0 || m > kMaxMem) return NGF_EARG;
-    Scratch* sc = scratch();
+    Scratch* sc = scratch(s);
     if (!sc) return NGF_ENOMEM;
     TwoLoopArgs<T> a;
     for (int k = 0; k < m; ++k) {
@@ -651,8 +655,8 @@ int two_loop_dev_launch(const TwoLoopArgs<T>* ap, int64_t n, cudaStream_t s) {
 
 template <typename T>
 int pair_dev_launch(const T* xn, const T* x, const T* gn, const T* g, T* const* s_ptr, T* const* y_ptr,
-                    int64_t n, double* out, cudaStream_t s) {
-    Scratch* sc = scratch();
+                    int64_t n, double* out, cudaStream_t s, cudaStream_t owner) {
+    Scratch* sc = scratch(owner);
     if (!sc) return NGF_ENOMEM;
     NGF_LAUNCH(k_pair_ind<T>, kRedBlocks, kRedThreads, 0, s, xn, x, gn, g, s_ptr, y_ptr, n, sc->parts,
                sc->counter, out);
@@ -667,17 +671,18 @@ int axpy_dev_launch(const T* x, const double* t, const T* d, T* out, int64_t n, 
     return 0;
 }
 
-double* lbfgs_parts() {
-    Scratch* sc = scratch();
+double* lbfgs_parts(cudaStream_t owner) {
+    Scratch* sc = scratch(owner);
     return sc ? sc->parts : nullptr;
 }
 
 template int two_loop_dev_launch<float>(const TwoLoopArgs<float>*, int64_t, cudaStream_t);
 template int two_loop_dev_launch<double>(const TwoLoopArgs<double>*, int64_t, cudaStream_t);
 template int pair_dev_launch<float>(const float*, const float*, const float*, const float*, float* const*,
-                                    float* const*, int64_t, double*, cudaStream_t);
+                                    float* const*, int64_t, double*, cudaStream_t, cudaStream_t);
 template int pair_dev_launch<double>(const double*, const double*, const double*, const double*,
-                                     double* const*, double* const*, int64_t, double*, cudaStream_t);
+                                     double* const*, double* const*, int64_t, double*, cudaStream_t,
+                                     cudaStream_t);
 template int axpy_dev_launch<float>(const float*, const double*, const float*, float*, int64_t, cudaStream_t);
 template int axpy_dev_launch<double>(const double*, const double*, const double*, double*, int64_t,
                                      cudaStream_t);
@@ -696,9 +701,9 @@ int ngf_vec_dot(int dtype, const void* a, const void* b, int64_t n, double* out_
 int ngf_vec_stats(int dtype, const void* g, const void* d, const void* s, const void* y, int64_t n,
                   double* out_dev, void* stream) {
     if (!out_dev || n < 0) return NGF_EARG;
-    Scratch* sc = scratch();
-    if (!sc) return NGF_ENOMEM;
     cudaStream_t st = as_stream(stream);
+    Scratch* sc = scratch(st);
+    if (!sc) return NGF_ENOMEM;
     if (dtype == NGF_F32)
         NGF_LAUNCH(k_stats<float>, kRedBlocks, kRedThreads, 0, st, (const float*)g, (const float*)d,
                    (const float*)s, (const float*)y, n, sc->parts, sc->counter, out_dev);
@@ -745,9 +750,9 @@ int ngf_vec_sub(int dtype, const void* a, const void* b, void* out, int64_t n, v
 int ngf_lbfgs_pair(int dtype, const void* x_new, const void* x, const void* g_new, const void* g,
                    void* s_out, void* y_out, int64_t n, double* out_dev, void* stream) {
     if (!x_new || !x || !g_new || !g || !s_out || !y_out || !out_dev || n < 0) return NGF_EARG;
-    Scratch* sc = scratch();
-    if (!sc) return NGF_ENOMEM;
     cudaStream_t st = as_stream(stream);
+    Scratch* sc = scratch(st);
+    if (!sc) return NGF_ENOMEM;
     if (dtype == NGF_F32)
         NGF_LAUNCH(k_pair<float>, kRedBlocks, kRedThreads, 0, st, (const float*)x_new, (const float*)x,
                    (const float*)g_new, (const float*)g, (float*)s_out, (float*)y_out, n, sc->parts,

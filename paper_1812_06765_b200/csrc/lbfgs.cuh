@@ -33,12 +33,14 @@ constexpr int64_t kTwoLoopClusterMaxN = 16 * 512 * 16;
 // the pair kernel writes to *s_ptr / *y_ptr, the step reads *t.
 template <typename T>
 int two_loop_dev_launch(const TwoLoopArgs<T>* args, int64_t n, cudaStream_t s);
+// (the pair kernel's reduction scratch belongs to `owner`, the stream the graph runs on)
 template <typename T>
 int pair_dev_launch(const T* xn, const T* x, const T* gn, const T* g, T* const* s_ptr, T* const* y_ptr,
-                    int64_t n, double* out, cudaStream_t s);
+                    int64_t n, double* out, cudaStream_t s, cudaStream_t owner);
 template <typename T>
 int axpy_dev_launch(const T* x, const double* t, const T* d, T* out, int64_t n, cudaStream_t s);
-// scratch partials of the reductions (allocated on first use; call before any capture)
-double* lbfgs_parts();
+// scratch partials of the reductions on `owner` (allocated on first use; call before any
+// capture)
+double* lbfgs_parts(cudaStream_t owner);
 
 }  // namespace ngf

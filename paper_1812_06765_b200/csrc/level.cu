@@ -59,6 +59,7 @@ struct ngf_level {
     void* hg;
     double* hsc;
     double* hsc_pin;
+    cudaEvent_t done;  // completion of the last launch: destroy waits for it, not the device
 };
 
 namespace ngf {
@@ -532,6 +533,10 @@ static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_g
     *out = nullptr;
     ngf_level* L = (ngf_level*)std::calloc(1, sizeof(ngf_level));
     if (!L) return NGF_ENOMEM;
+    if (cudaEventCreateWithFlags(&L->done, cudaEventDisableTiming) != cudaSuccess) {
+        std::free(L);
+        return NGF_ENOMEM;
+    }
     L->dtype = dtype;
     L->img = *img_grid;
     L->def = *def_grid;
@@ -575,6 +580,7 @@ static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_g
             if (!rc) rc = fused_setup<double>(L, 0, (int)L->img.dims[2]);
         }
     }
+    record_done(L->done, s);  // the creation kernels (reference terms, packing)
     if (rc) {
         ngf_level_destroy(L);
         return rc;
@@ -600,11 +606,19 @@ int ngf_level_create_terms(const ngf_grid_t* img_grid, const ngf_grid_t* def_gri
 
 void ngf_level_destroy(ngf_level_t* L) {
     if (!L) return;
-    if (L->plan) ngf_plan_destroy(L->plan);
+    // no kernel may still use the level's buffers: wait for its last launch
+    if (!L->done || cudaEventSynchronize(L->done) != cudaSuccess) {
+        cudaGetLastError();
+        cudaDeviceSynchronize();
+    }
+    if (L->done) cudaEventDestroy(L->done);
+    if (L->plan) {
+        L->plan->idle = 1;
+        ngf_plan_destroy(L->plan);
+    }
     void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart,
                     L->ex.yhat, L->ex.W, L->ex.terms, L->ex.q, L->ex.s, L->ex.ghat, L->ex.gD,
                     L->ex.cws, L->ex.dws, L->hx, L->hg, L->hsc};
-    cudaDeviceSynchronize();  // no kernel may still use them
     for (void* b : bufs) dev_free(b);
     if (L->hsc_pin) cudaFreeHost(L->hsc_pin);
     for (int k = 0; k < 2; ++k)
@@ -616,12 +630,17 @@ int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_de
                    void* stream) {
     if (!L || !y || !grad || !scalars_dev) return NGF_EARG;
     cudaStream_t s = as_stream(stream);
+    int rc;
     if (mode == 1) {
-        return L->dtype == NGF_F32 ? eval_exact<float>(L, y, grad, scalars_dev, s)
-                                   : eval_exact<double>(L, y, grad, scalars_dev, s);
+        rc = L->dtype == NGF_F32 ? eval_exact<float>(L, y, grad, scalars_dev, s)
+                                 : eval_exact<double>(L, y, grad, scalars_dev, s);
+    } else if (mode == 0 || mode == 2) {
+        rc = fused_part(L, y, grad, scalars_dev, s, mode == 2 ? 1 : 0);
+    } else {
+        return NGF_EARG;
     }
-    if (mode != 0 && mode != 2) return NGF_EARG;
-    return fused_part(L, y, grad, scalars_dev, s, mode == 2 ? 1 : 0);
+    record_done(L->done, s);
+    return rc;
 }
 
 int ngf_level_eval_host(ngf_level_t* L, const void* y_host, void* grad_host, double* scalars_host,
@@ -647,7 +666,9 @@ int ngf_level_eval_host(ngf_level_t* L, const void* y_host, void* grad_host, dou
 int ngf_level_add_curvature(ngf_level_t* L, const void* y, void* grad, double* scalars_dev,
                             void* stream) {
     if (!L || !y || !grad || !scalars_dev) return NGF_EARG;
-    return fused_part(L, y, grad, scalars_dev, as_stream(stream), 2);
+    const int rc = fused_part(L, y, grad, scalars_dev, as_stream(stream), 2);
+    record_done(L->done, as_stream(stream));
+    return rc;
 }
 
 int ngf_level_set_zrange(ngf_level_t* L, int64_t zlo, int64_t zhi) {

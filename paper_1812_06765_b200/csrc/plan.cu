@@ -222,7 +222,13 @@ void ngf_plan_destroy(ngf_plan_t* p) {
         std::free(p->h_counts[k]);
         std::free(p->h_w[k]);
     }
-    if (p->d_blob || p->d_tmp) cudaDeviceSynchronize();  // no kernel may still use them
+    if ((p->d_blob || p->d_tmp) && !p->idle) {  // no kernel may still use them
+        if (!p->done || cudaEventSynchronize(p->done) != cudaSuccess) {
+            cudaGetLastError();
+            cudaDeviceSynchronize();
+        }
+    }
+    if (p->done) cudaEventDestroy(p->done);
     ngf::dev_free(p->d_blob);
     ngf::dev_free(p->d_tmp);
     std::free(p);

@@ -316,7 +316,7 @@ int run_level_graph(ngf_level_t* level, int exact, T* x, T* g, T* d, T* xn, T* g
     int rc = 0;
     launched = false;
     if (n > kTwoLoopClusterMaxN || cfg->memory + 1 > kSlots) return NGF_EARG;
-    double* parts = lbfgs_parts();
+    double* parts = lbfgs_parts(s);
     if (!parts) return NGF_ENOMEM;
     auto alloc = [&](size_t bytes) -> void* {
         void* p = nullptr;
@@ -449,7 +449,7 @@ int run_level_graph(ngf_level_t* level, int exact, T* x, T* g, T* d, T* xn, T* g
                 return (int)cudaGetLastError();
             }));
             NGF_LAUNCH(k_ctl_pair_pre<T>, 1, 1, 0, c1, dst);
-            GRUN(pair_dev_launch<T>(xn, x, gn, g, &dst->cur_s, &dst->cur_y, n, stats, c1));
+            GRUN(pair_dev_launch<T>(xn, x, gn, g, &dst->cur_s, &dst->cur_y, n, stats, c1, s));
             NGF_LAUNCH(k_ctl_end<T>, 1, 1, 0, c1, dst);
             NGF_CUDA(cudaMemcpyAsync(x, xn, vb, cudaMemcpyDeviceToDevice, c1));
             NGF_CUDA(cudaMemcpyAsync(g, gn, vb, cudaMemcpyDeviceToDevice, c1));
