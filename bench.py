@@ -53,7 +53,7 @@ def parse():
                     help="working dtype (the reference's default precision is f64, multilevel.py:55)")
     ap.add_argument("--no-register", action="store_true", help="skip the full-registration leg")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU baseline work")
-    ap.add_argument("--streams", type=int, default=1,
+    ap.add_argument("--streams", type=int, default=4,
                     help="config 4: registrations in flight per GPU (host threads, one CUDA stream each)")
     ap.add_argument("--pairs", type=int, default=0,
                     help="config 4: also register this many independent pairs, split over the ranks "

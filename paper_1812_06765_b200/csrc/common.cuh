@@ -130,7 +130,12 @@ template <> inline const double* w1_host_sel<double>(const AxisDev& a) { return 
 
 struct ngf_plan;
 namespace ngf {
-int plan_upload(ngf_plan* p);  // lazily create the plan's device arrays (plan.cu)
+int plan_upload(ngf_plan* p);
+// Copy host -> device and wait until the bytes have LANDED.  A plain cudaMemcpy from
+// pageable memory returns once the data is staged, with the DMA still queued on the
+// legacy stream, which the (non-blocking) work streams do not wait for: a kernel on
+// another stream could read the destination before it is written.
+int upload_blocking(void* dst, const void* src, size_t bytes);  // lazily create the plan's device arrays (plan.cu)
 }
 
 // Opaque handle layouts (host side).

@@ -26,6 +26,7 @@
 
 #pragma once
 #include <cstdlib>
+#include <mutex>
 #include <type_traits>
 
 #include "fused_cfg.cuh"
@@ -613,8 +614,15 @@ static cudaError_t smem_attr(K kernel, size_t smem) {
     return cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
+// The dynamic shared memory limit is a per-kernel attribute shared by every level and
+// thread: it is only ever raised (levels of different sizes are created concurrently by
+// registrations on other streams, and a lowered limit would fail their launches).
 template <typename T, typename C>
 int march_prepare(size_t smem) {
+    static std::mutex mu;
+    static size_t granted = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (smem <= granted) return 0;
     cudaError_t e = smem_attr(k_eval_fused<T, C, true, false>, smem);
     if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, false, false>, smem);
     if (e == cudaSuccess) e = smem_attr(k_eval_fused<T, C, true, true>, smem);
@@ -625,6 +633,7 @@ int march_prepare(size_t smem) {
         if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, true, true>, smem);
         if (e == cudaSuccess) e = smem_attr(k_eval_pair<C, false, true>, smem);
     }
+    if (e == cudaSuccess) granted = smem;
     return (int)e;
 }
 

@@ -520,11 +520,10 @@ int launch_rv(const TwoLoopArgs<T>& a, int C, bool grid, cudaStream_t s) {
                                              dim3(kRvThreads), args, 0, s));
         return 0;
     }
-    static bool attr = false;
-    if (!attr) {
-        NGF_CUDA(cudaFuncSetAttribute(k_two_loop_rv<T, VPT, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    // once per instantiation (thread-safe static initialisation)
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k_two_loop_rv<T, VPT, false>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    NGF_CUDA(attr);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kRvThreads);
@@ -617,11 +616,9 @@ static void rv_shape(int64_t n, int& C, int& vpt) {
 
 template <typename T, int VPT>
 static int launch_rv_ind(const TwoLoopArgs<T>* ap, int C, cudaStream_t s) {
-    static bool attr = false;
-    if (!attr) {
-        NGF_CUDA(cudaFuncSetAttribute(k_two_loop_rv_ind<T, VPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        attr = true;
-    }
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(k_two_loop_rv_ind<T, VPT>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    NGF_CUDA(attr);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(C);
     cfg.blockDim = dim3(kRvThreads);

@@ -365,7 +365,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
            o_cz = appv(cz_), o_zb = appv(zbv), o_xcsr = appv(xcsr), o_ycsr = appv(ycsr),
            o_xcw = app(xcw.data(), xcw.size() * sizeof(T)), o_ycw = app(ycw.data(), ycw.size() * sizeof(T));
     NGF_CUDA((cudaError_t)dev_alloc((void**)&L->fp_blob, blob.size() * 4));
-    NGF_CUDA(cudaMemcpy(L->fp_blob, blob.data(), blob.size() * 4, cudaMemcpyHostToDevice));
+    NGF_CUDA((cudaError_t)upload_blocking(L->fp_blob, blob.data(), blob.size() * 4));
     const int32_t* b = (const int32_t*)L->fp_blob;
     fp.win_x = b + o_wx;
     fp.win_y = b + o_wy;

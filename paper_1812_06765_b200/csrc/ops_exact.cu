@@ -553,11 +553,11 @@ static int build_pw(int64_t off, int64_t n, PwProgram& P, int& height) {
 }
 
 static std::mutex g_pw_mu;
-static std::map<int64_t, PwProgram*> g_pw_cache;
+static std::map<std::pair<int64_t, cudaStream_t>, PwProgram*> g_pw_cache;
 
-static PwProgram* get_pw(int64_t n) {
+static PwProgram* get_pw(int64_t n, cudaStream_t s) {
     std::lock_guard<std::mutex> lk(g_pw_mu);
-    auto it = g_pw_cache.find(n);
+    auto it = g_pw_cache.find({n, s});
     if (it != g_pw_cache.end()) return it->second;
     PwProgram* P = new PwProgram();
     int h;
@@ -573,14 +573,17 @@ static PwProgram* get_pw(int64_t n) {
         delete P;
         return nullptr;
     }
-    cudaMemcpy(P->d_nodes, P->nodes.data(), P->nodes.size() * sizeof(PwNode), cudaMemcpyHostToDevice);
-    cudaMemcpy(P->d_ids, flat.data(), flat.size() * 4, cudaMemcpyHostToDevice);
-    g_pw_cache[n] = P;
+    if (upload_blocking(P->d_nodes, P->nodes.data(), P->nodes.size() * sizeof(PwNode)) ||
+        upload_blocking(P->d_ids, flat.data(), flat.size() * 4)) {
+        delete P;
+        return nullptr;
+    }
+    g_pw_cache[{n, s}] = P;
     return P;
 }
 
-// NOTE: the cached program's value buffer is shared per n; calls are stream-ordered,
-// callers on different streams with the same n must not overlap (one ctx per stream).
+// The cached program (and its value buffer) belongs to one (n, stream): calls on one
+// stream are ordered, calls on different streams use different buffers.
 template <typename T>
 int pairwise_sum_impl(const T* x, int64_t n, double* out, int mode, double scale, cudaStream_t s) {
     if (n <= 0) {
@@ -588,7 +591,7 @@ int pairwise_sum_impl(const T* x, int64_t n, double* out, int mode, double scale
         NGF_CUDA(cudaMemcpyAsync(out, &z, 8, cudaMemcpyHostToDevice, s));
         return 0;
     }
-    PwProgram* P = get_pw(n);
+    PwProgram* P = get_pw(n, s);
     if (!P) return NGF_ENOMEM;
     for (size_t h = 0; h < P->levels.size(); ++h) {
         int cnt = (int)P->levels[h].size();

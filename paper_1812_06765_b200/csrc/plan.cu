@@ -42,6 +42,12 @@ void dev_free(void* ptr) {
     if (ptr) cudaFreeAsync(ptr, 0);
 }
 
+int upload_blocking(void* dst, const void* src, size_t bytes) {
+    NGF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, 0));
+    NGF_CUDA(cudaStreamSynchronize(0));
+    return 0;
+}
+
 static bool same_extent(const ngf_grid_t& a, const ngf_grid_t& b, double tol = 1e-9) {
     for (int k = 0; k < 3; ++k) {
         double lo_a = a.origin[k] - a.spacing[k] / 2;
@@ -188,7 +194,7 @@ int plan_upload(ngf_plan_t* p) {
         a.wf = (const float*)put(wf.data(), wf.size() * 4);
         a.wd = (const double*)put(p->h_w[k], (size_t)nd * w * 8);
     }
-    if (cudaMemcpy(d_blob, host.data(), blob, cudaMemcpyHostToDevice) != cudaSuccess) {
+    if (upload_blocking(d_blob, host.data(), blob) != 0) {
         dev_free(d_blob);
         return NGF_ENOMEM;
     }

@@ -482,10 +482,11 @@ int run_level_graph(ngf_level_t* level, int exact, T* x, T* g, T* d, T* xn, T* g
     res->line_search_failed = h.ls_failed;
     res->rows = h.nrows;
     if (rows && max_rows > 0)
-        NGF_CUDA(cudaMemcpy(rows, drows, (size_t)std::min(h.nrows, max_rows) * 3 * sizeof(double),
-                            cudaMemcpyDeviceToHost));
+        NGF_CUDA(cudaMemcpyAsync(rows, drows, (size_t)std::min(h.nrows, max_rows) * 3 * sizeof(double),
+                                 cudaMemcpyDeviceToHost, s));
     if (rec && h.iter > 0)
-        NGF_CUDA(cudaMemcpy(rec, drec, (size_t)h.iter * 4 * sizeof(double), cudaMemcpyDeviceToHost));
+        NGF_CUDA(cudaMemcpyAsync(rec, drec, (size_t)h.iter * 4 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    NGF_CUDA(cudaStreamSynchronize(s));
     return 0;
 }
 

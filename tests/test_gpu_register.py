@@ -219,3 +219,43 @@ def test_native_driver_edge_cases(monkeypatch):
         assert tn.stop_reason == tp.stop_reason == reason and tn.evaluations == tp.evaluations
         assert tn.iterations == tp.iterations == 0 and tn.J_rows == tp.J_rows
         assert np.array_equal(xn, xp) and np.array_equal(xn, x0)
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_concurrent_registrations_on_streams_match_sequential(exact):
+    """Config 4 on one GPU: registrations in flight on several host threads, one CUDA
+    stream each (levels of different sizes created concurrently, per-stream reduction
+    scratch, table uploads that must land before another stream's kernels read them)
+    give bit-identical fields to the same registrations run one after another."""
+    import threading
+
+    import torch
+
+    cfg = ngf.MultilevelConfig(num_levels=3, grid_ratio=4, precision="f32", exact=exact,
+                               lbfgs=ngf.LbfgsConfig(max_iterations=8))
+    n = 64 if exact else 128
+    pairs = [ngf.ct_pair(n, seed=500 + p, dtype=np.float32)[:2] for p in range(6)]
+    ref = [ngf.register(R, T, cfg)[0].field for R, T in pairs]
+    k = 3
+    streams = [torch.cuda.Stream() for _ in range(k)]
+    out = [None] * len(pairs)
+    errors = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                for j in range(i, len(pairs), k):
+                    out[j] = ngf.register(*pairs[j], cfg)[0].field
+                streams[i].synchronize()
+        except Exception as e:  # re-raised below
+            errors.append(e)
+
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(k)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    torch.cuda.synchronize()
+    assert not errors, errors[0]
+    for o, r in zip(out, ref):
+        assert np.array_equal(o, r)

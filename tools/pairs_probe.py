@@ -19,8 +19,10 @@ import paper_1812_06765_b200 as ngf  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--pairs", type=int, default=16)
 ap.add_argument("--n", type=int, default=256)
+ap.add_argument("--streams", default="1,2,3,4,6,8")
+ap.add_argument("--levels", type=int, default=4)
 a = ap.parse_args()
-cfg = ngf.MultilevelConfig(num_levels=4, grid_ratio=4, precision="f32")
+cfg = ngf.MultilevelConfig(num_levels=a.levels, grid_ratio=4, precision="f32")
 batch = [bench.make_inputs(a.n, 4, seed=1000 + p)[:2] for p in range(a.pairs)]
 ngf.register(*batch[0], cfg)
 ref = [ngf.register(R, T, cfg)[0].field for R, T in batch]
@@ -57,5 +59,5 @@ def run(k):
           f"{', '.join(f'{p:.3f}' for p in per)}); fields bit-identical to sequential: {same}", flush=True)
 
 
-for k in (1, 2, 3, 4, 6, 8):
+for k in (int(v) for v in a.streams.split(",")):
     run(k)
