@@ -103,14 +103,15 @@ __device__ __forceinline__ void load_yplane(const FusedArgs<T>& a, const SmemL<T
     const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
     const T wx = sm.colPw[ex], wy = sm.rowPw[ey];
     const unsigned mm = (unsigned)(a.ndx * a.ndy * a.ndz);
-    const unsigned plane = (unsigned)zd * (unsigned)(a.ndx * a.ndy);
+    // 32-bit element offsets from the one 64-bit base (each load: one add and one wide
+    // multiply-add for the address, instead of a 64-bit pointer chain per row and column)
+    const unsigned o00 = (unsigned)zd * (unsigned)(a.ndx * a.ndy) + (unsigned)(y0 * a.ndx + x0);
+    const unsigned dx = (unsigned)(x1 - x0), dy = (unsigned)((y1 - y0) * a.ndx);
 #pragma unroll
     for (int k = 0; k < 3; ++k) {
-        const T* yc = a.y + (k * mm + plane);
-        const T* r0 = yc + y0 * a.ndx;
-        const T* r1 = yc + y1 * a.ndx;
-        const T X0 = lerp_exact(__ldg(r0 + x0), __ldg(r0 + x1), wx);
-        const T X1 = lerp_exact(__ldg(r1 + x0), __ldg(r1 + x1), wx);
+        const unsigned o = o00 + (unsigned)k * mm;
+        const T X0 = lerp_exact(__ldg(a.y + o), __ldg(a.y + (o + dx)), wx);
+        const T X1 = lerp_exact(__ldg(a.y + (o + dy)), __ldg(a.y + (o + dy + dx)), wx);
         out[k] = lerp_exact(X0, X1, wy);
     }
 }
