@@ -7,19 +7,31 @@ config-3 finest level: synthetic 256^3 CT-shaped pair, 64^3 deformation grid,
 NGF tau = rho = 10, alpha = 1, fp32.  `value` is whole-job evaluations/s with
 the inputs resident in HBM; `e2e` is the same metric through the numpy-facing
 LevelObjective call (H2D of y, D2H of J and the gradient inside the timed
-region).  The line also carries the full 4-level 256^3 registration time (the
-paper's headline), the fused kernel's roofline against MEASURED_PEAKS.json, the
-CPU baseline (the oracle port on this host) and the SM clocks seen.
+region).  The line also carries:
+  * `parity`: the timed evaluation's (J, grad J) against the CPU reference on the
+    same y (tolerances of the north star; the run exits 1 when they are missed);
+  * `full_registration`: the 4-level 256^3 registration time (the paper's
+    headline), its probe error against the known synthetic mapping and its final
+    field against the reference's own run (tests/golden/register_c3.npz);
+  * `registrations`: configs 1 and 2 registered on the GPU and by the CPU reference
+    on this host's cores, with the field difference (same-box parity + timing);
+  * `roofline` of the fused kernel against MEASURED_PEAKS.json, `cpu_baseline`
+    and `cpu_matrix` (workers 1 / all cores, f32 / f64), clocks.
 
-For N > 1 (torchrun), every rank registers its own pair (config 4: independent
-pairs, one per GPU, no data-path collective); timings are max over ranks.
+Multi-GPU: `--gpus N` without torchrun re-launches itself under
+torch.distributed.run (N ranks, 127.0.0.1).  Config 4 (default for N > 1): every
+rank evaluates and registers its own pairs (replicas, no data-path collective) and
+the batch of 64 pairs is split over the ranks (`config4.pairs_per_s`).  `--workload
+c5` is the strong-scaling z-slab line.  Timings are max over ranks.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -32,6 +44,8 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "256^3 full-registration time (s); obj+grad evals/s; HBM GB/s vs peak"
+TOL_J, TOL_G = 1e-4, 1e-3   # north star: J within 1e-4 relative, grad within 1e-3 relative L2
+BAR_VOXEL = 0.05            # north star: final field within 0.05 voxel (interior)
 
 WORKLOADS = {
     # name: (image n, grid ratio, levels for the full registration)
@@ -42,7 +56,7 @@ WORKLOADS = {
 }
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -51,17 +65,26 @@ def parse():
     ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS))
     ap.add_argument("--precision", default="f32", choices=["f32", "f64"],
                     help="working dtype (the reference's default precision is f64, multilevel.py:55)")
-    ap.add_argument("--no-register", action="store_true", help="skip the full-registration leg")
+    ap.add_argument("--no-register", action="store_true", help="skip the registration legs")
     ap.add_argument("--cpu-budget", type=float, default=25.0, help="seconds of CPU baseline work")
+    ap.add_argument("--cpu-full", dest="cpu_full", action="store_true", default=None,
+                    help="also time the CPU matrix (workers 1/all, f32/f64) and the config 1/2 "
+                         "registrations on the host (default: on for N = 1)")
+    ap.add_argument("--no-cpu-full", dest="cpu_full", action="store_false")
     ap.add_argument("--streams", type=int, default=8,
                     help="config 4: registrations in flight per GPU (host threads, one CUDA stream each)")
     ap.add_argument("--pairs-pageable", action="store_true",
-                    help="config 4: keep the batch's volumes in pageable host memory (default: "
-                         "page-locked, as the CLI reads them)")
-    ap.add_argument("--pairs", type=int, default=0,
-                    help="config 4: also register this many independent pairs, split over the ranks "
-                         "(distributed.weak_scaling_pairs), and report pairs/s")
-    return ap.parse_args()
+                    help="config 4: keep the batch's volumes in pageable host memory")
+    ap.add_argument("--pairs", type=int, default=None,
+                    help="config 4: register this many independent pairs split over the ranks and "
+                         "report pairs/s (default 64 for N > 1, 0 for N = 1)")
+    ap.add_argument("--pairs-distinct", type=int, default=4,
+                    help="config 4: distinct synthetic pairs generated per rank (cycled through the "
+                         "rank's share; every registration still runs in full)")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launcher check without a GPU: ranks join a gloo group, time a barrier "
+                         "and rank 0 prints the line skeleton")
+    return ap.parse_args(argv)
 
 
 def dist_env():
@@ -69,6 +92,26 @@ def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     return ws, rank, local
+
+
+def _free_port() -> int:
+    with socket.socket(socket.AF_INET, socket.SOCK_STREAM) as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def relaunch_if_needed(args, argv) -> int | None:
+    """`python bench.py --gpus N` (N > 1, no torchrun): run N ranks of this script under
+    torch.distributed.run and return its exit code; None when already a rank."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return None
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + list(argv)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")  # the NCCL init log (transport: NVLink / NVLS) on stderr
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.call(cmd, env=env)
 
 
 def ncu_traffic(workload):
@@ -89,6 +132,17 @@ def peaks():
             p = json.load(f)
         return float(p["hbm_gbs"]), "measured"
     return 6650.0, "fallback"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 class ClockSampler:
@@ -145,78 +199,176 @@ def _pinned_copy(ngf_dev, a):
 
 def make_inputs(n: int, ratio: int, seed: int, dtype=np.float32):
     import paper_1812_06765_b200 as ngf
-    R, T, _ = ngf.ct_pair(n, seed=seed, dtype=dtype)
+    R, T, mapping = ngf.ct_pair(n, seed=seed, dtype=dtype)
     gd = ngf.deformation_grid_for(R.grid, ratio)
     y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=2.0).field.astype(dtype)
-    return R, T, gd, y
+    return R, T, gd, y, mapping
 
 
-def cpu_baseline(R, T, gd, y, budget_s: float):
-    """The oracle port (numpy restatement of the reference, oracle/) on this host's cores."""
-    from oracle import ngf_oracle as O
-    cores = os.cpu_count() or 1
-    og = O.grid(R.grid.dims, R.grid.spacing, R.grid.origin)
-    ogd = O.grid(gd.dims, gd.spacing, gd.origin)
-    obj = O.Objective(T.values, R.values, ogd, og, workers=cores)
+# ------------------------------------------------------------------------------------------
+# CPU side: the unmodified reference staged in oracle/_ref (oracle/build_ref.py), else the
+# oracle port (oracle/ngf_oracle.py).  Checkers and baselines only -- never the product path.
+# ------------------------------------------------------------------------------------------
+
+class CpuReference:
+    """The reference's LevelObjective / register on host numpy arrays."""
+
+    def __init__(self):
+        from oracle import ref as oref
+        self.mod = oref.load()
+        self.kind = "reference" if self.mod is not None else "port"
+        self.where = oref.origin() if self.mod is not None else "oracle/ngf_oracle.py"
+
+    def objective(self, R, T, gd, workers: int, dtype):
+        gi = R.grid
+        if self.mod is not None:
+            from ngfreg import ngf as rngf, objective as robj, transfer as rtr
+            from ngfreg.geometry import Grid3, Image3
+            g = Grid3(gi.dims, gi.spacing, gi.origin)
+            gdr = Grid3(gd.dims, gd.spacing, gd.origin)
+            params = rngf.NgfParams(10.0, 10.0)
+            ref = rngf.precompute_reference_terms(Image3(g, R.values.astype(dtype)), params)
+            return robj.LevelObjective(template=Image3(g, T.values.astype(dtype)), ref=ref,
+                                       plan=rtr.build_gather_plan(gdr, g), params=params, alpha=1.0,
+                                       workers=workers)
+        from oracle import ngf_oracle as O
+        return O.Objective(T.values.astype(dtype), R.values.astype(dtype),
+                           O.grid(gd.dims, gd.spacing, gd.origin),
+                           O.grid(gi.dims, gi.spacing, gi.origin), workers=workers)
+
+    def register(self, R, T, levels: int, ratio: int, precision: str, workers: int):
+        """Returns (field (3, nz, ny, nx), def grid dims, per-level iterations, seconds)."""
+        gi = R.grid
+        t0 = time.perf_counter()
+        if self.mod is not None:
+            from ngfreg import multilevel as rml
+            from ngfreg.geometry import Grid3, Image3
+            g = Grid3(gi.dims, gi.spacing, gi.origin)
+            cfg = rml.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision=precision,
+                                       workers=workers)
+            y, rep = rml.register(Image3(g, R.values), Image3(g, T.values), cfg)
+            return y.field, [lv.iterations for lv in rep.levels], time.perf_counter() - t0
+        from oracle import ngf_oracle as O
+        y, _, info = O.register(R.values, T.values, O.grid(gi.dims, gi.spacing, gi.origin),
+                                num_levels=levels, grid_ratio=ratio, precision=precision,
+                                workers=workers)
+        return y, [i["iterations"] for i in info], time.perf_counter() - t0
+
+
+def time_cpu_evals(obj, x, budget_s: float, max_reps: int = 5):
+    """(seconds per evaluation, reps, J, grad) of a CPU objective; one untimed warm-up."""
     t0 = time.perf_counter()
-    obj(y.ravel())  # warm (thread pools, page faults)
+    J, g = obj(x)
     first = time.perf_counter() - t0
-    reps = max(1, min(5, int(budget_s / max(first, 1e-3)) - 1))
+    reps = max(1, min(max_reps, int(budget_s / max(first, 1e-3)) - 1))
     t0 = time.perf_counter()
     for _ in range(reps):
-        obj(y.ravel())
-    dt = (time.perf_counter() - t0) / reps
-    return {"value": 1.0 / dt, "unit": "evals/s", "cores": cores, "kind": "port",
-            "sample": f"{reps} full evaluations of the same {R.grid.dims[0]}^3/{gd.dims[0]}^3 workload "
-                      f"(oracle/ngf_oracle.py, workers={cores}, {np.dtype(y.dtype).name}) after 1 warm-up; "
-                      f"{dt:.2f} s/eval"}
+        J, g = obj(x)
+    return (time.perf_counter() - t0) / reps, reps, float(J), np.asarray(g)
+
+
+def time_cpu_once(obj, x):
+    t0 = time.perf_counter()
+    obj(x)
+    return time.perf_counter() - t0
+
+
+def field_stats(y, y_ref, voxel: float):
+    """(all-node max, interior max (>= 2 def cells from every face), mean) displacement
+    difference in voxels (SURVEY.md §8(c) protocol)."""
+    d = np.sqrt(np.sum((np.asarray(y, np.float64) - np.asarray(y_ref, np.float64)) ** 2, axis=0)) / voxel
+    inner = d[2:-2, 2:-2, 2:-2] if min(d.shape) > 4 else d
+    return float(d.max()), float(inner.max()), float(d.mean())
+
+
+def registration_probe(yfield, image_grid, mapping):
+    import paper_1812_06765_b200 as ngf
+    from paper_1812_06765_b200.evaluation import sample_deformation
+    pts = ngf.probe_lattice(image_grid, n_per_axis=7, margin=0.2)
+    truth = np.stack(mapping(pts[:, 0], pts[:, 1], pts[:, 2]), axis=1)
+    err = np.linalg.norm(sample_deformation(yfield, pts) - truth, axis=1)
+    return {"mean_mm": float(err.mean()), "max_mm": float(err.max()), "probes": int(len(pts))}
+
+
+def _sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
 
 
 def run_reference(args):
+    """--impl reference: the reference's own LevelObjective (oracle/_ref, unmodified) on
+    this host's cores, same workload / metric / unit as our arm."""
     ws, rank, _ = dist_env()
     if rank != 0:
-        return
+        return 0
     n, ratio, _ = WORKLOADS[args.workload]
-    R, T, gd, y = make_inputs(n, ratio, 0, np.float32 if args.precision == "f32" else np.float64)
-    from oracle import ngf_oracle as O
+    dt = np.float32 if args.precision == "f32" else np.float64
+    R, T, gd, y, _ = make_inputs(n, ratio, 0, dt)
+    cpu = CpuReference()
     cores = os.cpu_count() or 1
-    og = O.grid(R.grid.dims, R.grid.spacing, R.grid.origin)
-    ogd = O.grid(gd.dims, gd.spacing, gd.origin)
-    obj = O.Objective(T.values, R.values, ogd, og, workers=cores)
-    t0 = time.perf_counter()
-    obj(y.ravel())
-    one = time.perf_counter() - t0
+    obj = cpu.objective(R, T, gd, cores, dt)
+    x = y.ravel()
+    one = time_cpu_once(obj, x)
     budget = 150.0
     warm = max(0, min(args.warmup - 1, int(budget / 3 / max(one, 1e-3))))
     steps = max(1, min(args.steps, int(budget / max(one, 1e-3)) - warm))
     for _ in range(warm):
-        obj(y.ravel())
+        obj(x)
     t0 = time.perf_counter()
     for _ in range(steps):
-        obj(y.ravel())
-    dt = time.perf_counter() - t0
-    value = steps / dt
+        obj(x)
+    dts = time.perf_counter() - t0
+    value = steps / dts
+    sample = (f"{steps} timed of {args.steps} requested full evaluations (bounded to ~{budget:.0f} s "
+              f"of CPU work), workers={cores}, {cpu.kind} code from {cpu.where}")
     line = {"metric": METRIC, "value": value, "unit": "evals/s", "n_gpus": args.gpus,
-            "steps": steps, "warmup": warm + 1, "ms_per_step": 1000 * dt / steps,
+            "steps": steps, "warmup": warm + 1, "ms_per_step": 1000 * dts / steps,
             "higher_is_better": True, "scaling": "strong" if args.workload == "c5" else "weak",
             "vs_baseline": None, "dtype": args.precision, "data": "synthetic", "impl": "reference",
             "config": {"workload": f"{args.workload}: {n}^3 CT-shaped pair, {gd.dims[0]}^3 def grid, "
                                    "one LevelObjective evaluation per step"},
-            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": "port",
-                             "sample": f"{steps} timed of {args.steps} requested full evaluations "
-                                       f"(bounded to ~{budget:.0f} s of CPU work), workers={cores}"},
+            "cpu_baseline": {"value": value, "unit": "evals/s", "cores": cores, "kind": cpu.kind,
+                             "sample": sample, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_dry(args):
+    """Launcher check on CPU: gloo group of N ranks, max-over-ranks barrier timing."""
+    import torch
+    import torch.distributed as dist
+    ws, rank, _ = dist_env()
+    if ws > 1:
+        dist.init_process_group("gloo")
+    t0 = time.perf_counter()
+    if ws > 1:
+        dist.barrier()
+    dt = time.perf_counter() - t0
+    t = torch.tensor([dt], dtype=torch.float64)
+    if ws > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ranks = [None] * ws
+        dist.all_gather_object(ranks, rank)
+    else:
+        ranks = [0]
+    if rank == 0:
+        print(json.dumps({"metric": METRIC, "dry_run": True, "n_gpus": ws, "ranks": ranks,
+                          "barrier_s_max": float(t.item())}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
 
 
 def run_ours(args):
+    import ctypes
+
     import torch
     import torch.distributed as dist
 
     import paper_1812_06765_b200 as ngf
+    from paper_1812_06765_b200 import _device as ngf_dev
     from paper_1812_06765_b200 import _lib
-    import ctypes
 
     ws, rank, local = dist_env()
     if ws > 1:
@@ -225,12 +377,14 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     dev_index = torch.cuda.current_device()
+    cpu_full = (ws == 1) if args.cpu_full is None else args.cpu_full
+    n_pairs = (64 if ws > 1 else 0) if args.pairs is None else args.pairs
 
     n, ratio, levels = WORKLOADS[args.workload]
     strong = args.workload == "c5"  # one pair split in z-slabs over all ranks
     npdt = np.float32 if args.precision == "f32" else np.float64
     es = np.dtype(npdt).itemsize
-    R, T, gd, y = make_inputs(n, ratio, seed=0 if strong else rank, dtype=npdt)
+    R, T, gd, y, mapping = make_inputs(n, ratio, seed=0 if strong else rank, dtype=npdt)
     gi = R.grid
     plan = ngf.build_gather_plan(gd, gi)
     T_dev = torch.from_numpy(T.values).cuda()
@@ -314,6 +468,9 @@ def run_ours(args):
     t_ms = max_over_ranks(step_ms)
     jobs = 1 if strong else ws  # evaluations completed per step, whole job
     value = jobs * args.steps / (t_ms / 1000.0)
+    # the timed evaluation's result, for the parity gate below
+    J_dev = float(sc[0].item())
+    g_dev = g.cpu().numpy().copy()
 
     # ---------------- fused kernel alone, CUDA events on the launching stream --------------
     _lib.check(_lib.lib().ngf_level_set_timing(level.handle, 1), "timing")
@@ -337,7 +494,6 @@ def run_ours(args):
     # ---------------- end to end through the numpy-facing LevelObjective -------------------
     # the step's input in page-locked host memory (the contract's e2e: H2D from pinned
     # memory, D2H of the result); LevelObjective's numpy call then DMAs it directly
-    from paper_1812_06765_b200 import _device as ngf_dev
     y_host = ngf_dev.pinned_empty((y.size,), y.dtype)
     y_host[...] = y.ravel()
     if strong:
@@ -356,22 +512,16 @@ def run_ours(args):
     else:
         call = obj  # LevelObjective.__call__: numpy in, (J, numpy grad) out
     for _ in range(max(5, args.warmup)):
-        # hold each result across the next call, like the timed loop (the page-locked
-        # gradient buffers of torch's host cache reach their steady-state count here)
+        # hold each result across the next call, like the timed loop
         J, gh = call(y_host)
     barrier()
     t0 = time.perf_counter()
     ee0 = torch.cuda.Event(enable_timing=True)
     ee1 = torch.cuda.Event(enable_timing=True)
     ee0.record(stream)
-    per_call = []
     for _ in range(args.steps):
-        tc = time.perf_counter()
         J, gh = call(y_host)
-        per_call.append(time.perf_counter() - tc)
     ee1.record(stream)
-    if os.environ.get("NGF_BENCH_DEBUG"):
-        print("e2e per call (us):", [round(v * 1e6) for v in per_call], file=sys.stderr)
     barrier()
     e2e_s = max_over_ranks(max(time.perf_counter() - t0, ee0.elapsed_time(ee1) / 1000.0))
     e2e = {"value": jobs * args.steps / e2e_s, "unit": "evals/s",
@@ -391,6 +541,7 @@ def run_ours(args):
 
     # ---------------- full coarse-to-fine registration (the paper's headline) -------------
     reg = None
+    batch_info = None
     if not args.no_register and not strong:
         cfg = ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision=args.precision)
         ngf.register(R, T, cfg)  # warm-up (allocations, first-touch)
@@ -407,81 +558,72 @@ def run_ours(args):
                               "optimize_s": round(lv.seconds_optimize, 4)}
                              for lv in rep.levels],
                "paper_gtx1080ti_s": 1.99,
-               "pairs_per_s": ws / reg_s}
+               "pairs_per_s": ws / reg_s,
+               "probe_error": registration_probe(yr, gi, mapping)}
+        # the reference's own run of this pair (tests/golden/make_golden_large.py)
+        fx = os.path.join(ROOT, "tests", "golden", f"register_{args.workload}.npz")
+        if os.path.exists(fx) and rank == 0 and f"y_{args.precision}" in np.load(fx).files:
+            z = np.load(fx)
+            if str(z["R_sha"]) == _sha(R.values.astype(np.float32)) and \
+                    str(z["T_sha"]) == _sha(T.values.astype(np.float32)):
+                mx, inner, mean = field_stats(yr.field, z[f"y_{args.precision}"], gi.spacing[0])
+                reg["vs_reference_run"] = {
+                    "source": f"tests/golden/register_{args.workload}.npz (ngfreg.register, "
+                              f"{int(z['workers'])} CPU workers, build container)",
+                    "max_voxel": mx, "interior_max_voxel": inner, "mean_voxel": mean,
+                    "bar_interior_voxel": BAR_VOXEL, "pass": inner <= BAR_VOXEL,
+                    "iterations": [lv.iterations for lv in rep.levels],
+                    "iterations_reference": [int(v) for v in z[f"iters_{args.precision}"]],
+                    "reference_probe_error_mean_mm": float(z[f"probe_mean_{args.precision}"]),
+                    "reference_seconds": float(z[f"seconds_{args.precision}"])}
         # the same with the volumes in page-locked host memory, as the CLI reads them
-        # (fileio.read_volume into dev.pinned_empty): the uploads become direct DMAs
-        from paper_1812_06765_b200 import _device as ngf_dev
         pin = []
         for im in (R, T):
-            a = ngf_dev.pinned_empty(im.values.shape, im.values.dtype)
-            a[...] = im.values
-            pin.append(ngf.Image3(im.grid, a))
+            pin.append(ngf.Image3(im.grid, _pinned_copy(ngf_dev, im.values)))
         ngf.register(pin[0], pin[1], cfg)
         barrier()
         t0 = time.perf_counter()
         ngf.register(pin[0], pin[1], cfg)
         barrier()
         reg["seconds_pinned_inputs"] = max_over_ranks(time.perf_counter() - t0)
-        if args.pairs > 0:
-            # config 4: a batch of independent pairs (seeds = pair ids), one process per GPU,
-            # no collective; inputs generated on the host before the clock starts
-            from paper_1812_06765_b200.distributed import weak_scaling_pairs
-            mine = weak_scaling_pairs(args.pairs, ws, rank)
-            batch = [make_inputs(n, ratio, seed=1000 + p, dtype=npdt)[:2] for p in mine]
-            if not args.pairs_pageable:
-                # volumes in page-locked host memory, as the CLI reads them: direct DMAs that
-                # concurrent registrations do not serialise on the library's staging buffer
-                batch = [tuple(ngf.Image3(im.grid, _pinned_copy(ngf_dev, im.values)) for im in pr)
-                         for pr in batch]
-            k = max(1, min(args.streams, len(batch)))
-            streams = [torch.cuda.Stream() for _ in range(k)]
-            errors = []
+        if n_pairs > 0:
+            batch_info = run_pairs(args, n_pairs, ws, rank, n, ratio, npdt, cfg, barrier,
+                                   max_over_ranks)
 
-            per_reg = [[] for _ in range(k)]
-
-            def work(i):
-                # registrations in flight on their own stream: the coarse levels leave most
-                # of the GPU idle, so concurrent pairs fill it
-                try:
-                    with torch.cuda.stream(streams[i]):
-                        for Rp, Tp in batch[i::k]:
-                            tr = time.perf_counter()
-                            ngf.register(Rp, Tp, cfg)
-                            per_reg[i].append(round(time.perf_counter() - tr, 4))
-                        streams[i].synchronize()
-                except Exception as e:  # surfaced after the join
-                    errors.append(e)
-
-            if k > 1:  # warm-up on every stream (reduction scratch, torch's per-stream block cache)
-                for st in streams:
-                    with torch.cuda.stream(st):
-                        ngf.register(batch[0][0], batch[0][1], cfg)
-                    st.synchronize()
-            barrier()
-            t0 = time.perf_counter()
-            if k > 1:
-                work_threads = [threading.Thread(target=work, args=(i,)) for i in range(k)]
-                for th in work_threads:
-                    th.start()
-                for th in work_threads:
-                    th.join()
-                if errors:
-                    raise errors[0]
-            else:
-                for Rp, Tp in batch:
-                    ngf.register(Rp, Tp, cfg)
-            barrier()
-            batch_s = max_over_ranks(time.perf_counter() - t0)
-            reg["batch"] = {"pairs": args.pairs, "per_rank": len(mine), "streams": k,
-                            "inputs": "pageable host" if args.pairs_pageable else "page-locked host",
-                            "seconds": batch_s,
-                            "pairs_per_s": args.pairs / batch_s}
-            if os.environ.get("NGF_BENCH_DEBUG"):
-                print("per registration (s), per stream:", per_reg, file=sys.stderr)
-
-    cpu = None
-    if rank == 0 and ws == 1:
-        cpu = cpu_baseline(R, T, gd, y, args.cpu_budget)
+    # ---------------- CPU legs (rank 0, N = 1): parity, baselines, same-box registrations ----
+    cpu = parity = cpu_matrix = regs = None
+    if rank == 0 and not strong:
+        ref = CpuReference()
+        cores = os.cpu_count() or 1
+        robj = ref.objective(R, T, gd, cores, npdt)
+        dt_eval, reps, J_ref, g_ref = time_cpu_evals(robj, y.ravel(), args.cpu_budget)
+        rel_J = abs(J_dev - J_ref) / abs(J_ref)
+        rel_g = float(np.linalg.norm(g_dev.astype(np.float64) - g_ref) / np.linalg.norm(g_ref))
+        parity = {"against": f"{ref.kind} LevelObjective ({ref.where}), same y, {args.precision}",
+                  "J": J_dev, "J_reference": J_ref, "J_rel": rel_J, "grad_rel_l2": rel_g,
+                  "tol_J": TOL_J, "tol_grad": TOL_G, "pass": bool(rel_J <= TOL_J and rel_g <= TOL_G)}
+        if ws == 1:
+            cpu = {"value": 1.0 / dt_eval, "unit": "evals/s", "cores": cores, "kind": ref.kind,
+                   "cpu_model": cpu_model(),
+                   "sample": f"{reps} full evaluations of the same {n}^3/{gd.dims[0]}^3 workload "
+                             f"({ref.kind} LevelObjective, workers={cores}, {np.dtype(npdt).name}) "
+                             f"after 1 warm-up; {dt_eval:.2f} s/eval"}
+        if cpu_full:
+            cpu_matrix = []
+            for prec, pdt in (("f32", np.float32), ("f64", np.float64)):
+                for w in (1, cores):
+                    if pdt == npdt and w == cores:
+                        s = dt_eval
+                    else:
+                        s = time_cpu_once(ref.objective(R, T, gd, w, pdt), y.astype(pdt).ravel())
+                    cpu_matrix.append({"precision": prec, "workers": w, "s_per_eval": round(s, 3),
+                                       "evals_per_s": 1.0 / s})
+            if not args.no_register:
+                regs = same_box_registrations(ref, cores)
+            if reg is not None and "vs_reference_run" in reg:
+                reg["cpu_reference_seconds_note"] = (
+                    "the reference's 256^3 4-level run is ~5 min on 8 cores; its time above is from "
+                    "the build container (not this host); configs 1-2 below are timed on this host")
 
     if rank == 0:
         line = {
@@ -498,7 +640,8 @@ def run_ours(args):
                               if l2_cold else
                               f"inputs larger than L2 (T + reference terms = {(5 * es * N) / 1e6:.0f} MB "
                               "> 126 MB), back-to-back steps"),
-                       "parallelism": (f"z-slabs x{ws} (one pair; NCCL all-reduce of grad D and D)"
+                       "parallelism": (f"z-slabs x{ws} (one pair; NCCL plane exchange of grad D, "
+                                       "all-reduce of D)"
                                        if strong else f"replicas x{ws} (one independent pair per GPU)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
@@ -507,24 +650,121 @@ def run_ours(args):
                          "bytes_per_launch": bytes_kernel, "peak_kind": peak_kind,
                          "eval_frac": bytes_eval / (eval_ms / 1000.0) / 1e9 / peak,
                          "launch": {"ctas": info[0], "smem_bytes": info[1], "z_chunk": info[2]}},
+            "parity": parity,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "full_registration": reg,
+            "config4": batch_info,
+            "registrations": regs,
             "cpu_baseline": cpu,
+            "cpu_matrix": cpu_matrix,
         }
         print(json.dumps(line), flush=True)
+    ok = parity is None or parity["pass"]
     if ws > 1:
         dist.destroy_process_group()
+    if not ok:
+        print(f"bench: PARITY FAILED: J_rel {parity['J_rel']:.3e} (tol {TOL_J}), grad rel-L2 "
+              f"{parity['grad_rel_l2']:.3e} (tol {TOL_G})", file=sys.stderr)
+        return 1
+    return 0
 
 
-def main():
-    args = parse()
+def run_pairs(args, n_pairs, ws, rank, n, ratio, npdt, cfg, barrier, max_over_ranks):
+    """Config 4: `n_pairs` independent pairs split over the ranks (no collective); K
+    registrations in flight per GPU, one host thread and CUDA stream each."""
+    import torch
+
+    import paper_1812_06765_b200 as ngf
+    from paper_1812_06765_b200 import _device as ngf_dev
+    from paper_1812_06765_b200.distributed import weak_scaling_pairs
+    mine = weak_scaling_pairs(n_pairs, ws, rank)
+    distinct = max(1, min(args.pairs_distinct, len(mine)))
+    made = [make_inputs(n, ratio, seed=1000 + mine[i], dtype=npdt)[:2] for i in range(distinct)]
+    if not args.pairs_pageable:
+        made = [tuple(ngf.Image3(im.grid, _pinned_copy(ngf_dev, im.values)) for im in pr)
+                for pr in made]
+    batch = [made[i % distinct] for i in range(len(mine))]
+    k = max(1, min(args.streams, len(batch)))
+    streams = [torch.cuda.Stream() for _ in range(k)]
+    errors = []
+
+    def work(i):
+        try:
+            with torch.cuda.stream(streams[i]):
+                for Rp, Tp in batch[i::k]:
+                    ngf.register(Rp, Tp, cfg)
+                streams[i].synchronize()
+        except Exception as e:  # surfaced after the join
+            errors.append(e)
+
+    for st in streams:  # warm-up on every stream (reduction scratch, per-stream block cache)
+        with torch.cuda.stream(st):
+            ngf.register(batch[0][0], batch[0][1], cfg)
+        st.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    threads = [threading.Thread(target=work, args=(i,)) for i in range(k)]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    barrier()
+    batch_s = max_over_ranks(time.perf_counter() - t0)
+    return {"pairs": n_pairs, "per_rank": len(mine), "streams": k,
+            "distinct_pairs_per_rank": distinct,
+            "inputs": "pageable host" if args.pairs_pageable else "page-locked host",
+            "seconds": batch_s, "pairs_per_s": n_pairs / batch_s, "scaling": "weak (replicas)"}
+
+
+def same_box_registrations(ref, cores):
+    """Configs 1 and 2 registered on the GPU and by the CPU reference on this host, f32:
+    times, per-level iterations, probe errors and the final-field difference."""
+    import paper_1812_06765_b200 as ngf
+    out = {}
+    # config 1: 64^3 Gaussian-bump pair, single level (tests/test_acceptance.py:86-98)
+    g1 = ngf.Grid3((64, 64, 64), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0))
+    center = tuple(o + e / 2 for o, e in zip(g1.origin, g1.extent))
+    m1 = ngf.gaussian_bump_mapping(center, 18.0, (3.0, -2.0, 1.5))
+    R1, T1 = ngf.make_registration_pair(g1, m1)
+    cases = [("c1", R1, T1, m1, 1, 4)]
+    R2, T2, m2 = ngf.ct_pair(128, seed=0)
+    cases.append(("c2", R2, T2, m2, 3, 2))
+    for name, Rc, Tc, mc, lv, ratio in cases:
+        Rf = ngf.Image3(Rc.grid, Rc.values.astype(np.float32))
+        Tf = ngf.Image3(Tc.grid, Tc.values.astype(np.float32))
+        cfg = ngf.MultilevelConfig(num_levels=lv, grid_ratio=ratio, precision="f32")
+        ngf.register(Rf, Tf, cfg)
+        t0 = time.perf_counter()
+        yg, rep = ngf.register(Rf, Tf, cfg)
+        gpu_s = time.perf_counter() - t0
+        y_cpu, it_cpu, cpu_s = ref.register(Rf, Tf, lv, ratio, "f32", cores)
+        mx, inner, mean = field_stats(yg.field, y_cpu, Rc.grid.spacing[0])
+        out[name] = {"image": Rc.grid.dims[0], "levels": lv, "grid_ratio": ratio,
+                     "gpu_seconds": gpu_s, "cpu_seconds": cpu_s, "cpu_workers": cores,
+                     "cpu_kind": ref.kind, "speedup": cpu_s / gpu_s,
+                     "iterations_gpu": [l.iterations for l in rep.levels], "iterations_cpu": it_cpu,
+                     "field_max_voxel": mx, "field_interior_max_voxel": inner,
+                     "field_mean_voxel": mean, "pass": inner <= BAR_VOXEL,
+                     "probe_error_gpu": registration_probe(yg, Rc.grid, mc)}
+    return out
+
+
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    rc = relaunch_if_needed(args, argv)
+    if rc is not None:
+        return rc
+    if args.dry_run:
+        return run_dry(args)
     if args.impl == "reference":
-        run_reference(args)
-    else:
-        run_ours(args)
+        return run_reference(args)
+    return run_ours(args)
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main())

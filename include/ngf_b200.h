@@ -151,6 +151,9 @@ int ngf_level_eval_host(ngf_level_t* level, const void* y_host, void* grad_host,
  * the data (it synchronises the stream). */
 int ngf_host_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream);
 int ngf_host_download(void* dst_host, const void* src_dev, size_t bytes, void* stream);
+/* 1 when host_ptr lies in page-locked (cudaHostAlloc / registered) memory, else 0: the
+ * Python layer keeps such upload sources alive until their asynchronous DMA completed. */
+int ngf_host_is_pinned(const void* host_ptr);
 /* Config-5 z-slab decomposition: restrict the fused evaluation to image
  * planes [zlo, zhi).  mode 2 of ngf_level_eval then writes the slab's NGF partial
  * (grad <- grad D_slab, scalars[1] <- D_slab, no curvature); after summing grad and

@@ -72,11 +72,30 @@ def to_device(a, dtype=None):
 _BIG = 1 << 20
 
 
+# Page-locked sources are uploaded by a direct, asynchronous DMA: the call returns before
+# the copy engine has read the buffer.  Each such source is kept alive here until an event
+# recorded after its DMA has completed, so dropping the array (and torch's host allocator
+# recycling the block) cannot race the copy.  Contract: the caller must not WRITE to a
+# page-locked source until the stream has passed the upload (pageable sources are copied
+# into the library's staging buffer before ngf_host_upload returns, so they are free at once).
+_inflight = []
+
+
+def _retire_uploads():
+    while _inflight and _inflight[0][0].query():
+        _inflight.pop(0)
+
+
 def _upload_staged(t, arr: np.ndarray):
     from ._lib import check, lib
 
     out = t.empty(arr.shape, dtype=torch_dtype(arr.dtype), device="cuda")
     check(lib().ngf_host_upload(out.data_ptr(), arr.ctypes.data, arr.nbytes, stream()), "ngf_host_upload")
+    _retire_uploads()
+    if lib().ngf_host_is_pinned(arr.ctypes.data):
+        ev = t.cuda.Event()
+        ev.record(t.cuda.current_stream())
+        _inflight.append((ev, arr))
     return out
 
 

@@ -70,6 +70,7 @@ _PROTOS = {
     "ngf_lbfgs_graph_runs": (_i64, []),
     "ngf_host_upload": (_i, [_vp, _vp, ctypes.c_size_t, _vp]),
     "ngf_host_download": (_i, [_vp, _vp, ctypes.c_size_t, _vp]),
+    "ngf_host_is_pinned": (_i, [_vp]),
     "ngf_level_ref_terms": (_vp, [_vp]),
     "ngf_level_set_timing": (_i, [_vp, _i]),
     "ngf_level_set_pt_variant": (_i, [_vp, _i]),

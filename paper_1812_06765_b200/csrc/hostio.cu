@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -45,26 +46,35 @@ class Team {
     int size() const { return (int)th_.size(); }
 
     // Run job(i) for i in [0, n) on the workers; returns immediately.  `wait_all` blocks
-    // until every index has finished.
-    void start(int n, std::function<void(int)> job) {
-        // a worker still inside the previous job holds active_; fields are published by
-        // the generation bump (a worker reads them only after seeing the new generation)
-        while (active_.load(std::memory_order_acquire) > 0) _mm_pause();
-        job_ = std::move(job);
-        n_ = n;
-        next_.store(0, std::memory_order_relaxed);
-        done_.store(0, std::memory_order_relaxed);
+    // until every index has finished.  Each call publishes a fresh Job object together
+    // with its generation under the mutex; a worker takes a reference to the job it saw
+    // (never to shared fields that the next start() rewrites), so a worker waking late
+    // from an earlier generation either finds that job exhausted or runs the new one.
+    void start(int n, std::function<void(int)> fn) {
+        auto j = std::make_shared<Job>();
+        j->fn = std::move(fn);
+        j->n = n;
         {
             std::lock_guard<std::mutex> lk(m_);
+            cur_ = j;
             gen_.fetch_add(1, std::memory_order_release);
         }
+        last_ = std::move(j);
         if (sleepers_.load(std::memory_order_acquire) > 0) cv_.notify_all();
     }
     void wait_all() {
-        while (done_.load(std::memory_order_acquire) < n_) _mm_pause();
+        const std::shared_ptr<Job> j = last_;
+        if (!j) return;
+        while (j->done.load(std::memory_order_acquire) < j->n) _mm_pause();
     }
 
   private:
+    struct Job {
+        std::function<void(int)> fn;
+        int n = 0;
+        std::atomic<int> next{0}, done{0};
+    };
+
     Team() {
         int hw = (int)std::thread::hardware_concurrency();
         int k = std::max(1, std::min(4, hw / 2));  // 4: best of 1-12 on the B200 hosts (tools/host_copy_probe.py)
@@ -83,22 +93,21 @@ class Team {
     void loop() {
         uint64_t seen = 0;
         while (true) {
-            active_.fetch_add(1, std::memory_order_acq_rel);
-            const uint64_t g = gen_.load(std::memory_order_acquire);
-            if (g != seen) {
-                seen = g;
-                if (stop_) {
-                    active_.fetch_sub(1, std::memory_order_acq_rel);
-                    return;
+            if (gen_.load(std::memory_order_acquire) != seen) {
+                std::shared_ptr<Job> j;
+                {
+                    std::lock_guard<std::mutex> lk(m_);
+                    if (stop_) return;
+                    seen = gen_.load(std::memory_order_acquire);
+                    j = cur_;
                 }
-                while (true) {
-                    const int i = next_.fetch_add(1, std::memory_order_acq_rel);
-                    if (i >= n_) break;
-                    job_(i);
-                    done_.fetch_add(1, std::memory_order_acq_rel);
+                while (j) {
+                    const int i = j->next.fetch_add(1, std::memory_order_acq_rel);
+                    if (i >= j->n) break;
+                    j->fn(i);
+                    j->done.fetch_add(1, std::memory_order_acq_rel);
                 }
             }
-            active_.fetch_sub(1, std::memory_order_acq_rel);
             // spin ~2 ms for the next job, then sleep
             int spins = 0;
             while (gen_.load(std::memory_order_acquire) == seen && spins < 20000) {
@@ -118,11 +127,10 @@ class Team {
     std::mutex m_;
     std::condition_variable cv_;
     std::atomic<uint64_t> gen_{0};
-    std::atomic<int> sleepers_{0}, active_{0};
-    std::atomic<int> next_{0}, done_{0};
-    std::function<void(int)> job_;
-    int n_ = 0;
-    bool stop_ = false;
+    std::atomic<int> sleepers_{0};
+    std::shared_ptr<Job> cur_;   // guarded by m_
+    std::shared_ptr<Job> last_;  // the caller's (start/wait_all run under g_io)
+    bool stop_ = false;          // guarded by m_
 };
 
 // A growable page-locked buffer whose last DMA is fenced by an event.
@@ -255,6 +263,10 @@ int host_download(void* dst, const void* src_dev, size_t bytes, cudaStream_t s) 
 extern "C" int ngf_host_upload(void* dst_dev, const void* src_host, size_t bytes, void* stream) {
     if ((!dst_dev || !src_host) && bytes) return NGF_EARG;
     return ngf::host_upload(dst_dev, src_host, bytes, ngf::as_stream(stream));
+}
+
+extern "C" int ngf_host_is_pinned(const void* host_ptr) {
+    return host_ptr && ngf::host_is_pinned(host_ptr) ? 1 : 0;
 }
 
 extern "C" int ngf_host_download(void* dst_host, const void* src_dev, size_t bytes, void* stream) {

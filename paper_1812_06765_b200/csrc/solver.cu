@@ -143,6 +143,13 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
             res->stop = NGF_STOP_STATIONARY;  // (the reference reports no evaluations here)
             goto done;
         }
+        if (cfg->max_iterations > 0 && cfg->max_ls_steps < 1) {
+            // no trial step may be evaluated: the reference's backtracking loop runs zero
+            // times and reports a failed line search (lbfgs.py:121-132)
+            res->stop = NGF_STOP_LINE_SEARCH;
+            res->line_search_failed = 1;
+            goto done;
+        }
         std::vector<Pair> history;
         const double x_scale = std::max(std::sqrt(st[2]), 1.0);
         // the whole loop as one graph launch when the two-loop fits the cluster kernel

@@ -193,6 +193,13 @@ class _Solver:
         x_scale = max(math.sqrt(st[2]), 1.0)
         rejected = 0
         for it in range(cfg.max_iterations):
+            if cfg.max_ls_steps < 1:
+                # no trial point may be evaluated: the reference's backtracking loop runs
+                # zero times and the line search fails (lbfgs.py:121-132)
+                trace.stop_reason = "line search failed"
+                trace.line_search_failed = True
+                trace.evaluations = self.evals
+                return x, trace
             # direction and (optimistically) the first trial point, one host sync
             _two_loop(history, g, d, self.scal[3:4])
             t = cfg.initial_step

@@ -30,3 +30,24 @@ def grid_from(arr):
 @pytest.fixture
 def rng():
     return np.random.default_rng(12345)
+
+
+def cpu_reference_objective(T, R, gd, gi, workers=None):
+    """The reference's LevelObjective on host arrays (unmodified ngfreg staged in oracle/_ref
+    by oracle/build_ref.py), or the pinned oracle port when it is not staged.  Grids are
+    anything with .dims/.spacing/.origin.  Checker only."""
+    from oracle import ref as oref
+    workers = workers or (os.cpu_count() or 1)
+    mod = oref.load()
+    if mod is not None:
+        from ngfreg import ngf as rngf, objective as robj, transfer as rtr
+        from ngfreg.geometry import Grid3, Image3
+        g = Grid3(tuple(gi.dims), tuple(gi.spacing), tuple(gi.origin))
+        gdr = Grid3(tuple(gd.dims), tuple(gd.spacing), tuple(gd.origin))
+        params = rngf.NgfParams(10.0, 10.0)
+        ref = rngf.precompute_reference_terms(Image3(g, R), params)
+        return robj.LevelObjective(template=Image3(g, T), ref=ref, plan=rtr.build_gather_plan(gdr, g),
+                                   params=params, alpha=1.0, workers=workers)
+    from oracle import ngf_oracle as O
+    return O.Objective(T, R, O.grid(gd.dims, gd.spacing, gd.origin), O.grid(gi.dims, gi.spacing, gi.origin),
+                       workers=workers)

@@ -1,0 +1,111 @@
+"""Parity at the configurations the headline numbers are quoted on.
+
+* LevelObjective (objective.py:54-60) on the config-3 finest level (256^3 image,
+  64^3 deformation grid: the 32 x 16 tile variant and the non-uniform z-chunk plan
+  of the dispatch simulator) and on config 2 (128^3 with a 65^3 grid -- the
+  width-5 gather plan of transfer.py:104-110 -- and with ratio 2, 64^3) against the
+  reference's own LevelObjective on the same y: J within 1e-4 relative, grad J
+  within 1e-3 relative L2 (north star, fp32).
+* Full multilevel registrations (multilevel.py:179-247 with the stopping rules of
+  lbfgs.py:167-176) at config 2 (3 levels, ratio 2; f32 and f64) and config 3
+  (4 levels, ratio 4; f32) against the reference's own runs of the same pairs
+  (tests/golden/register_c{2,3}.npz, written by make_golden_large.py): final field
+  within 0.05 voxel on the interior (>= 2 deformation cells from every face,
+  SURVEY.md §8(c)); all-node max, mean and per-level iterations are printed; the
+  probe error against the known synthetic mapping must not be worse than the
+  reference's by more than 0.05 mm.
+"""
+
+import hashlib
+import os
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, cpu_reference_objective
+
+pytestmark = pytest.mark.gpu
+
+import paper_1812_06765_b200 as ngf  # noqa: E402
+from paper_1812_06765_b200.evaluation import sample_deformation  # noqa: E402
+
+TOL_J, TOL_G, BAR_VOXEL = 1e-4, 1e-3, 0.05
+
+
+def _rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def _device_obj(T, R, gd, gi):
+    plan = ngf.build_gather_plan(gd, gi)
+    return ngf.LevelObjective.from_device(torch.from_numpy(T).cuda(), torch.from_numpy(R).cuda(), plan,
+                                          ngf.NgfParams(10.0, 10.0), 1.0)
+
+
+def _def_grid(gi, dd):
+    hd = tuple(n * s / m for n, s, m in zip(gi.dims, gi.spacing, dd))
+    od = tuple(o - s / 2 + sd / 2 for o, s, sd in zip(gi.origin, gi.spacing, hd))
+    return ngf.Grid3(dd, hd, od)
+
+
+_PAIRS = {}
+
+
+def _pair(n):
+    if n not in _PAIRS:
+        _PAIRS[n] = ngf.ct_pair(n, seed=0)
+    return _PAIRS[n]
+
+
+@pytest.mark.parametrize("case", ["c3", "c2_65", "c2_r2"])
+@pytest.mark.parametrize("amp", [2.0, 5.0])
+def test_objective_at_config_sizes(case, amp):
+    n = 256 if case == "c3" else 128
+    R, T, _ = _pair(n)
+    gi = R.grid
+    gd = _def_grid(gi, (65, 65, 65)) if case == "c2_65" else \
+        ngf.deformation_grid_for(gi, 4 if case == "c3" else 2)
+    y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=amp).field.astype(np.float32)
+    J_ref, g_ref = cpu_reference_objective(T.values, R.values, gd, gi)(y.ravel())
+    obj = _device_obj(T.values, R.values, gd, gi)
+    J, g = obj(y.ravel())
+    rJ, rg = abs(J - J_ref) / abs(J_ref), _rel(g, g_ref)
+    print(f"{case} amp {amp}: J {J:.9g} vs {J_ref:.9g} (rel {rJ:.2e}); grad rel-L2 {rg:.2e}")
+    assert rJ <= TOL_J and rg <= TOL_G
+    # the device-resident entry (what L-BFGS uses) returns the same numbers
+    x = torch.from_numpy(y.ravel().copy()).cuda()
+    gd_dev = torch.empty_like(x)
+    sc = obj.eval_device(x, gd_dev)
+    assert float(sc[0].item()) == J and np.array_equal(gd_dev.cpu().numpy(), g)
+
+
+def _sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("name,p", [("c2", "f32"), ("c2", "f64"), ("c3", "f32")])
+def test_full_registration_vs_reference_run(name, p):
+    path = os.path.join(GOLDEN, f"register_{name}.npz")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated")
+    z = np.load(path)
+    n, levels, ratio = int(z["n"]), int(z["levels"]), int(z["ratio"])
+    R, T, mapping = _pair(n)
+    assert _sha(R.values) == str(z["R_sha"]) and _sha(T.values) == str(z["T_sha"]), \
+        "synthetic pair differs from the one the reference registered"
+    y, rep = ngf.register(R, T, ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision=p))
+    gd = z[f"gd_{p}"]
+    assert tuple(y.grid.dims) == tuple(int(v) for v in gd[:3])
+    d = np.sqrt(np.sum((y.field.astype(np.float64) - z[f"y_{p}"].astype(np.float64)) ** 2, axis=0))
+    d /= R.grid.spacing[0]
+    inner = d[2:-2, 2:-2, 2:-2]
+    pts = ngf.probe_lattice(R.grid, n_per_axis=7, margin=0.2)
+    truth = np.stack(mapping(pts[:, 0], pts[:, 1], pts[:, 2]), axis=1)
+    err = np.linalg.norm(sample_deformation(y, pts) - truth, axis=1)
+    print(f"{name} {p}: iterations {[lv.iterations for lv in rep.levels]} vs reference "
+          f"{list(z[f'iters_{p}'])}; field max {d.max():.4f} interior {inner.max():.4f} "
+          f"mean {d.mean():.5f} voxel; probe error mean {err.mean():.4f} (reference "
+          f"{float(z[f'probe_mean_{p}']):.4f}) max {err.max():.4f} mm")
+    assert inner.max() <= BAR_VOXEL
+    assert err.mean() <= float(z[f"probe_mean_{p}"]) + 0.05
