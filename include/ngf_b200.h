@@ -174,6 +174,11 @@ int ngf_level_set_timing(ngf_level_t* level, int on);
 int ngf_level_kernel_ms(ngf_level_t* level, float* ms);
 /* info[0..8]: fused CTAs, smem bytes, z chunk, P^T window wx, wy, wz, tiles ntx, nty, ntz. */
 int ngf_level_info(const ngf_level_t* level, int64_t* info);
+/* Kernel variant of the level's fused march: 0-5 the classic two-slot / one-slot tile
+ * shapes (fused_march.cuh), 6 the lean march (march_lean.cu; f32, power-of-two spacing,
+ * grid ratio >= 2).  NGF_FUSED_VARIANT=<v> forces one when eligible, NGF_NO_LEAN=1 keeps
+ * the classic ones. */
+int ngf_level_variant(const ngf_level_t* level);
 
 /* ---------------------------------------------------------------- L-BFGS vector algebra
  * lbfgs.py:68-181.  Scalars that the reference keeps as Python floats live in

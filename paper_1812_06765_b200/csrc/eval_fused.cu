@@ -6,6 +6,7 @@
 #include <vector>
 
 #include "fused_cfg.cuh"
+#include "march_lean.cuh"
 
 namespace ngf {
 
@@ -379,6 +380,7 @@ void fused_variant_geom(int v, int* ty, int* nt) {
         case 3: *ty = V3::TY; *nt = V3::NT; return;
         case 4: *ty = V4::TY; *nt = V4::NT; return;
         case 5: *ty = V5::TY; *nt = V5::NT; return;
+        case kLeanVariant: *ty = lean::kTYI; *nt = lean::kNT; return;
         default: *ty = V0::TY; *nt = V0::NT; return;
     }
 }
@@ -393,6 +395,8 @@ size_t fused_smem(int v, int wx, int wy) {
         case 3: return smem_bytes_cfg<T, V3>(wx, wy);
         case 4: return smem_bytes_cfg<T, V4>(wx, wy);
         case 5: return smem_bytes_cfg<T, V5>(wx, wy);
+        case kLeanVariant: return std::is_same<T, float>::value && wx <= lean::kWXM && wy <= lean::kWYM
+                                      ? lean_smem(0, 0) : size_t(1) << 30;
         default: return smem_bytes_cfg<T, V0>(wx, wy);
     }
 }
@@ -405,6 +409,7 @@ int fused_prepare<float>(int v, size_t smem) {
         case 3: return march_prepare<float, V3>(smem);
         case 4: return march_prepare<float, V4>(smem);
         case 5: return march_prepare<float, V5>(smem);
+        case kLeanVariant: return lean_prepare(smem);
         default: return march_prepare<float, V0>(smem);
     }
 }
@@ -429,6 +434,7 @@ void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
         case 3: march_launch<float, V3>(a, s); return;
         case 4: march_launch<float, V4>(a, s); return;
         case 5: march_launch<float, V5>(a, s); return;
+        case kLeanVariant: lean_launch(a, s); return;
         default: march_launch<float, V0>(a, s); return;
     }
 }

@@ -33,7 +33,15 @@ struct FusedPlan {
     const void* ycw;      // [nty][2*(ty+2)]
     int n_cta;
     size_t smem_bytes;
+    // lean march (variant kLeanVariant, march_lean.cu): zero-pad offset after the template
+    // (reads outside the image hull land there), entries per P^T window output, and the
+    // per-tile (E1 column / row, weight bits) lists of the x and y passes
+    unsigned pad_off;
+    int kx, ky;
+    const int32_t* lx;  // [ntx][wx][kx] int2
+    const int32_t* ly;  // [nty][wy][ky] int2
 };
+constexpr int kLeanVariant = 6;
 constexpr int kCover = 8;
 
 struct LevelDev;  // defined in level.cu

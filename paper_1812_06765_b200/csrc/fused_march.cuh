@@ -37,37 +37,6 @@ namespace ngf {
 #define NGF_T_PREFETCH 0  // measured slower: 356 vs 340 us at 256^3
 #endif
 
-template <typename T>
-__host__ __device__ __forceinline__ void fd_coef(int i, int n, T ih, T& cm, T& c0, T& cp) {
-    // derivative at index i as cm*v[i-1] + c0*v[i] + cp*v[i+1] (warp.py:130-143)
-    cm = (T)0;
-    c0 = (T)0;
-    cp = (T)0;
-    if (n < 2 || i < 0 || i >= n) return;
-    if (i == 0) {
-        c0 = -ih;
-        cp = ih;
-    } else if (i == n - 1) {
-        cm = -ih;
-        c0 = ih;
-    } else {
-        cm = (T)-0.5 * ih;
-        cp = (T)0.5 * ih;
-    }
-}
-
-// transpose coefficients at index i: multiply q[i-1], q[i], q[i+1]
-template <typename T>
-__host__ __device__ __forceinline__ void fdt_coef(int i, int n, T ih, T& gm, T& g0, T& gp) {
-    T a, b, c;
-    fd_coef<T>(i - 1, n, ih, a, b, c);
-    gm = c;
-    fd_coef<T>(i, n, ih, a, b, c);
-    g0 = b;
-    fd_coef<T>(i + 1, n, ih, a, b, c);
-    gp = a;
-}
-
 // Per-thread march state.  Slot s owns E1 position P = tid + s * NT for all planes.
 template <typename T, typename C>
 struct March {

@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "eval_fused.cuh"
 #include "fused_impl.cuh"
+#include "march_lean.cuh"
 #include "ops_exact.cuh"
 
 namespace ngf {
@@ -38,6 +39,7 @@ struct ngf_level {
     ngf_grid_t img, def;
     ngf_plan_t* plan;
     const void* T;
+    void* Tpad;  // lean march: copy of T followed by a zero pad (reads outside the hull)
     void* gR;   // 3N exact reference terms
     void* nR;   // N
     void* RT;   // packed N x 4
@@ -152,8 +154,50 @@ static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, 
     return true;
 }
 
+// Can the lean march (march_lean.cu) evaluate this level?  f32, every image axis >= 4
+// voxels and every deformation axis >= 2 nodes, power-of-two image spacing (exact
+// reciprocal in the cell lookup), the z index map advancing by <= 1 node per image plane
+// and never on two consecutive planes (the staggered P^T flush), and windows / entry counts
+// within the kernel's compile-time bounds.  Returns the entries per window output (x, y).
+static bool lean_eligible(const ngf_level* L, int* kx, int* ky) {
+    const ngf_plan_t* p = L->plan;
+    if (L->dtype != NGF_F32 || std::getenv("NGF_NO_LEAN")) return false;
+    for (int ax = 0; ax < 3; ++ax) {
+        if (L->img.dims[ax] < 4 || L->def.dims[ax] < 2) return false;
+        if (!is_pow2(L->img.spacing[ax])) return false;
+    }
+    const int nz = (int)L->img.dims[2];
+    const int32_t* iz = p->h_i0[2];
+    for (int z = 0; z + 1 < nz; ++z) {
+        const int adv = iz[z + 1] - iz[z];
+        if (adv < 0 || adv > 1) return false;
+        if (adv == 1 && z + 2 < nz && iz[z + 2] - iz[z + 1] == 1) return false;
+    }
+    // entries per window output: image columns (rows) of a tile + ring feeding one node
+    int k[2] = {0, 0};
+    const int tile[2] = {kTX, lean::kTYI};
+    for (int ax = 0; ax < 2; ++ax) {
+        const int n = (int)L->img.dims[ax], nd = (int)L->def.dims[ax];
+        const int32_t* i0 = p->h_i0[ax];
+        for (int t = 0; t * tile[ax] < n; ++t) {
+            std::map<int, int> cnt;
+            for (int e = 0; e < tile[ax] + 2; ++e) {
+                const int i = t * tile[ax] - 1 + e;
+                if (i < 0 || i >= n) continue;
+                ++cnt[i0[i]];
+                if (nd > 1) ++cnt[i0[i] + 1];
+            }
+            for (auto& kv : cnt) k[ax] = std::max(k[ax], kv.second);
+        }
+    }
+    if (k[0] > lean::kKMax || k[1] > lean::kKMax) return false;
+    *kx = k[0] <= 4 ? 4 : 8;
+    *ky = k[1] <= 4 ? 4 : 8;
+    return true;
+}
+
 template <typename T>
-static int fused_setup(ngf_level* L, int zlo, int zhi) {
+static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) {
     const auto t_start = std::chrono::steady_clock::now();
     const ngf_plan_t* p = L->plan;
     const int nx = (int)L->img.dims[0], ny = (int)L->img.dims[1], nz = (int)L->img.dims[2];
@@ -171,8 +215,8 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     // threads with the derivative ring in shared memory take 1.16x the time of 32 x 12
     // tiles of 256 threads per plane for 1.33x the voxels).  Every
     // chunking must keep each def node covered by at most kCover chunks (k_post's sum).
-    static const int kMinBlocks[] = {2, 2, 2, 2, 1, 1};
-    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5, 1.0, 1.14};  // f64 (4, 5) relative to 4
+    static const int kMinBlocks[] = {2, 2, 2, 2, 1, 1, 2};
+    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5, 1.0, 1.14, 1.0};  // f64 (4, 5) relative to 4; lean alone
     // the search depends only on the geometry (dims, slab, index maps), the dtype and the
     // tuning overrides: memoised per process, so repeated registrations of one size (a
     // batch of pairs, config 4) skip it (1.4 ms at 256^3, 4.9 ms at 512^3)
@@ -191,6 +235,8 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     }
     std::vector<int> bounds;
     int variant = -1;
+    int lean_kx = 8, lean_ky = 8;
+    const bool lean_ok = sizeof(T) == 4 && lean_eligible(L, &lean_kx, &lean_ky);
     size_t n_choices = 0;
     static std::mutex plan_mu;
     static std::map<std::string, std::pair<int, std::vector<int>>> plan_cache;
@@ -208,9 +254,11 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
         if (sizeof(T) == 8) {  // f64 shapes: 0, 4, 5
             const int v = env ? std::atoi(env) : -1;
             cand = (v == 0 || v == 4 || v == 5) ? std::vector<int>{v} : std::vector<int>{4, 5};
-        } else if (env) {
-            const int v = std::atoi(env) % 6;  // f32 shapes: 0 .. 5
+        } else if (env && (std::atoi(env) % 7 != kLeanVariant || lean_ok)) {
+            const int v = std::atoi(env) % 7;  // f32 shapes: 0 .. 5, 6 = lean
             cand = {v};
+        } else if (lean_ok) {
+            cand = {kLeanVariant};
         } else {
             cand = {1, 2};
         }
@@ -350,6 +398,50 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     std::vector<T> xcw, ycw;
     build_csr(0, kTX, fp.ntx, fp.wx, xl, xcsr, xcw);
     build_csr(1, fp.ty, fp.nty, fp.wy, yl, ycsr, ycw);
+    // lean march: per tile and window output, K (E1 index, f32 weight bits) entries in
+    // ascending E1 order (the reference's gather order, transfer.py:89-96), zero-padded
+    std::vector<int32_t> lxv(2), lyv(2);
+    fp.kx = fp.ky = 0;
+    auto build_list = [&](int axis, int tile, int ntile, int w, int K, const std::vector<int>& lo,
+                          std::vector<int32_t>& out) {
+        const int ne = tile + 2, n = p->n_img[axis], nd = p->n_def[axis];
+        out.assign((size_t)ntile * w * K * 2, 0);
+        for (int t = 0; t < ntile; ++t)
+            for (int d = 0; d < w; ++d) {
+                int32_t* ent = out.data() + ((size_t)t * w + d) * K * 2;
+                int cnt = 0;
+                for (int e = 0; e < ne; ++e) {
+                    const int i = t * tile - 1 + e;
+                    if (i < 0 || i >= n) continue;
+                    const int dl = p->h_i0[axis][i] - lo[t];
+                    const double w1 = p->h_w1[axis][i];
+                    float wt;
+                    if (dl == d) wt = (float)(1.0 - w1);
+                    else if (dl == d - 1 && nd > 1) wt = (float)w1;
+                    else continue;
+                    if (cnt < K) {
+                        ent[2 * cnt] = e;
+                        std::memcpy(&ent[2 * cnt + 1], &wt, 4);
+                    }
+                    ++cnt;
+                }
+            }
+    };
+    if (variant == kLeanVariant) {
+        fp.kx = lean_kx;
+        fp.ky = lean_ky;
+        build_list(0, kTX, fp.ntx, fp.wx, fp.kx, xl, lxv);
+        build_list(1, fp.ty, fp.nty, fp.wy, fp.ky, yl, lyv);
+        const size_t n = (size_t)nx * ny * nz;
+        fp.pad_off = (unsigned)n;
+        if (!L->Tpad) {
+            const size_t pad = (size_t)nx * ny + nx + 64;
+            NGF_CUDA((cudaError_t)dev_alloc(&L->Tpad, (n + pad) * sizeof(float)));
+            NGF_CUDA(cudaStreamSynchronize(0));  // the pool allocation (stream 0) before use on `stream`
+            NGF_CUDA(cudaMemcpyAsync(L->Tpad, L->T, n * sizeof(float), cudaMemcpyDeviceToDevice, stream));
+            NGF_CUDA(cudaMemsetAsync((float*)L->Tpad + n, 0, pad * sizeof(float), stream));
+        }
+    }
     std::vector<int32_t> blob;
     auto app = [&](const void* v, size_t bytes) {
         size_t off = blob.size();
@@ -363,7 +455,8 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     auto appv = [&](const std::vector<int32_t>& v) { return app(v.data(), v.size() * 4); };
     size_t o_wx = appv(wxv), o_wy = appv(wyv), o_wz = appv(wzv), o_cx = appv(cx), o_cy = appv(cy),
            o_cz = appv(cz_), o_zb = appv(zbv), o_xcsr = appv(xcsr), o_ycsr = appv(ycsr),
-           o_xcw = app(xcw.data(), xcw.size() * sizeof(T)), o_ycw = app(ycw.data(), ycw.size() * sizeof(T));
+           o_xcw = app(xcw.data(), xcw.size() * sizeof(T)), o_ycw = app(ycw.data(), ycw.size() * sizeof(T)),
+           o_lx = appv(lxv), o_ly = appv(lyv);
     NGF_CUDA((cudaError_t)dev_alloc((void**)&L->fp_blob, blob.size() * 4));
     NGF_CUDA((cudaError_t)upload_blocking(L->fp_blob, blob.data(), blob.size() * 4));
     const int32_t* b = (const int32_t*)L->fp_blob;
@@ -378,6 +471,8 @@ static int fused_setup(ngf_level* L, int zlo, int zhi) {
     fp.ycsr = b + o_ycsr;
     fp.xcw = b + o_xcw;
     fp.ycw = b + o_ycw;
+    fp.lx = b + o_lx;
+    fp.ly = b + o_ly;
     const size_t win = (size_t)fp.wz * fp.wy * fp.wx;
     NGF_CUDA((cudaError_t)dev_alloc((void**)&L->partial, (size_t)fp.n_cta * 3 * win * sizeof(T)));
     NGF_CUDA((cudaError_t)dev_alloc((void**)&L->dpart, (size_t)fp.n_cta * sizeof(double)));
@@ -427,7 +522,7 @@ static FusedArgs<T> fused_args(const ngf_level* L, const void* y) {
     a.hix = (T)(a.nx > 2 ? a.nx - 2 : 0);
     a.hiy = (T)(a.ny > 2 ? a.ny - 2 : 0);
     a.hiz = (T)(a.nz > 2 ? a.nz - 2 : 0);
-    a.Tv = (const T*)L->T;
+    a.Tv = (const T*)(L->fp.variant == kLeanVariant ? L->Tpad : L->T);
     a.RT = (const V4T<T>*)L->RT;
     a.y = (const T*)y;
     a.partial = (T*)L->partial;
@@ -574,7 +669,7 @@ static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_g
     if (!rc) {
         if (dtype == NGF_F32) {
             rc = pack_rt<float>((const float*)L->gR, (const float*)L->nR, n, L->RT, s);
-            if (!rc) rc = fused_setup<float>(L, 0, (int)L->img.dims[2]);
+            if (!rc) rc = fused_setup<float>(L, 0, (int)L->img.dims[2], s);
         } else {
             rc = pack_rt<double>((const double*)L->gR, (const double*)L->nR, n, L->RT, s);
             if (!rc) rc = fused_setup<double>(L, 0, (int)L->img.dims[2]);
@@ -616,7 +711,7 @@ void ngf_level_destroy(ngf_level_t* L) {
         L->plan->idle = 1;
         ngf_plan_destroy(L->plan);
     }
-    void* bufs[] = {L->flag, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart,
+    void* bufs[] = {L->flag, L->Tpad, L->gR, L->nR, L->RT, L->fp_blob, L->partial, L->dpart, L->spart,
                     L->ex.yhat, L->ex.W, L->ex.terms, L->ex.q, L->ex.s, L->ex.ghat, L->ex.gD,
                     L->ex.cws, L->ex.dws, L->hx, L->hg, L->hsc};
     for (void* b : bufs) dev_free(b);
@@ -716,5 +811,7 @@ int ngf_level_info(const ngf_level_t* L, int64_t* info) {
 }
 
 const void* ngf_level_ref_terms(const ngf_level_t* L) { return L ? L->RT : nullptr; }
+
+int ngf_level_variant(const ngf_level_t* L) { return L ? L->fp.variant : NGF_EARG; }
 
 }  // extern "C"

@@ -148,6 +148,7 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
             // times and reports a failed line search (lbfgs.py:121-132)
             res->stop = NGF_STOP_LINE_SEARCH;
             res->line_search_failed = 1;
+            res->evaluations = evals;
             goto done;
         }
         std::vector<Pair> history;

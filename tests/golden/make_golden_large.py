@@ -31,15 +31,22 @@ sys.path.insert(0, ROOT)
 from ngfreg import multilevel  # noqa: E402
 from ngfreg.evaluation import sample_deformation  # noqa: E402
 from ngfreg.geometry import Grid3, Image3  # noqa: E402
+from ngfreg.lbfgs import LbfgsConfig, StoppingRules  # noqa: E402
 from ngfreg.synthetic import probe_lattice  # noqa: E402
 
 from paper_1812_06765_b200.synthetic import ct_pair  # noqa: E402  (host numpy only)
 
 CASES = {
-    # name: (n, levels, ratio, precisions)
-    "c2": (128, 3, 2, ("f32", "f64")),
-    "c3": (256, 4, 4, ("f32",)),
+    # name: (n, levels, ratio, precisions, converged)
+    "c2": (128, 3, 2, ("f32", "f64"), False),
+    "c3": (256, 4, 4, ("f32",), False),
+    # the same pairs run to convergence (tol_J 1e-9, <= 300 iterations per
+    # level), where the final field no longer depends on when the stopping rules fire
+    "c2conv": (128, 3, 2, ("f32",), True),
+    "c3conv": (256, 4, 4, ("f32",), True),
 }
+CONVERGED_TOL_J = 1e-9
+CONVERGED_MAX_ITERS = 300
 
 
 def sha(a: np.ndarray) -> str:
@@ -47,17 +54,23 @@ def sha(a: np.ndarray) -> str:
 
 
 def run(name: str, workers: int):
-    n, levels, ratio, precs = CASES[name]
+    n, levels, ratio, precs, conv = CASES[name]
     R, T, mapping = ct_pair(n, seed=0)
     g = Grid3(R.grid.dims, R.grid.spacing, R.grid.origin)
     out = {"R_sha": np.array(sha(R.values)), "T_sha": np.array(sha(T.values)),
            "n": np.array(n), "levels": np.array(levels), "ratio": np.array(ratio),
-           "workers": np.array(workers)}
+           "workers": np.array(workers), "converged": np.array(conv),
+           "tol_J": np.array(CONVERGED_TOL_J if conv else 1e-4),
+           "max_iterations": np.array(CONVERGED_MAX_ITERS if conv else 100)}
     pts = probe_lattice(g, n_per_axis=7, margin=0.2)
     truth = np.stack(mapping(pts[:, 0], pts[:, 1], pts[:, 2]), axis=1)
     for p in precs:
+        kw = {}
+        if conv:
+            kw = dict(lbfgs=LbfgsConfig(max_iterations=CONVERGED_MAX_ITERS),
+                      stopping=StoppingRules(tol_J=CONVERGED_TOL_J))
         cfg = multilevel.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision=p,
-                                          workers=workers)
+                                          workers=workers, **kw)
         t0 = time.perf_counter()
         y, rep = multilevel.register(Image3(g, R.values), Image3(g, T.values), cfg)
         dt = time.perf_counter() - t0
@@ -78,6 +91,6 @@ def run(name: str, workers: int):
 
 
 if __name__ == "__main__":
-    names = [a for a in sys.argv[1:] if a in CASES] or list(CASES)
+    names = [a for a in sys.argv[1:] if a in CASES] or ["c2", "c3"]
     for nm in names:
         run(nm, os.cpu_count() or 1)
