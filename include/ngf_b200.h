@@ -159,6 +159,13 @@ int ngf_host_is_pinned(const void* host_ptr);
  * (grad <- grad D_slab, scalars[1] <- D_slab, no curvature); after summing grad and
  * scalars[1] over slabs (e.g. an NCCL all-reduce), ngf_level_add_curvature adds
  * alpha grad S and sets scalars = (J, D, S), identically on every rank. */
+/* A config-5 slab level: like ngf_level_create, but the reference terms are computed on
+ * image planes [zlo, zhi) only (R itself is read on the neighbouring planes, so no halo
+ * exchange is needed) and the fused march is restricted to that slab.  Only mode 2 of
+ * ngf_level_eval and ngf_level_add_curvature are valid on it (NGF_ESTATE otherwise). */
+int ngf_level_create_zslab(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
+                           const void* T, const void* R, double tau, double rho, double alpha,
+                           int64_t zlo, int64_t zhi, void* stream, ngf_level_t** out);
 int ngf_level_set_zrange(ngf_level_t* level, int64_t zlo, int64_t zhi);
 int ngf_level_add_curvature(ngf_level_t* level, const void* y, void* grad, double* scalars_dev,
                             void* stream);

@@ -63,6 +63,7 @@ _PROTOS = {
     "ngf_level_create": (_i, [_pg, _pg, _i, _vp, _vp, _d, _d, _d, _vp, ctypes.POINTER(_vp)]),
     "ngf_level_create_terms": (_i, [_pg, _pg, _i, _vp, _vp, _vp, _d, _d, _d, _vp,
                                     ctypes.POINTER(_vp)]),
+    "ngf_level_create_zslab": (_i, [_pg, _pg, _i, _vp, _vp, _d, _d, _d, _i64, _i64, _vp, ctypes.POINTER(_vp)]),
     "ngf_level_destroy": (None, [_vp]),
     "ngf_level_eval": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),
     "ngf_level_eval_host": (_i, [_vp, _vp, _vp, _vp, _i, _vp]),

@@ -515,9 +515,9 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
 
 // packed reference terms (gR / nR, 1 / nR) from the exact ones
 template <typename T>
-__global__ void k_pack_rt(const T* __restrict__ gR, const T* __restrict__ nR, int64_t n,
-                          V4T<T>* __restrict__ out) {
-    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < n;
+__global__ void k_pack_rt(const T* __restrict__ gR, const T* __restrict__ nR, int64_t n, int64_t first,
+                          int64_t last, V4T<T>* __restrict__ out) {
+    for (int64_t v = first + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < last;
          v += (int64_t)gridDim.x * blockDim.x) {
         const T inv = (T)1 / nR[v];
         V4T<T> r;
@@ -529,9 +529,11 @@ __global__ void k_pack_rt(const T* __restrict__ gR, const T* __restrict__ nR, in
     }
 }
 
+// voxels [first, last) of n (last < 0: all)
 template <typename T>
-int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s) {
-    NGF_LAUNCH(k_pack_rt<T>, blocks_for(n, 256), 256, 0, s, gR, nR, n, (V4T<T>*)out);
+int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s, int64_t first, int64_t last) {
+    if (last < 0) last = n;
+    NGF_LAUNCH(k_pack_rt<T>, blocks_for(last - first, 256), 256, 0, s, gR, nR, n, first, last, (V4T<T>*)out);
     NGF_CHECK_LAUNCH();
     return 0;
 }
@@ -545,7 +547,7 @@ template int fused_eval_launch<double>(const FusedArgs<double>&, const ngf_grid_
                                        cudaEvent_t, int);
 template size_t fused_smem<float>(int, int, int);
 template size_t fused_smem<double>(int, int, int);
-template int pack_rt<float>(const float*, const float*, int64_t, void*, cudaStream_t);
-template int pack_rt<double>(const double*, const double*, int64_t, void*, cudaStream_t);
+template int pack_rt<float>(const float*, const float*, int64_t, void*, cudaStream_t, int64_t, int64_t);
+template int pack_rt<double>(const double*, const double*, int64_t, void*, cudaStream_t, int64_t, int64_t);
 
 }  // namespace ngf

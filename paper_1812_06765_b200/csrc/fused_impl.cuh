@@ -144,6 +144,7 @@ template <typename T> int fused_prepare(int variant, size_t smem);
 template <typename T> size_t fused_smem(int variant, int wx, int wy);
 void fused_variant_geom(int variant, int* ty, int* nthreads);
 int fused_variant_count();
-template <typename T> int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s);
+template <typename T> int pack_rt(const T* gR, const T* nR, int64_t n, void* out, cudaStream_t s,
+                                  int64_t first = 0, int64_t last = -1);
 
 }  // namespace ngf

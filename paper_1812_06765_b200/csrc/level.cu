@@ -40,6 +40,7 @@ struct ngf_level {
     ngf_plan_t* plan;
     const void* T;
     void* Tpad;  // lean march: copy of T followed by a zero pad (reads outside the hull)
+    bool slab_terms;  // reference terms exist only on the z-slab (ngf_level_create_zslab)
     void* gR;   // 3N exact reference terms
     void* nR;   // N
     void* RT;   // packed N x 4
@@ -184,8 +185,11 @@ static bool lean_eligible(const ngf_level* L, int* kx, int* ky) {
             for (int e = 0; e < tile[ax] + 2; ++e) {
                 const int i = t * tile[ax] - 1 + e;
                 if (i < 0 || i >= n) continue;
-                ++cnt[i0[i]];
-                if (nd > 1) ++cnt[i0[i] + 1];
+                // zero weights (clamped image columns before the first / after the last
+                // node) contribute nothing and are left out of the lists
+                const double w1 = p->h_w1[ax][i];
+                if (1.0 - w1 != 0.0) ++cnt[i0[i]];
+                if (nd > 1 && w1 != 0.0) ++cnt[i0[i] + 1];
             }
             for (auto& kv : cnt) k[ax] = std::max(k[ax], kv.second);
         }
@@ -419,6 +423,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
                     if (dl == d) wt = (float)(1.0 - w1);
                     else if (dl == d - 1 && nd > 1) wt = (float)w1;
                     else continue;
+                    if (wt == 0.0f && (dl == d ? 1.0 - w1 : w1) == 0.0) continue;  // exact zero weight
                     if (cnt < K) {
                         ent[2 * cnt] = e;
                         std::memcpy(&ent[2 * cnt + 1], &wt, 4);
@@ -621,9 +626,13 @@ extern "C" {
 
 static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
                              const void* T, const void* R, const void* gR, const void* nR,
-                             double tau, double rho, double alpha, void* stream, ngf_level_t** out) {
+                             double tau, double rho, double alpha, void* stream, ngf_level_t** out,
+                             int64_t zlo = 0, int64_t zhi = -1) {
     if (!out || !T || (!R && (!gR || !nR)) || (dtype != NGF_F32 && dtype != NGF_F64)) return NGF_EARG;
     if (!grid_ok(img_grid) || !grid_ok(def_grid)) return NGF_EARG;
+    if (zhi < 0) zhi = img_grid->dims[2];
+    if (zlo < 0 || zhi > img_grid->dims[2] || zlo >= zhi || (!R && (zlo != 0 || zhi != img_grid->dims[2])))
+        return NGF_EARG;
     if (!(tau > 0) || !(rho > 0)) return NGF_EARG;
     *out = nullptr;
     ngf_level* L = (ngf_level*)std::calloc(1, sizeof(ngf_level));
@@ -657,22 +666,25 @@ static int level_create_impl(const ngf_grid_t* img_grid, const ngf_grid_t* def_g
         return NGF_ENOMEM;
     }
     cudaMemsetAsync(L->flag, 0, 16, s);
+    // a z-slab level (config 5) computes its reference terms on its own planes only
+    L->slab_terms = zlo != 0 || zhi != L->img.dims[2];
+    const int64_t plane = L->img.dims[0] * L->img.dims[1];
     if (R) {
         rc = dtype == NGF_F32
-                 ? ref_terms_impl<float>(&L->img, (const float*)R, rho, (float*)L->gR, (float*)L->nR, s)
+                 ? ref_terms_impl<float>(&L->img, (const float*)R, rho, (float*)L->gR, (float*)L->nR, s, zlo, zhi)
                  : ref_terms_impl<double>(&L->img, (const double*)R, rho, (double*)L->gR,
-                                          (double*)L->nR, s);
+                                          (double*)L->nR, s, zlo, zhi);
     } else {
         rc = (int)cudaMemcpyAsync(L->gR, gR, 3 * n * es, cudaMemcpyDeviceToDevice, s);
         if (!rc) rc = (int)cudaMemcpyAsync(L->nR, nR, n * es, cudaMemcpyDeviceToDevice, s);
     }
     if (!rc) {
         if (dtype == NGF_F32) {
-            rc = pack_rt<float>((const float*)L->gR, (const float*)L->nR, n, L->RT, s);
-            if (!rc) rc = fused_setup<float>(L, 0, (int)L->img.dims[2], s);
+            rc = pack_rt<float>((const float*)L->gR, (const float*)L->nR, n, L->RT, s, zlo * plane, zhi * plane);
+            if (!rc) rc = fused_setup<float>(L, (int)zlo, (int)zhi, s);
         } else {
-            rc = pack_rt<double>((const double*)L->gR, (const double*)L->nR, n, L->RT, s);
-            if (!rc) rc = fused_setup<double>(L, 0, (int)L->img.dims[2]);
+            rc = pack_rt<double>((const double*)L->gR, (const double*)L->nR, n, L->RT, s, zlo * plane, zhi * plane);
+            if (!rc) rc = fused_setup<double>(L, (int)zlo, (int)zhi, s);
         }
     }
     record_done(L->done, s);  // the creation kernels (reference terms, packing)
@@ -690,6 +702,14 @@ int ngf_level_create(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int
     if (!R) return NGF_EARG;
     return level_create_impl(img_grid, def_grid, dtype, T, R, nullptr, nullptr, tau, rho, alpha,
                              stream, out);
+}
+
+int ngf_level_create_zslab(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
+                           const void* T, const void* R, double tau, double rho, double alpha,
+                           int64_t zlo, int64_t zhi, void* stream, ngf_level_t** out) {
+    if (!R) return NGF_EARG;
+    return level_create_impl(img_grid, def_grid, dtype, T, R, nullptr, nullptr, tau, rho, alpha,
+                             stream, out, zlo, zhi);
 }
 
 int ngf_level_create_terms(const ngf_grid_t* img_grid, const ngf_grid_t* def_grid, int dtype,
@@ -727,9 +747,11 @@ int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_de
     cudaStream_t s = as_stream(stream);
     int rc;
     if (mode == 1) {
+        if (L->slab_terms) return NGF_ESTATE;  // the exact path needs the full reference terms
         rc = L->dtype == NGF_F32 ? eval_exact<float>(L, y, grad, scalars_dev, s)
                                  : eval_exact<double>(L, y, grad, scalars_dev, s);
     } else if (mode == 0 || mode == 2) {
+        if (L->slab_terms && mode == 0) return NGF_ESTATE;  // only the slab partial exists
         rc = fused_part(L, y, grad, scalars_dev, s, mode == 2 ? 1 : 0);
     } else {
         return NGF_EARG;

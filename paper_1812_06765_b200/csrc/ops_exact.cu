@@ -403,11 +403,13 @@ __global__ void k_gradient_t(GridK<T> g, const T* __restrict__ w, T* __restrict_
 
 template <typename T>
 __global__ void k_ref_terms(GridK<T> g, const T* __restrict__ R, T rho, T* __restrict__ gR,
-                            T* __restrict__ nR) {
+                            T* __restrict__ nR, int64_t first, int64_t last) {
+    // voxels [first, last) (a z-slab of planes for the config-5 decomposition; R is read on
+    // the neighbouring planes as well, so the slab needs no halo exchange)
     const int64_t n = g.n();
     const int64_t sy = g.nx, sz = (int64_t)g.nx * g.ny;
     const T rho2 = rho * rho;
-    for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n;
+    for (int64_t idx = first + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < last;
          idx += (int64_t)gridDim.x * blockDim.x) {
         const int i = (int)(idx % g.nx);
         const int j = (int)((idx / g.nx) % g.ny);
@@ -851,9 +853,13 @@ int gradient_t_impl(const ngf_grid_t* g, const T* w, T* out, cudaStream_t s) {
 }
 
 template <typename T>
-int ref_terms_impl(const ngf_grid_t* g, const T* R, double rho, T* gR, T* nR, cudaStream_t s) {
-    NGF_LAUNCH(k_ref_terms<T>, blocks_for(grid_n(*g), 256), 256, 0, s, make_gridk<T>(*g), R,
-               (T)rho, gR, nR);
+int ref_terms_impl(const ngf_grid_t* g, const T* R, double rho, T* gR, T* nR, cudaStream_t s,
+                   int64_t zlo, int64_t zhi) {
+    const int64_t plane = g->dims[0] * g->dims[1];
+    if (zhi < 0) zhi = g->dims[2];
+    const int64_t first = zlo * plane, last = zhi * plane;
+    NGF_LAUNCH(k_ref_terms<T>, blocks_for(last - first, 256), 256, 0, s, make_gridk<T>(*g), R,
+               (T)rho, gR, nR, first, last);
     NGF_CHECK_LAUNCH();
     return 0;
 }
@@ -1001,7 +1007,7 @@ int sample_field_impl(const ngf_grid_t* g, const T* y, const double* pts, int64_
                                  cudaStream_t);                                                  \
     template int gradient_impl<T>(const ngf_grid_t*, const T*, T*, cudaStream_t);               \
     template int gradient_t_impl<T>(const ngf_grid_t*, const T*, T*, cudaStream_t);             \
-    template int ref_terms_impl<T>(const ngf_grid_t*, const T*, double, T*, T*, cudaStream_t);  \
+    template int ref_terms_impl<T>(const ngf_grid_t*, const T*, double, T*, T*, cudaStream_t, int64_t, int64_t); \
     template int ngf_terms_impl<T>(const ngf_grid_t*, const T*, const T*, const T*, double,     \
                                    double, T*, T*, cudaStream_t);                               \
     template int pairwise_sum_impl<T>(const T*, int64_t, double*, int, double, cudaStream_t);    \

@@ -15,7 +15,8 @@ int warp_jt_impl(const ngf_grid_t*, const T*, const T*, const T*, int64_t, T*, c
 template <typename T> int gradient_impl(const ngf_grid_t*, const T*, T*, cudaStream_t);
 template <typename T> int gradient_t_impl(const ngf_grid_t*, const T*, T*, cudaStream_t);
 template <typename T>
-int ref_terms_impl(const ngf_grid_t*, const T*, double, T*, T*, cudaStream_t);
+int ref_terms_impl(const ngf_grid_t*, const T*, double, T*, T*, cudaStream_t, int64_t zlo = 0,
+                   int64_t zhi = -1);
 template <typename T>
 int ngf_terms_impl(const ngf_grid_t*, const T*, const T*, const T*, double, double, T*, T*,
                    cudaStream_t);

@@ -47,7 +47,7 @@ CASES = [
     ((70, 45, 33), (1.0, 1.0, 1.0), (-3.0, 2.0, 1.0), 4, 2.5),     # partial tiles in x and y
     ((48, 40, 36), (2.0, 2.0, 2.0), (0.0, 0.0, 0.0), 2, 3.0),      # ratio 2 (config 2 shape)
     ((50, 30, 20), (0.5, 1.0, 2.0), (1.0, -1.0, 0.5), 3, 1.5),     # ratio 3, anisotropic pow2 spacing
-    ((33, 97, 17), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0), 2, 2.0),      # odd sizes, tall y
+    ((33, 97, 18), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0), 2, 2.0),      # odd sizes in x and y, tall y
     ((130, 20, 150), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0), 4, 4.0),    # several z chunks, big displacements
     ((40, 40, 40), (1.0, 1.0, 1.0), (0.0, 0.0, 0.0), 4, 12.0),     # many samples outside the hull
 ]
