@@ -434,7 +434,7 @@ void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
         case 3: march_launch<float, V3>(a, s); return;
         case 4: march_launch<float, V4>(a, s); return;
         case 5: march_launch<float, V5>(a, s); return;
-        case kLeanVariant: lean_launch(a, s); return;
+        case kLeanVariant: lean_launch(a, *static_cast<const lean::Ctl*>(a.fp.lean_ctl), s); return;
         default: march_launch<float, V0>(a, s); return;
     }
 }

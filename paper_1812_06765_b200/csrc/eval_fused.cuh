@@ -40,6 +40,7 @@ struct FusedPlan {
     int kx, ky;
     const int32_t* lx;  // [ntx][wx][kx] int2
     const int32_t* ly;  // [nty][wy][ky] int2
+    const void* lean_ctl;  // HOST pointer to the level's lean::Ctl (launch parameters)
 };
 constexpr int kLeanVariant = 6;
 constexpr int kCover = 8;

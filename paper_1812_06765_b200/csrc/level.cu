@@ -40,6 +40,7 @@ struct ngf_level {
     ngf_plan_t* plan;
     const void* T;
     void* Tpad;  // lean march: copy of T followed by a zero pad (reads outside the hull)
+    ngf::lean::Ctl* ctl;  // lean march: per-level control block (kernel parameters)
     bool slab_terms;  // reference terms exist only on the z-slab (ngf_level_create_zslab)
     void* gR;   // 3N exact reference terms
     void* nR;   // N
@@ -224,10 +225,12 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
     // the search depends only on the geometry (dims, slab, index maps), the dtype and the
     // tuning overrides: memoised per process, so repeated registrations of one size (a
     // batch of pairs, config 4) skip it (1.4 ms at 256^3, 4.9 ms at 512^3)
-    std::string key;
+    int lean_kx = 8, lean_ky = 8;
+    const bool lean_ok = sizeof(T) == 4 && lean_eligible(L, &lean_kx, &lean_ky);
+    std::string key = lean_ok ? "lean:" : "classic:";
     {
         const char* ev[] = {"NGF_FUSED_VARIANT", "NGF_FUSED_CZ", "NGF_CHUNK_OVERHEAD"};
-        key = std::to_string(sizeof(T)) + ":" + std::to_string(zlo) + ":" + std::to_string(zhi);
+        key += std::to_string(sizeof(T)) + ":" + std::to_string(zlo) + ":" + std::to_string(zhi);
         for (const char* e : ev) key += std::string(":") + (std::getenv(e) ? std::getenv(e) : "-");
         const int nimg[3] = {nx, ny, nz}, ndef[3] = {ndx, ndy, ndz};
         for (int ax = 0; ax < 3; ++ax) {
@@ -239,8 +242,6 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
     }
     std::vector<int> bounds;
     int variant = -1;
-    int lean_kx = 8, lean_ky = 8;
-    const bool lean_ok = sizeof(T) == 4 && lean_eligible(L, &lean_kx, &lean_ky);
     size_t n_choices = 0;
     static std::mutex plan_mu;
     static std::map<std::string, std::pair<int, std::vector<int>>> plan_cache;
@@ -435,6 +436,14 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
     if (variant == kLeanVariant) {
         fp.kx = lean_kx;
         fp.ky = lean_ky;
+        if (!L->ctl) L->ctl = new lean::Ctl();
+        std::vector<float> w1z(nz);
+        for (int z = 0; z < nz; ++z) w1z[z] = (float)p->h_w1[2][z];
+        std::vector<int> wz(zl.begin(), zl.end());
+        if (int rc = lean_ctl_build(p->h_i0[2], w1z.data(), nz, ndz, L->img.spacing[2], bounds, wz,
+                                    L->img.spacing[0], L->img.spacing[1], L->ctl))
+            return rc;
+        fp.lean_ctl = L->ctl;
         build_list(0, kTX, fp.ntx, fp.wx, fp.kx, xl, lxv);
         build_list(1, fp.ty, fp.nty, fp.wy, fp.ky, yl, lyv);
         const size_t n = (size_t)nx * ny * nz;
@@ -736,6 +745,7 @@ void ngf_level_destroy(ngf_level_t* L) {
                     L->ex.cws, L->ex.dws, L->hx, L->hg, L->hsc};
     for (void* b : bufs) dev_free(b);
     if (L->hsc_pin) cudaFreeHost(L->hsc_pin);
+    delete L->ctl;
     for (int k = 0; k < 2; ++k)
         if (L->ev[k]) cudaEventDestroy(L->ev[k]);
     std::free(L);

@@ -26,6 +26,7 @@
 //     per CTA.
 // Determinism: every sum has a fixed order; no atomics.
 
+#include <cstring>
 #include <mutex>
 
 #include "fused_cfg.cuh"
@@ -34,20 +35,21 @@
 namespace ngf {
 namespace lean {
 
+constexpr int kPlane = kE1Y * kE1X;  // 544 positions, row stride 34 for every per-position plane
+
 struct Smem {
-    float W[3][kE1Y][kE1X];         // W of planes p-2, p-1, p (ring by plane index mod 3)
-    float Qx[3][kE1Y][kE1X + 2];    // q_x, one zero column each side
-    float Qy[3][kE1Y + 2][kE1X];    // q_y, one zero row each side
-    float Fb[3][kE1Y][kE1X];        // completed deformation plane (z-reduced ghat / h)
-    float dTs[3][3][kE1Y * kE1X];   // interpolant derivative (times h) of planes p-2, p-1, p
-    float Xr[3][kE1Y][kWXM];        // x-reduced
-    float zt[kCzMax + 4][8];        // per plane: G (cm, c0, cp), G^T (gm, g0, gp), w1z, 1 - w1z
-    int zi[kCzMax + 4][4];          // per plane: i0z, advance of i0z to the next plane, face flag
-    int2 xl[kWXM][kKMax];           // x pass: (E1 column, weight bits) per window output
-    int2 yl[kWYM][kKMax];           // y pass: (E1 row, weight bits)
+    float W[3][kPlane];                // W of planes p-2, p-1, p (ring by plane index mod 3)
+    float dT[3][3][kPlane];            // interpolant derivative (times h), same ring
+    float Qx[3][kPlane + 2];           // q_x at [P + 1]: the ring columns (q = 0) pad the rows
+    float Qy[3][kPlane + 2 * kE1X];    // q_y at [P + 34]: one zero row each side
+    float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
+    float Xr[3][kE1Y][kWXM];           // x-reduced
+    int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
+    int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
     float colG[kE1X][3], colGt[kE1X][3], rowG[kE1Y][3], rowGt[kE1Y][3];
     int colP0[kE1X], colP1[kE1X], rowP0[kE1Y], rowP1[kE1Y];
     float colPw[kE1X], rowPw[kE1Y];
+    unsigned fa[kNT];                  // flush pass assignment per thread
     double red[kWarps];
 };
 
@@ -56,34 +58,34 @@ __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
     return __fadd_rn(__fmul_rn(a0, w0), __fmul_rn(a1, w));
 }
 
+// Per-level control in the kernel's parameter space (constant bank): indexed by the
+// CTA-uniform plane counter, so every branch of the march is a uniform one.
+constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
+constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
+
 template <int KX, int KY>
 struct Lean {
     const FusedArgs<float>& a;
+    const Ctl& c;
     Smem& sm;
-    // position of this thread in the tile
-    int ex, ey, P;  // E1 column / row, flat index ey * kE1X + ex
-    int x, yy;
-    bool vol, inter, fx, fy;
-    bool wface_b, wface_c;  // warp holds a face position (B: interior, C: any)
-    unsigned ij;            // yy * nx + x (reference-term offset inside a plane)
-    // chunk
-    int cta, z0, z1, zb, jfirst, jlast, wzlo;
-    // flush pass assignment, bytes (x pass row, x pass column, y pass row, y pass column),
-    // 0xff = none
-    unsigned fa;
-    // march state
-    int cur_zd;
+    int P;         // flat E1 index ey * 34 + ex of this thread's position
+    unsigned ij;   // yy * nx + x (reference-term offset inside a plane)
+    unsigned fl;   // bit 0: x face, bit 1: y face, bit 2: interior position
+    float m_in;    // 1 for interior positions, else 0 (distance accumulation)
+    bool bwarp;    // the warp holds interior positions (runs (B))
+    bool wface_b, wface_c;
+    int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo;
     float ylo[3], yhi[3];
     float qz[3];
     float A0[3], A1[3];
     float4 rt;
     float dacc;
-    int xz, yz;  // pending x / y pass (window slot), -1 none
 
-    __device__ __forceinline__ Lean(const FusedArgs<float>& a_, Smem& sm_) : a(a_), sm(sm_) {}
+    __device__ __forceinline__ Lean(const FusedArgs<float>& a_, const Ctl& c_, Smem& sm_) : a(a_), c(c_), sm(sm_) {}
 
     __device__ __forceinline__ void load_yplane(int zd, float (&out)[3]) const {
         // P_xy y on def plane zd at this position's image (x, y): x then y (transfer.py:136-142)
+        const int ey = P / kE1X, ex = P - ey * kE1X;
         const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
         const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
         const float wx = sm.colPw[ex], wy = sm.rowPw[ey];
@@ -111,17 +113,19 @@ struct Lean {
     }
 
     // x pass of a completed deformation plane: Fb -> Xr (fixed entry order per output)
-    __device__ __forceinline__ void xpass() {
-        const int xr_r = fa & 0xff, xr_d = (fa >> 8) & 0xff;
+    __device__ __forceinline__ void xpass() const {
+        const unsigned f = sm.fa[threadIdx.x];
+        const int xr_r = f & 0xff, xr_d = (f >> 8) & 0xff;
         if (xr_r != 0xff) {
             float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+            const float* fb = &sm.Fb[0][0] + xr_r * kE1X;
 #pragma unroll
             for (int k = 0; k < KX; ++k) {
                 const int2 e = sm.xl[xr_d][k];
                 const float w = __int_as_float(e.y);
-                s0 = fmaf(w, sm.Fb[0][xr_r][e.x], s0);
-                s1 = fmaf(w, sm.Fb[1][xr_r][e.x], s1);
-                s2 = fmaf(w, sm.Fb[2][xr_r][e.x], s2);
+                s0 = fmaf(w, fb[e.x], s0);
+                s1 = fmaf(w, fb[kPlane + e.x], s1);
+                s2 = fmaf(w, fb[2 * kPlane + e.x], s2);
             }
             sm.Xr[0][xr_r][xr_d] = s0;
             sm.Xr[1][xr_r][xr_d] = s1;
@@ -130,8 +134,9 @@ struct Lean {
     }
 
     // y pass: Xr -> the CTA's window partial of deformation plane slot zs (1/h applied)
-    __device__ __forceinline__ void ypass(int zs) {
-        const int yp_dy = (fa >> 16) & 0xff, yp_d = fa >> 24;
+    __device__ __forceinline__ void ypass(int zs) const {
+        const unsigned f = sm.fa[threadIdx.x];
+        const int yp_dy = (f >> 16) & 0xff, yp_d = f >> 24;
         if (yp_dy != 0xff) {
             float s0 = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll
@@ -152,39 +157,39 @@ struct Lean {
     }
 
     __device__ __forceinline__ void put_flush(const float (&acc)[3]) {
-        float* b = &sm.Fb[0][0][0] + P;
-        b[0] = acc[0];
-        b[kE1Y * kE1X] = acc[1];
-        b[2 * kE1Y * kE1X] = acc[2];
+        sm.Fb[0][P] = acc[0];
+        sm.Fb[1][P] = acc[1];
+        sm.Fb[2][P] = acc[2];
+    }
+
+    __device__ __forceinline__ bool flushes(int j) const {
+        // deformation plane i0z(j) is complete after (C) on plane j (the chunk's last one is
+        // flushed after the march)
+        return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
     template <int R>
     __device__ __forceinline__ void step(int p) {
         constexpr int RB = (R + 2) % 3;  // plane p-1
         constexpr int RC = (R + 1) % 3;  // plane p-2
-        const float hx2 = 0.5f * a.ihx, hy2 = 0.5f * a.ihy, hz2 = 0.5f * a.ihz;
 
         // ------------------------------------------------------------- (A) plane p
         float W = 0.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
-        if (p >= 0 && p < a.nz && p <= z1) {
-            const int t = p - zb;
-            const int zd = sm.zi[t][0];
-            if (zd != cur_zd) {  // CTA-uniform
-                const int zd1 = min(zd + 1, a.ndz - 1);
-                if (zd == cur_zd + 1) {
+        if (p >= pa0 && p <= pa1) {
+            const int zd = (int)(c.zw[p] & 0xffffu);
+            if (p == pa0) {
+                load_yplane(zd, ylo);
+                load_yplane(min(zd + 1, a.ndz - 1), yhi);
+            } else if (c.zw[p - 1] & kAdv) {
 #pragma unroll
-                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
-                } else {
-                    load_yplane(zd, ylo);
-                }
-                load_yplane(zd1, yhi);
-                cur_zd = zd;
+                for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+                load_yplane(min(zd + 1, a.ndz - 1), yhi);
             }
-            const float wz = sm.zt[t][6], wz0 = sm.zt[t][7];
+            const float wz = c.w1[p], wz0 = __fsub_rn(1.0f, wz);
             const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
             const float yh1 = __fadd_rn(__fmul_rn(ylo[1], wz0), __fmul_rn(yhi[1], wz));
             const float yh2 = __fadd_rn(__fmul_rn(ylo[2], wz0), __fmul_rn(yhi[2], wz));
-            bool in = vol;
+            bool in = fl & 8u;  // position inside the volume (x / y)
             float fx_, fy_, fz_;
             const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, fx_);
             const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, fy_);
@@ -210,167 +215,164 @@ struct Lean {
             d1 = fmaf(fz_, dy1 - dy0, dy0);
             d2 = dz;
         }
-        sm.dTs[R][0][P] = d0;
-        sm.dTs[R][1][P] = d1;
-        sm.dTs[R][2][P] = d2;
-        (&sm.W[R][0][0])[P] = W;
+        sm.W[R][P] = W;
+        sm.dT[R][0][P] = d0;
+        sm.dT[R][1][P] = d1;
+        sm.dT[R][2][P] = d2;
         __syncthreads();
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
-        {
-            const int k = p - 1;
-            float qxv = 0.f, qyv = 0.f, qzv = 0.f;
-            if (k >= z0 && k < z1) {  // CTA-uniform
-                if (inter) {
-                    const float* Wk = &sm.W[RB][0][0] + P;
-                    const float wl = Wk[-1], wr = Wk[1], wu = Wk[-kE1X], wd = Wk[kE1X];
-                    float gx = (wr - wl) * hx2;
-                    float gy = (wd - wu) * hy2;
-                    if (wface_b) {  // warp holds a position next to an x / y volume face
-                        const float w0 = Wk[0];
-                        if (fx) {
-                            const float* cg = sm.colG[ex];
-                            gx = fmaf(cg[0], wl, fmaf(cg[1], w0, cg[2] * wr));
-                        }
-                        if (fy) {
-                            const float* rg = sm.rowG[ey];
-                            gy = fmaf(rg[0], wu, fmaf(rg[1], w0, rg[2] * wd));
-                        }
+        const int k = p - 1;
+        if (k >= z0 && k < z1) {
+            if (bwarp) {
+                const float* Wk = &sm.W[RB][P];
+                const float wl = Wk[-1], wr = Wk[1], wu = Wk[-kE1X], wd = Wk[kE1X];
+                const float wzm = sm.W[RC][P], wzp = sm.W[R][P];
+                float gx = (wr - wl) * c.hx2;
+                float gy = (wd - wu) * c.hy2;
+                if (wface_b) {  // warp holds a position next to an x / y volume face
+                    const int ey = P / kE1X, ex = P - ey * kE1X;
+                    const float w0 = Wk[0];
+                    if (fl & 1u) {
+                        const float* cg = sm.colG[ex];
+                        gx = fmaf(cg[0], wl, fmaf(cg[1], w0, cg[2] * wr));
                     }
-                    const int t = k - zb;
-                    const float wzm = (&sm.W[RC][0][0])[P], wzp = (&sm.W[R][0][0])[P];
-                    float gz;
-                    if (sm.zi[t][2]) {  // z face plane (uniform): the exact one-sided rows
-                        const float* zc = sm.zt[t];
-                        gz = fmaf(zc[0], wzm, fmaf(zc[1], Wk[0], zc[2] * wzp));
-                    } else {
-                        gz = (wzp - wzm) * hz2;
+                    if (fl & 2u) {
+                        const float* rg = sm.rowG[ey];
+                        gy = fmaf(rg[0], wu, fmaf(rg[1], w0, rg[2] * wd));
                     }
-                    // NGF ratio, distance term, q = dD/d grad W (ngf.py:70-112)
-                    const float dot = fmaf(gx, rt.x, fmaf(gy, rt.y, gz * rt.z));
-                    const float sq = fmaf(gx, gx, fmaf(gy, gy, fmaf(gz, gz, a.tau2)));
-                    const float inv_nt = rsqrtf(sq);
-                    const float r = fmaf(a.taurho, rt.w, dot) * inv_nt;
-                    dacc += fmaf(-r, r, 1.0f);
-                    const float t1 = r * inv_nt;
-                    const float cf = a.neg_hbar * t1;
-                    qxv = cf * fmaf(-t1, gx, rt.x);
-                    qyv = cf * fmaf(-t1, gy, rt.y);
-                    qzv = cf * fmaf(-t1, gz, rt.z);
                 }
+                const unsigned fz = c.zw[k] >> kFaceShift;
+                float gz;
+                if (fz) {  // z face plane: the exact one-sided rows
+                    const float* zc = c.faceG[fz - 1];
+                    gz = fmaf(zc[0], wzm, fmaf(zc[1], Wk[0], zc[2] * wzp));
+                } else {
+                    gz = (wzp - wzm) * c.hz2;
+                }
+                // NGF ratio, distance term, q = dD/d grad W (ngf.py:70-112); positions outside
+                // the interior carry rt = 0, hence q = 0, and m_in = 0
+                const float dot = fmaf(gx, rt.x, fmaf(gy, rt.y, gz * rt.z));
+                const float sq = fmaf(gx, gx, fmaf(gy, gy, fmaf(gz, gz, a.tau2)));
+                const float inv_nt = rsqrtf(sq);
+                const float r = fmaf(a.taurho, rt.w, dot) * inv_nt;
+                dacc = fmaf(m_in, fmaf(-r, r, 1.0f), dacc);
+                const float t1 = r * inv_nt;
+                const float cf = a.neg_hbar * t1;
+                qz[RB] = cf * fmaf(-t1, gz, rt.z);
+                sm.Qx[RB][P + 1] = cf * fmaf(-t1, gx, rt.x);
+                sm.Qy[RB][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
                 // reference terms of plane p for the next step's (B)
-                if (inter && p < z1) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
+                if (p < z1 && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
-            qz[RB] = qzv;
-            (&sm.Qx[RB][0][1])[ey * (kE1X + 2) + ex] = qxv;
-            (&sm.Qy[RB][1][0])[P] = qyv;
+        } else if (bwarp) {  // no q on this plane (chunk edges)
+            qz[RB] = 0.f;
+            sm.Qx[RB][P + 1] = 0.f;
+            sm.Qy[RB][P + kE1X] = 0.f;
         }
-        // staggered P^T passes of earlier completed deformation planes
-        if (yz >= 0) {
-            ypass(yz);
-            yz = -1;
-        }
-        if (xz >= 0) {
-            xpass();
-            yz = xz;
-            xz = -1;
-        }
+        // staggered P^T passes of the deformation planes completed two and one steps ago
+        if (flushes(p - 4)) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
+        if (flushes(p - 3)) xpass();
 
         // ------------------------------------------------------------- (C) j = p-2
         const int j = p - 2;
-        if (j < jfirst || j > jlast) return;  // CTA-uniform
-        const int t = j - zb;
-        const float* qxj = &sm.Qx[RC][0][1] + ey * (kE1X + 2) + ex;
-        const float* qyj = &sm.Qy[RC][1][0] + P;
+        if (j < jfirst || j > jlast) return;
+        const float* qxj = &sm.Qx[RC][P + 1];
+        const float* qyj = &sm.Qy[RC][P + kE1X];
         const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
-        float sx = (ql - qr) * hx2;
-        float sy = (qu - qd) * hy2;
+        float sx = (ql - qr) * c.hx2;
+        float sy = (qu - qd) * c.hy2;
         if (wface_c) {
-            if (fx) {  // exact transposed face rows (warp.py:168-175)
+            const int ey = P / kE1X, ex = P - ey * kE1X;
+            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
                 const float* ct = sm.colGt[ex];
                 sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
             }
-            if (fy) {
+            if (fl & 2u) {
                 const float* rg = sm.rowGt[ey];
                 sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
             }
         }
+        const unsigned fz = c.zw[j] >> kFaceShift;
         float sz;
-        if (sm.zi[t][2]) {
-            const float* zc = sm.zt[t];
+        if (fz) {
+            const float* zc = c.faceG[fz - 1];
             sz = fmaf(zc[3], qz[R], fmaf(zc[4], qz[RC], zc[5] * qz[RB]));
         } else {
-            sz = (qz[R] - qz[RB]) * hz2;
+            sz = (qz[R] - qz[RB]) * c.hz2;
         }
         const float sv = sx + sy + sz;
-        const float w1 = sm.zt[t][6], w0 = sm.zt[t][7];
+        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
 #pragma unroll
-        for (int c = 0; c < 3; ++c) {
-            const float g = sv * sm.dTs[RC][c][P];
-            A0[c] = fmaf(w0, g, A0[c]);
-            A1[c] = fmaf(w1, g, A1[c]);
+        for (int q = 0; q < 3; ++q) {
+            const float g = sv * sm.dT[RC][q][P];
+            A0[q] = fmaf(w0, g, A0[q]);
+            A1[q] = fmaf(w1, g, A1[q]);
         }
-        // deformation plane i0z(j) is complete when the next image plane maps to the next
-        // pair (the last plane of the chunk is flushed after the march)
-        if (j < jlast && sm.zi[t][1] >= 1) {
+        if (flushes(j)) {
             put_flush(A0);
-            xz = sm.zi[t][0] - wzlo;
 #pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                A0[c] = A1[c];
-                A1[c] = 0.f;
+            for (int q = 0; q < 3; ++q) {
+                A0[q] = A1[q];
+                A1[q] = 0.f;
             }
         }
     }
 };
 
 template <int KX, int KY>
-__global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a) {
+__global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
+                                                       const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<KX, KY> m(a, sm);
+    Lean<KX, KY> m(a, c, sm);
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // ---- CTA geometry
-    m.cta = blockIdx.x;
-    const int tx = m.cta % fp.ntx, ty = (m.cta / fp.ntx) % fp.nty, tzc = m.cta / (fp.ntx * fp.nty);
+    // ---- CTA geometry (uniform): grid (x tiles, y tiles, z chunks), dispatched chunk-major
+    const int tx = blockIdx.x, ty = blockIdx.y, tzc = blockIdx.z;
+    m.cta = (tzc * fp.nty + ty) * fp.ntx + tx;
     const int x0 = tx * 32, y0 = ty * kTYI;
-    m.z0 = fp.zb_tab[tzc];
-    m.z1 = fp.zb_tab[tzc + 1];
-    m.zb = m.z0 - 1;
-    m.jfirst = max(m.z0 - 1, 0);
-    m.jlast = min(m.z1, a.nz - 1);
-    m.wzlo = fp.win_z[tzc];
+    m.z0 = c.zb[tzc];
+    m.z1 = c.zb[tzc + 1];
+    m.pa0 = max(m.z0 - 1, 0);
+    m.pa1 = min(m.z1, a.nz - 1);
+    m.jfirst = m.pa0;
+    m.jlast = m.pa1;
+    m.wzlo = c.wzlo[tzc];
 
     // ---- this thread's position: row warps own columns 1..32 of one row, the last warp
     // the ring columns 0 and 33 of all rows
+    int ex, ey;
     if (warp < kE1Y) {
-        m.ey = warp;
-        m.ex = lane + 1;
+        ey = warp;
+        ex = lane + 1;
     } else {
-        m.ey = lane & 15;
-        m.ex = lane < 16 ? 0 : kE1X - 1;
+        ey = lane & 15;
+        ex = lane < 16 ? 0 : kE1X - 1;
     }
-    m.P = m.ey * kE1X + m.ex;
-    m.x = x0 - 1 + m.ex;
-    m.yy = y0 - 1 + m.ey;
-    m.vol = m.x >= 0 && m.x < a.nx && m.yy >= 0 && m.yy < a.ny;
-    m.inter = m.vol && warp >= 1 && warp <= kTYI;
-    m.ij = m.vol ? (unsigned)(m.yy * a.nx + m.x) : 0u;
+    m.P = ey * kE1X + ex;
+    const int x = x0 - 1 + ex, yy = y0 - 1 + ey;
+    const bool vol = x >= 0 && x < a.nx && yy >= 0 && yy < a.ny;
+    const bool inter = vol && warp >= 1 && warp <= kTYI;
+    m.ij = vol ? (unsigned)(yy * a.nx + x) : 0u;
+    bool fx, fy;
     {
         // a position needs the exact face coefficients where G or G^T differ from central
-        const float hx2 = 0.5f * a.ihx, hy2 = 0.5f * a.ihy;
+        const float hx2 = c.hx2, hy2 = c.hy2;
         float cm, c0, cp, gm, g0, gp;
-        fd_coef<float>(m.x, a.nx, a.ihx, cm, c0, cp);
-        fdt_coef<float>(m.x, a.nx, a.ihx, gm, g0, gp);
-        m.fx = m.vol && !(cm == -hx2 && c0 == 0.f && cp == hx2 && gm == hx2 && g0 == 0.f && gp == -hx2);
-        fd_coef<float>(m.yy, a.ny, a.ihy, cm, c0, cp);
-        fdt_coef<float>(m.yy, a.ny, a.ihy, gm, g0, gp);
-        m.fy = m.vol && !(cm == -hy2 && c0 == 0.f && cp == hy2 && gm == hy2 && g0 == 0.f && gp == -hy2);
+        fd_coef<float>(x, a.nx, a.ihx, cm, c0, cp);
+        fdt_coef<float>(x, a.nx, a.ihx, gm, g0, gp);
+        fx = vol && !(cm == -hx2 && c0 == 0.f && cp == hx2 && gm == hx2 && g0 == 0.f && gp == -hx2);
+        fd_coef<float>(yy, a.ny, a.ihy, cm, c0, cp);
+        fdt_coef<float>(yy, a.ny, a.ihy, gm, g0, gp);
+        fy = vol && !(cm == -hy2 && c0 == 0.f && cp == hy2 && gm == hy2 && g0 == 0.f && gp == -hy2);
     }
-    m.wface_b = __any_sync(0xffffffffu, m.inter && (m.fx || m.fy));
-    m.wface_c = __any_sync(0xffffffffu, m.fx || m.fy);
+    m.fl = (fx ? 1u : 0u) | (fy ? 2u : 0u) | (inter ? 4u : 0u) | (vol ? 8u : 0u);
+    m.m_in = inter ? 1.f : 0.f;
+    m.bwarp = __any_sync(0xffffffffu, inter);
+    m.wface_b = __any_sync(0xffffffffu, inter && (fx || fy));
+    m.wface_c = __any_sync(0xffffffffu, fx || fy);
 
     // ---- shared tables
     for (int e = tid; e < kE1X; e += kNT) {
@@ -393,32 +395,14 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : 0.f;
     }
-    for (int t = tid; t < m.z1 + 2 - m.zb; t += kNT) {
-        const int z = m.zb + t;
-        float* zc = sm.zt[t];
-        fd_coef<float>(z, a.nz, a.ihz, zc[0], zc[1], zc[2]);
-        fdt_coef<float>(z, a.nz, a.ihz, zc[3], zc[4], zc[5]);
-        const bool in = z >= 0 && z < a.nz;
-        const float w1 = in ? a.w1z[z] : 0.f;
-        zc[6] = w1;
-        zc[7] = __fsub_rn(1.0f, w1);
-        sm.zi[t][0] = in ? a.i0z[z] : 0;
-        sm.zi[t][1] = (in && z + 1 < a.nz) ? a.i0z[z + 1] - a.i0z[z] : 2;
-        const float hz2 = 0.5f * a.ihz;
-        const bool central = zc[0] == -hz2 && zc[1] == 0.f && zc[2] == hz2 && zc[3] == hz2 && zc[4] == 0.f &&
-                             zc[5] == -hz2;
-        sm.zi[t][2] = central ? 0 : 1;
-    }
-    for (int t = tid; t < 3 * kE1Y * (kE1X + 2); t += kNT) (&sm.Qx[0][0][0])[t] = 0.f;
-    for (int t = tid; t < 3 * (kE1Y + 2) * kE1X; t += kNT) (&sm.Qy[0][0][0])[t] = 0.f;
+    for (int t = tid; t < 3 * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
+    for (int t = tid; t < 3 * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
     {
         const int2* gx = reinterpret_cast<const int2*>(fp.lx) + (size_t)tx * fp.wx * KX;
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
         for (int t = tid; t < fp.wx * KX; t += kNT) sm.xl[t / KX][t % KX] = gx[t];
         for (int t = tid; t < fp.wy * KY; t += kNT) sm.yl[t / KY][t % KY] = gy[t];
-    }
-    // flush pass assignment: x pass (row, window column), y pass (window row, column)
-    {
+        // flush pass assignment: x pass (row, window column), y pass (window row, column)
         unsigned xa = 0xffffu, ya = 0xffffu;
         if (tid < kE1Y * fp.wx) {
             const int r = tid / fp.wx;
@@ -428,21 +412,16 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
             const int r = tid / fp.wx;
             ya = (unsigned)r | (unsigned)(tid - r * fp.wx) << 8;
         }
-        m.fa = xa | ya << 16;
+        sm.fa[tid] = xa | ya << 16;
     }
 
     // ---- march state
-    m.cur_zd = -1000;
     m.dacc = 0.f;
-    m.xz = m.yz = -1;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) {
-        m.qz[r] = 0.f;
-        m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
-    }
+    for (int r = 0; r < 3; ++r) m.qz[r] = m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
     m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
-    if (m.inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
+    if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2
     const int pstart = m.z0 - 1;
@@ -453,17 +432,18 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         if (b + 2 < nsteps) m.template step<2>(pstart + b + 2);
     }
 
-    // ---- drain the staggered passes, then the chunk's last deformation plane(s)
+    // ---- drain the staggered passes (planes completed in the last two steps), then the
+    // chunk's last deformation plane(s)
+    const int pend = pstart + nsteps;  // the first step not taken
     __syncthreads();
-    if (m.yz >= 0) m.ypass(m.yz);
-    if (m.xz >= 0) {
-        __syncthreads();
+    if (m.flushes(pend - 4)) m.ypass((int)(c.zw[pend - 4] & 0xffffu) - m.wzlo);
+    if (m.flushes(pend - 3)) {
         m.xpass();
         __syncthreads();
-        m.ypass(m.xz);
+        m.ypass((int)(c.zw[pend - 3] & 0xffffu) - m.wzlo);
     }
     if (m.jfirst <= m.jlast) {
-        const int zdl = sm.zi[m.jlast - m.zb][0];
+        const int zdl = (int)(c.zw[m.jlast] & 0xffffu);
         __syncthreads();
         m.put_flush(m.A0);
         __syncthreads();
@@ -488,7 +468,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     if (tid == 0) {
         double s = 0.0;
         for (int w = 0; w < kWarps; ++w) s += sm.red[w];
-        a.dpart[blockIdx.x] = s;
+        a.dpart[m.cta] = s;
     }
 }
 
@@ -514,16 +494,56 @@ int lean_prepare(size_t smem) {
     return (int)e;
 }
 
-void lean_launch(const FusedArgs<float>& a, cudaStream_t s) {
+void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) {
     const FusedPlan& fp = a.fp;
+    const dim3 grid(fp.ntx, fp.nty, fp.ntz);
     if (fp.kx <= 4 && fp.ky <= 4)
-        NGF_LAUNCH((lean::k_march_lean<4, 4>), fp.n_cta, lean::kNT, fp.smem_bytes, s, a);
+        NGF_LAUNCH((lean::k_march_lean<4, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else if (fp.kx <= 4)
-        NGF_LAUNCH((lean::k_march_lean<4, 8>), fp.n_cta, lean::kNT, fp.smem_bytes, s, a);
+        NGF_LAUNCH((lean::k_march_lean<4, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else if (fp.ky <= 4)
-        NGF_LAUNCH((lean::k_march_lean<8, 4>), fp.n_cta, lean::kNT, fp.smem_bytes, s, a);
+        NGF_LAUNCH((lean::k_march_lean<8, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else
-        NGF_LAUNCH((lean::k_march_lean<8, 8>), fp.n_cta, lean::kNT, fp.smem_bytes, s, a);
+        NGF_LAUNCH((lean::k_march_lean<8, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+}
+
+// The per-level control block (kernel parameters) from the host plan.
+int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double hz, const std::vector<int>& bounds,
+                   const std::vector<int>& wzlo, double hx, double hy, lean::Ctl* c) {
+    using namespace lean;
+    if (nz > kMaxZ || (int)bounds.size() - 1 > kMaxChunks || ndz > 0xffff) return NGF_EARG;
+    std::memset(c, 0, sizeof(Ctl));
+    c->nchunk = (int)bounds.size() - 1;
+    for (size_t t = 0; t < bounds.size(); ++t) c->zb[t] = bounds[t];
+    for (int t = 0; t < c->nchunk; ++t) c->wzlo[t] = wzlo[t];
+    const float ihz = (float)(1.0 / hz);
+    c->hx2 = 0.5f * (float)(1.0 / hx);
+    c->hy2 = 0.5f * (float)(1.0 / hy);
+    c->hz2 = 0.5f * ihz;
+    const int faces[4] = {0, 1, nz - 2, nz - 1};
+    for (int f = 0; f < 4; ++f) {
+        fd_coef<float>(faces[f], nz, ihz, c->faceG[f][0], c->faceG[f][1], c->faceG[f][2]);
+        fdt_coef<float>(faces[f], nz, ihz, c->faceG[f][3], c->faceG[f][4], c->faceG[f][5]);
+    }
+    for (int z = 0; z < nz; ++z) {
+        unsigned w = (unsigned)i0z[z];
+        if (z + 1 < nz && i0z[z + 1] == i0z[z] + 1) w |= kAdv;
+        float cm, c0, cp, gm, g0, gp;
+        fd_coef<float>(z, nz, ihz, cm, c0, cp);
+        fdt_coef<float>(z, nz, ihz, gm, g0, gp);
+        const bool central = cm == -c->hz2 && c0 == 0.f && cp == c->hz2 && gm == c->hz2 && g0 == 0.f &&
+                             gp == -c->hz2;
+        if (!central) {
+            int slot = 0;
+            for (int f = 0; f < 4; ++f)
+                if (faces[f] == z) slot = f + 1;
+            if (!slot) return NGF_EARG;  // a non-central row away from the faces cannot happen
+            w |= (unsigned)slot << kFaceShift;
+        }
+        c->zw[z] = w;
+        c->w1[z] = w1z[z];
+    }
+    return 0;
 }
 
 }  // namespace ngf

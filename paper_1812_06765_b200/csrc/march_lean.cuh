@@ -1,6 +1,8 @@
 // Lean fused march (f32, sm_100a): declarations shared with the host planner (level.cu)
 // and the dispatcher (eval_fused.cu).  See march_lean.cu for the design.
 #pragma once
+#include <vector>
+
 #include "fused_impl.cuh"
 
 namespace ngf {
@@ -24,15 +26,27 @@ constexpr int kKMax = 8;          // max image columns (rows) feeding one window
 // by at most one node per image plane and never on two consecutive planes (every
 // deformation plane spans >= 2 image planes: the staggered flush), window and entry
 // counts within the compile-time bounds.
-struct Eligibility {
-    bool ok;
-    int kx, ky;  // entries per window output (4 or 8)
+constexpr int kMaxZ = 1024;      // image planes
+constexpr int kMaxChunks = 128;  // z chunks per level
+
+// Per-level control of the march, passed as a kernel parameter (constant bank) and indexed
+// by the CTA-uniform plane counter so that every branch of the march is uniform.
+struct Ctl {
+    int nchunk;
+    int zb[kMaxChunks + 1];   // chunk boundaries (image planes)
+    int wzlo[kMaxChunks];     // lowest deformation plane of each chunk's P^T window
+    unsigned zw[kMaxZ];       // per image plane: i0z (bits 0-15), advance flag, z-face slot
+    float w1[kMaxZ];          // f32(w1z)
+    float faceG[4][8];        // z = 0, 1, nz-2, nz-1: G (cm, c0, cp), G^T (gm, g0, gp)
+    float hx2, hy2, hz2;      // 1 / (2 h): central differences
 };
 
 }  // namespace lean
 
 int lean_prepare(size_t smem);
 size_t lean_smem(int kx, int ky);
-void lean_launch(const FusedArgs<float>& a, cudaStream_t s);
+void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s);
+int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double hz, const std::vector<int>& bounds,
+                   const std::vector<int>& wzlo, double hx, double hy, lean::Ctl* c);
 
 }  // namespace ngf

@@ -34,7 +34,8 @@ import numpy as np
 from . import _device as dev
 from ._lib import check, lib
 
-__all__ = ["slab_ranges", "slab_plane_layout", "SlabObjective", "DeviceSlab"]
+__all__ = ["slab_ranges", "slab_plane_layout", "combine_slab_partials", "SlabObjective", "LocalSlabGroup",
+           "DeviceSlab", "register_slab"]
 
 
 def slab_ranges(nz: int, nd_z: int, world: int):
@@ -80,14 +81,74 @@ def slab_plane_layout(image_grid, def_grid, slabs):
     return windows, owned
 
 
+def _overlap(windows, owned, q, r):
+    lo = max(windows[q][0], owned[r][0])
+    hi = min(windows[q][1] + 1, owned[r][1])
+    return (lo, hi) if lo < hi else None
+
+
+def combine_slab_partials(partials, windows, owned):
+    """grad D from the slab partials exactly as the distributed plane exchange forms it:
+    for every owner r (in rank order), its planes are the sum, in rank order q = 0, 1, ...,
+    of the contributions of the slabs whose windows overlap them (zeros where none does).
+    `partials` are torch tensors (3, ndz, rest), one per rank.  One-process reference of
+    SlabObjective's exchange (bit-identical for the same partials)."""
+    import torch
+
+    out = torch.zeros_like(partials[0])
+    for r in range(len(owned)):
+        olo, ohi = owned[r]
+        acc = torch.zeros_like(out[:, olo:ohi])
+        for q in range(len(partials)):
+            ov = _overlap(windows, owned, q, r)
+            if ov:
+                acc[:, ov[0] - olo:ov[1] - olo] += partials[q][:, ov[0]:ov[1]]
+        out[:, olo:ohi] = acc
+    return out
+
+
+def ordered_sum(values):
+    """Sum of per-rank scalars in rank order (the distributed D)."""
+    acc = 0.0
+    for v in values:
+        acc = acc + float(v)
+    return acc
+
+
 class DeviceSlab:
     """Slab partial of a device level (`DeviceLevel` restricted to [zlo, zhi))."""
 
-    def __init__(self, level, zlo: int, zhi: int):
-        check(lib().ngf_level_set_zrange(level.handle, int(zlo), int(zhi)), "ngf_level_set_zrange")
+    def __init__(self, level, zlo: int, zhi: int, restrict: bool = True):
+        if restrict:
+            check(lib().ngf_level_set_zrange(level.handle, int(zlo), int(zhi)), "ngf_level_set_zrange")
         self.level = level
         self.zlo, self.zhi = zlo, zhi
         self.image_grid, self.def_grid = level.image_grid, level.def_grid
+
+    @classmethod
+    def create(cls, image_grid, def_grid, T_dev, R_dev, params, alpha: float, zlo: int, zhi: int):
+        """A slab level whose reference terms are computed on planes [zlo, zhi) only
+        (ngf_level_create_zslab): the template and R are replicated, nothing else is."""
+        import ctypes
+
+        from ._lib import dtype_code, ngf_grid
+        from .objective import DeviceLevel
+
+        lvl = DeviceLevel.__new__(DeviceLevel)
+        lvl.image_grid, lvl.def_grid = image_grid, def_grid
+        lvl.dtype = T_dev.dtype
+        lvl.T, lvl._R = T_dev, R_dev
+        lvl.alpha = float(alpha)
+        h = ctypes.c_void_p()
+        ig, dg = ngf_grid(image_grid), ngf_grid(def_grid)
+        check(lib().ngf_level_create_zslab(ctypes.byref(ig), ctypes.byref(dg), dtype_code(T_dev.dtype),
+                                           dev.ptr(T_dev), dev.ptr(R_dev), float(params.tau), float(params.rho),
+                                           lvl.alpha, int(zlo), int(zhi), dev.stream(), ctypes.byref(h)),
+              "ngf_level_create_zslab")
+        lvl.handle = h
+        lvl.n = 3 * def_grid.num_points
+        lvl.scalars = dev.zeros((3,), "float64")
+        return cls(lvl, zlo, zhi, restrict=False)
 
     def partial(self, x, grad, scal):
         """grad <- grad D_slab, scal[1] <- D_slab (device, no sync)."""
@@ -139,9 +200,7 @@ class SlabObjective:
         g = grad.view(3, nd[2], nd[1] * nd[0])
 
         def overlap(q, r):
-            lo = max(windows[q][0], owned[r][0])
-            hi = min(windows[q][1] + 1, owned[r][1])
-            return (lo, hi) if lo < hi else None
+            return _overlap(windows, owned, q, r)
 
         # window planes owned by other ranks go to their owners
         ops, recv = [], {}
@@ -178,20 +237,85 @@ class SlabObjective:
             g[:, lo:hi] = blocks[q][:, :hi - lo]
 
     def eval_device(self, x, grad, scal):
+        import torch
         import torch.distributed as dist
 
         self.evals += 1
         self.local.partial(x, grad, scal)
-        if dist.is_initialized():
+        if dist.is_initialized() and dist.get_world_size(self.group) > 1:
             if self.exchange == "planes":
                 self._exchange_planes(grad)
             else:
                 dist.all_reduce(grad, op=dist.ReduceOp.SUM, group=self.group)
+            # D: the slab values gathered and summed in rank order (deterministic for a
+            # given world size, whatever order the backend's all-reduce would use)
             d = scal[1:2].clone()
-            dist.all_reduce(d, op=dist.ReduceOp.SUM, group=self.group)
-            scal[1:2].copy_(d)
+            ds = [torch.empty_like(d) for _ in range(dist.get_world_size(self.group))]
+            dist.all_gather(ds, d, group=self.group)
+            scal[1] = ordered_sum(v.item() for v in ds)
         self.local.finish(x, grad, scal)
         return scal
+
+    def __call__(self, x):
+        """The reference's objective contract, numpy in -> (J, numpy grad) out
+        (objective.py:54-60), identical on every rank."""
+        return _numpy_call(self, _is_device(self.local), x)
+
+
+class LocalSlabGroup:
+    """All slabs of a decomposition evaluated in ONE process and combined exactly like
+    SlabObjective over a process group (plane exchange in rank order, D summed in rank
+    order): the single-process reference a distributed run is compared against
+    bit-for-bit, and a way to run the config-5 decomposition on one device."""
+
+    def __init__(self, slabs):
+        self.slabs = list(slabs)
+        self.evals = 0
+        first = self.slabs[0]
+        self.image_grid, self.def_grid = first.image_grid, first.def_grid
+        self.layout = slab_plane_layout(first.image_grid, first.def_grid,
+                                        [(int(s.zlo), int(s.zhi)) for s in self.slabs])
+
+    def eval_device(self, x, grad, scal):
+        import torch
+
+        self.evals += 1
+        nd = self.def_grid.dims
+        parts, ds = [], []
+        for s in self.slabs:
+            g = torch.empty_like(grad)
+            sc = torch.zeros_like(scal)
+            s.partial(x, g, sc)
+            parts.append(g.view(3, nd[2], nd[1] * nd[0]))
+            ds.append(float(sc[1].item()))
+        windows, owned = self.layout
+        grad.view(3, nd[2], nd[1] * nd[0]).copy_(combine_slab_partials(parts, windows, owned))
+        scal[1] = ordered_sum(ds)
+        self.slabs[0].finish(x, grad, scal)
+        return scal
+
+    def __call__(self, x):
+        return _numpy_call(self, _is_device(self.slabs[0]), x)
+
+
+def _is_device(slab) -> bool:
+    return hasattr(getattr(slab, "level", None), "handle")
+
+
+def _numpy_call(obj, on_gpu: bool, x):
+    import torch
+
+    xa = np.asarray(x)
+    if not np.all(np.isfinite(xa)):
+        # overflowed line-search trial point; force a backtrack (objective.py:55-57)
+        return float("inf"), np.zeros_like(xa)
+    xt = torch.from_numpy(np.ascontiguousarray(xa).reshape(-1).copy())
+    if on_gpu:
+        xt = xt.cuda()
+    g = torch.empty_like(xt)
+    sc = torch.zeros(3, dtype=torch.float64, device=xt.device)
+    obj.eval_device(xt, g, sc)
+    return float(sc[0].item()), g.cpu().numpy().reshape(xa.shape)
 
 
 def weak_scaling_pairs(total_pairs: int, world: int, rank: int):
@@ -202,3 +326,75 @@ def weak_scaling_pairs(total_pairs: int, world: int, rank: int):
 
 def as_numpy(t):
     return t.detach().cpu().numpy() if dev.is_tensor(t) else np.asarray(t)
+
+
+def register_slab(R, T, cfg=None, group=None, emulate_world: int | None = None):
+    """Config 5: ONE registration (multilevel.py:179-247) with every level z-slab
+    decomposed over the ranks of `group`.
+
+    Each rank holds the template and R (replicated, read-only), builds both pyramids, and
+    per level creates a slab level whose reference terms cover its own planes only
+    (`DeviceSlab.create`); `SlabObjective` combines the slab partials (plane exchange +
+    D in rank order), and the L-BFGS state is replicated: every rank runs the same
+    `lbfgs_minimize` on identical (J, grad J), so the ranks stay in lock-step with no
+    further communication.  With `emulate_world=G` and no process group, the G slabs of
+    each level are evaluated in this process (`LocalSlabGroup`) -- the bit-for-bit
+    single-process reference of a G-rank run.  Returns (DeformationField, report)."""
+    import time
+
+    import torch.distributed as dist
+
+    from .geometry import DeformationField, identity_field_array, precision_dtype
+    from .lbfgs import lbfgs_minimize
+    from .multilevel import (LevelReport, MultilevelConfig, RegistrationReport, _coarser, _downsample_dev,
+                             _prolong_dev, deformation_grid_for, num_auto_levels)
+
+    cfg = cfg or MultilevelConfig()
+    if R.grid != T.grid:
+        from ._lib import GridError
+        raise GridError("reference and template must share one grid; resample the template first")
+    distributed = emulate_world is None and dist.is_initialized()
+    world = dist.get_world_size(group) if distributed else (emulate_world or 1)
+    rank = dist.get_rank(group) if distributed else 0
+    t_start = time.perf_counter()
+    dtype = precision_dtype(cfg.precision)
+    levels = cfg.num_levels or num_auto_levels(R.grid.dims, cfg.coarsest_min_dim)
+    np_out = not dev.is_tensor(R.values)
+    Rv = R.values.astype(dtype, copy=False) if np_out else R.values
+    Tv = T.values.astype(dtype, copy=False) if not dev.is_tensor(T.values) else T.values
+    pyr = [(dev.to_device(Rv, dtype), dev.to_device(Tv, dtype), R.grid)]
+    for _ in range(levels - 1):
+        r_, t_, g = pyr[-1]
+        ng = _coarser(g)
+        if ng.dims == g.dims:
+            raise ValueError(f"cannot build {levels} levels from dims {R.grid.dims}")
+        pyr.append((_downsample_dev(r_, g), _downsample_dev(t_, g), ng))
+    pyr.reverse()
+    report = RegistrationReport(seconds_pyramid=time.perf_counter() - t_start)
+    y = prev = None
+    for lvl, (R_l, T_l, gi) in enumerate(pyr):
+        t0 = time.perf_counter()
+        gd = deformation_grid_for(gi, cfg.grid_ratio)
+        slabs = slab_ranges(gi.dims[2], gd.dims[2], world)
+        if distributed:
+            zlo, zhi = slabs[rank]
+            obj = SlabObjective(DeviceSlab.create(gi, gd, T_l, R_l, cfg.ngf, cfg.alpha, zlo, zhi), group)
+        else:
+            obj = LocalSlabGroup([DeviceSlab.create(gi, gd, T_l, R_l, cfg.ngf, cfg.alpha, lo, hi)
+                                  for lo, hi in slabs])
+        y = dev.to_device(identity_field_array(gd, dtype)) if y is None else _prolong_dev(y, prev, gd)
+        setup_s = time.perf_counter() - t0
+        t0 = time.perf_counter()
+        x, trace = lbfgs_minimize(obj, y.reshape(-1), cfg.lbfgs, cfg.stopping)
+        y = x.reshape((3,) + gd.shape)
+        prev = gd
+        final_g = trace.records[-1].grad_inf if trace.records else 0.0
+        report.levels.append(LevelReport(
+            level_index=lvl, image_dims=gi.dims, def_dims=gd.dims, iterations=trace.iterations,
+            stop_reason=trace.stop_reason, line_search_failed=trace.line_search_failed,
+            records=trace.records, J_trace=list(trace.J_rows), final_grad_inf=final_g,
+            seconds_setup=setup_s, seconds_optimize=time.perf_counter() - t0,
+            evaluations=trace.evaluations))
+        report.final_grad_inf = final_g
+    report.seconds_total = time.perf_counter() - t_start
+    return DeformationField(prev, dev.to_host(y) if np_out else y), report
