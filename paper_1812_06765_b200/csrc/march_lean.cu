@@ -26,6 +26,7 @@
 //     per CTA.
 // Determinism: every sum has a fixed order; no atomics.
 
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -36,12 +37,17 @@ namespace ngf {
 namespace lean {
 
 constexpr int kPlane = kE1Y * kE1X;  // 544 positions, row stride 34 for every per-position plane
+constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4, aligned with the
+                                     // deformation cells at grid ratio 2 and 4 (steady blocks)
+
+// events of a steady-state step (compile-time schedule, see Lean::block)
+constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8;
 
 struct Smem {
-    float W[3][kPlane];                // W of planes p-2, p-1, p (ring by plane index mod 3)
-    float dT[3][3][kPlane];            // interpolant derivative (times h), same ring
-    float Qx[3][kPlane + 2];           // q_x at [P + 1]: the ring columns (q = 0) pad the rows
-    float Qy[3][kPlane + 2 * kE1X];    // q_y at [P + 34]: one zero row each side
+    float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
+    float dT[kRing][3][kPlane];           // interpolant derivative (times h), same ring
+    float Qx[kRing][kPlane + 2];          // q_x at [P + 1]: the ring columns (q = 0) pad the rows
+    float Qy[kRing][kPlane + 2 * kE1X];   // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
     float Xr[3][kE1Y][kWXM];           // x-reduced
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
@@ -63,8 +69,9 @@ __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int KX, int KY>
+template <int RATIO, int K>
 struct Lean {
+    static constexpr int KX = K, KY = K;
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
@@ -74,9 +81,9 @@ struct Lean {
     float m_in;    // 1 for interior positions, else 0 (distance accumulation)
     bool bwarp;    // the warp holds interior positions (runs (B))
     bool wface_b, wface_c;
-    int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo;
+    int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo, pstart, pend;
     float ylo[3], yhi[3];
-    float qz[3];
+    float qz[kRing];
     float A0[3], A1[3];
     float4 rt;
     float dacc;
@@ -168,19 +175,31 @@ struct Lean {
         return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
-    template <int R>
+    // One plane step: (A) on p, (B) on p-1, (C) on p-2.  R = ring slot of plane p.  GEN: the
+    // generic step (chunk edges, volume faces: every condition tested on the uniform plane
+    // counter); otherwise a steady-state step whose events EV are known at compile time.
+    template <int R, bool GEN, unsigned EV>
     __device__ __forceinline__ void step(int p) {
-        constexpr int RB = (R + 2) % 3;  // plane p-1
-        constexpr int RC = (R + 1) % 3;  // plane p-2
+        constexpr int RB = (R + 3) & 3;  // plane p-1
+        constexpr int RC = (R + 2) & 3;  // plane p-2
+        constexpr int RD = (R + 1) & 3;  // plane p-3
+        if (GEN && (p < pstart || p >= pend)) return;  // alignment padding of the loop
 
         // ------------------------------------------------------------- (A) plane p
         float W = 0.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
-        if (p >= pa0 && p <= pa1) {
-            const int zd = (int)(c.zw[p] & 0xffffu);
-            if (p == pa0) {
-                load_yplane(zd, ylo);
-                load_yplane(min(zd + 1, a.ndz - 1), yhi);
-            } else if (c.zw[p - 1] & kAdv) {
+        if (!GEN || (p >= pa0 && p <= pa1)) {
+            if (GEN) {
+                const int zd = (int)(c.zw[p] & 0xffffu);
+                if (p == pa0) {
+                    load_yplane(zd, ylo);
+                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
+                } else if (c.zw[p - 1] & kAdv) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
+                }
+            } else if (EV & kEvA) {
+                const int zd = (int)(c.zw[p] & 0xffffu);
 #pragma unroll
                 for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
                 load_yplane(min(zd + 1, a.ndz - 1), yhi);
@@ -223,7 +242,7 @@ struct Lean {
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
-        if (k >= z0 && k < z1) {
+        if (!GEN || (k >= z0 && k < z1)) {
             if (bwarp) {
                 const float* Wk = &sm.W[RB][P];
                 const float wl = Wk[-1], wr = Wk[1], wu = Wk[-kE1X], wd = Wk[kE1X];
@@ -242,13 +261,13 @@ struct Lean {
                         gy = fmaf(rg[0], wu, fmaf(rg[1], w0, rg[2] * wd));
                     }
                 }
-                const unsigned fz = c.zw[k] >> kFaceShift;
-                float gz;
-                if (fz) {  // z face plane: the exact one-sided rows
-                    const float* zc = c.faceG[fz - 1];
-                    gz = fmaf(zc[0], wzm, fmaf(zc[1], Wk[0], zc[2] * wzp));
-                } else {
-                    gz = (wzp - wzm) * c.hz2;
+                float gz = (wzp - wzm) * c.hz2;
+                if (GEN) {
+                    const unsigned fz = c.zw[k] >> kFaceShift;
+                    if (fz) {  // z face plane: the exact one-sided rows
+                        const float* zc = c.faceG[fz - 1];
+                        gz = fmaf(zc[0], wzm, fmaf(zc[1], Wk[0], zc[2] * wzp));
+                    }
                 }
                 // NGF ratio, distance term, q = dD/d grad W (ngf.py:70-112); positions outside
                 // the interior carry rt = 0, hence q = 0, and m_in = 0
@@ -263,20 +282,20 @@ struct Lean {
                 sm.Qx[RB][P + 1] = cf * fmaf(-t1, gx, rt.x);
                 sm.Qy[RB][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
                 // reference terms of plane p for the next step's (B)
-                if (p < z1 && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
+                if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
-        } else if (bwarp) {  // no q on this plane (chunk edges)
+        } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
             sm.Qx[RB][P + 1] = 0.f;
             sm.Qy[RB][P + kE1X] = 0.f;
         }
         // staggered P^T passes of the deformation planes completed two and one steps ago
-        if (flushes(p - 4)) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
-        if (flushes(p - 3)) xpass();
+        if (GEN ? flushes(p - 4) : (EV & kEvY) != 0) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
+        if (GEN ? flushes(p - 3) : (EV & kEvX) != 0) xpass();
 
         // ------------------------------------------------------------- (C) j = p-2
         const int j = p - 2;
-        if (j < jfirst || j > jlast) return;
+        if (GEN && (j < jfirst || j > jlast)) return;
         const float* qxj = &sm.Qx[RC][P + 1];
         const float* qyj = &sm.Qy[RC][P + kE1X];
         const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
@@ -293,13 +312,13 @@ struct Lean {
                 sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
             }
         }
-        const unsigned fz = c.zw[j] >> kFaceShift;
-        float sz;
-        if (fz) {
-            const float* zc = c.faceG[fz - 1];
-            sz = fmaf(zc[3], qz[R], fmaf(zc[4], qz[RC], zc[5] * qz[RB]));
-        } else {
-            sz = (qz[R] - qz[RB]) * c.hz2;
+        float sz = (qz[RD] - qz[RB]) * c.hz2;
+        if (GEN) {
+            const unsigned fz = c.zw[j] >> kFaceShift;
+            if (fz) {
+                const float* zc = c.faceG[fz - 1];
+                sz = fmaf(zc[3], qz[RD], fmaf(zc[4], qz[RC], zc[5] * qz[RB]));
+            }
         }
         const float sv = sx + sy + sz;
         const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
@@ -309,7 +328,7 @@ struct Lean {
             A0[q] = fmaf(w0, g, A0[q]);
             A1[q] = fmaf(w1, g, A1[q]);
         }
-        if (flushes(j)) {
+        if (GEN ? flushes(j) : (EV & kEvF) != 0) {
             put_flush(A0);
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
@@ -318,14 +337,43 @@ struct Lean {
             }
         }
     }
+
+    // four steps from plane p (p = phase mod 4)
+    __device__ __forceinline__ void generic4(int p) {
+        step<0, true, 0>(p);
+        step<1, true, 0>(p + 1);
+        step<2, true, 0>(p + 2);
+        step<3, true, 0>(p + 3);
+    }
+
+    // four steady-state steps from a plane p that starts a deformation cell, away from the
+    // chunk edges and the volume faces: the events follow the grid ratio (a new cell at
+    // every RATIO-th plane, its predecessor flushed one step later, x and y passes one and
+    // two steps after that)
+    __device__ __forceinline__ void block(int p) {
+        if constexpr (RATIO == 4) {
+            step<0, false, kEvA>(p);
+            step<1, false, kEvF>(p + 1);
+            step<2, false, kEvX>(p + 2);
+            step<3, false, kEvY>(p + 3);
+        } else if constexpr (RATIO == 2) {
+            step<0, false, kEvA | kEvX>(p);
+            step<1, false, kEvF | kEvY>(p + 1);
+            step<2, false, kEvA | kEvX>(p + 2);
+            step<3, false, kEvF | kEvY>(p + 3);
+        } else {
+            generic4(p);
+        }
+    }
 };
 
-template <int KX, int KY>
+template <int RATIO, int K>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<KX, KY> m(a, c, sm);
+    Lean<RATIO, K> m(a, c, sm);
+    constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
@@ -395,8 +443,8 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : 0.f;
     }
-    for (int t = tid; t < 3 * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
-    for (int t = tid; t < 3 * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
+    for (int t = tid; t < kRing * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
+    for (int t = tid; t < kRing * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
     {
         const int2* gx = reinterpret_cast<const int2*>(fp.lx) + (size_t)tx * fp.wx * KX;
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
@@ -418,23 +466,29 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // ---- march state
     m.dacc = 0.f;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) m.qz[r] = m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
+    for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
+#pragma unroll
+    for (int r = 0; r < kRing; ++r) m.qz[r] = 0.f;
     m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
     if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
 
-    // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2
-    const int pstart = m.z0 - 1;
-    const int nsteps = (m.z1 + 2) - pstart + 1;
-    for (int b = 0; b < nsteps; b += 3) {
-        m.template step<0>(pstart + b);
-        if (b + 1 < nsteps) m.template step<1>(pstart + b + 1);
-        if (b + 2 < nsteps) m.template step<2>(pstart + b + 2);
+    // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
+    // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
+    // steady range [s0, s1) run the compile-time event schedule
+    m.pstart = m.z0 - 1;
+    m.pend = m.z1 + 3;
+    const int s0 = c.s0[tzc], s1 = c.s1[tzc];
+    for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
+        if (p >= s0 && p + 4 <= s1)
+            m.block(p);
+        else
+            m.generic4(p);
     }
 
     // ---- drain the staggered passes (planes completed in the last two steps), then the
     // chunk's last deformation plane(s)
-    const int pend = pstart + nsteps;  // the first step not taken
+    const int pend = m.pend;  // the first step not taken
     __syncthreads();
     if (m.flushes(pend - 4)) m.ypass((int)(c.zw[pend - 4] & 0xffffu) - m.wzlo);
     if (m.flushes(pend - 3)) {
@@ -472,9 +526,9 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 }
 
-template <int KX, int KY>
+template <int RATIO, int K>
 static cudaError_t set_smem(size_t smem) {
-    return cudaFuncSetAttribute(k_march_lean<KX, KY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_march_lean<RATIO, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace lean
@@ -486,10 +540,10 @@ int lean_prepare(size_t smem) {
     static size_t granted = 0;
     std::lock_guard<std::mutex> lk(mu);
     if (smem <= granted) return 0;
-    cudaError_t e = lean::set_smem<8, 8>(smem);
-    if (e == cudaSuccess) e = lean::set_smem<4, 4>(smem);
-    if (e == cudaSuccess) e = lean::set_smem<8, 4>(smem);
-    if (e == cudaSuccess) e = lean::set_smem<4, 8>(smem);
+    cudaError_t e = lean::set_smem<4, 8>(smem);
+    if (e == cudaSuccess) e = lean::set_smem<2, 4>(smem);
+    if (e == cudaSuccess) e = lean::set_smem<2, 8>(smem);
+    if (e == cudaSuccess) e = lean::set_smem<0, 8>(smem);
     if (e == cudaSuccess) granted = smem;
     return (int)e;
 }
@@ -497,14 +551,15 @@ int lean_prepare(size_t smem) {
 void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) {
     const FusedPlan& fp = a.fp;
     const dim3 grid(fp.ntx, fp.nty, fp.ntz);
-    if (fp.kx <= 4 && fp.ky <= 4)
-        NGF_LAUNCH((lean::k_march_lean<4, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
-    else if (fp.kx <= 4)
+    const int k = (fp.kx <= 4 && fp.ky <= 4) ? 4 : 8;
+    if (c.ratio == 4 && k == 8)
         NGF_LAUNCH((lean::k_march_lean<4, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
-    else if (fp.ky <= 4)
-        NGF_LAUNCH((lean::k_march_lean<8, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+    else if (c.ratio == 2 && k == 4)
+        NGF_LAUNCH((lean::k_march_lean<2, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+    else if (c.ratio == 2)
+        NGF_LAUNCH((lean::k_march_lean<2, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else
-        NGF_LAUNCH((lean::k_march_lean<8, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LAUNCH((lean::k_march_lean<0, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
 }
 
 // The per-level control block (kernel parameters) from the host plan.
@@ -542,6 +597,56 @@ int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double
         }
         c->zw[z] = w;
         c->w1[z] = w1z[z];
+    }
+    // the steady-state schedule: find the cell period r in {4, 2} and the phase, then per
+    // chunk the planes [s0, s1) whose four-step groups may run it; every plane there is
+    // checked against the z map (a new cell exactly at p = phase mod r, no face rows)
+    auto adv = [&](int z) { return z >= 0 && z + 1 < nz && i0z[z + 1] == i0z[z] + 1; };
+    c->ratio = 0;
+    c->phase = 0;
+    for (int r : {4, 2}) {
+        int first = -1;
+        for (int z = 3; z + 1 < nz && first < 0; ++z)
+            if (adv(z - 1)) first = z;  // a plane starting a cell, away from the low face
+        if (first < 0) continue;
+        int run = 0;  // planes after `first` that follow the period-r pattern
+        for (int z = first; z < nz - 2; ++z) {
+            if (adv(z - 1) != ((z - first) % r == 0)) break;
+            ++run;
+        }
+        if (run >= 8) {
+            c->ratio = r;
+            c->phase = first & 3;
+            break;
+        }
+    }
+    for (int t = 0; t < c->nchunk; ++t) {
+        c->s0[t] = c->s1[t] = 0;
+        if (!c->ratio) continue;
+        const int z0 = bounds[t], z1 = bounds[t + 1];
+        int lo = std::max(z0 + 2, 4);
+        lo += ((c->phase - lo) % 4 + 4) % 4;  // first group start = phase (mod 4)
+        const int hi = std::min(z1 - 1, nz - 2);  // last plane a steady step may be on
+        // a group at s is valid when the z map follows the period on planes s-4 .. s+3 (the
+        // passes of steps s .. s+3 refer back to flushes after planes s-4 .. s-1) and its (B)
+        // / (C) planes use central z rows; the steady range is the first run of valid groups
+        auto valid = [&](int s) {
+            for (int p = s - 4; p < s + 4; ++p) {
+                const bool want = ((p - c->phase) % c->ratio + c->ratio) % c->ratio == 0;
+                if (adv(p - 1) != want) return false;
+            }
+            for (int p = s; p < s + 4; ++p)
+                if (c->zw[p - 1] >> kFaceShift || c->zw[p - 2] >> kFaceShift) return false;
+            return true;
+        };
+        int s = lo;
+        while (s + 3 <= hi && !valid(s)) s += 4;
+        int e = s;
+        while (e + 3 <= hi && valid(e)) e += 4;
+        if (e > s) {
+            c->s0[t] = s;
+            c->s1[t] = e;
+        }
     }
     return 0;
 }

@@ -33,6 +33,10 @@ constexpr int kMaxChunks = 128;  // z chunks per level
 // by the CTA-uniform plane counter so that every branch of the march is uniform.
 struct Ctl {
     int nchunk;
+    int ratio;                // 2 or 4: deformation cells of `ratio` planes in the steady range; 0: none
+    int phase;                // a deformation cell starts at every plane = phase (mod 4) in the steady range
+    int s0[kMaxChunks];       // per chunk: steady four-step groups cover planes [s0, s1)
+    int s1[kMaxChunks];
     int zb[kMaxChunks + 1];   // chunk boundaries (image planes)
     int wzlo[kMaxChunks];     // lowest deformation plane of each chunk's P^T window
     unsigned zw[kMaxZ];       // per image plane: i0z (bits 0-15), advance flag, z-face slot
