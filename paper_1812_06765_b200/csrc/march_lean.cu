@@ -49,6 +49,9 @@ struct Smem {
     float Qx[kRing][kPlane + 2];          // q_x at [P + 1]: the ring columns (q = 0) pad the rows
     float Qy[kRing][kPlane + 2 * kE1X];   // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
+    float4 Y[2][kPlane];               // P_xy y of this position on deformation planes zd, zd + 1
+    float4 RTs[2][kPlane];             // reference terms of two interior planes (TMA bulk copies)
+    uint64_t mbar[2];                  // completion of the RTs slots
     float Xr[3][kE1Y][kWXM];           // x-reduced
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
@@ -62,6 +65,29 @@ struct Smem {
 __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
     // a0 * (1 - w) + a1 * w, each op correctly rounded (transfer.py:126)
     return __fadd_rn(__fmul_rn(a0, w0), __fmul_rn(a1, w));
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done)
+        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
+                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on the mbarrier (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
 }
 
 // Per-level control in the kernel's parameter space (constant bank): indexed by the
@@ -82,10 +108,10 @@ struct Lean {
     bool bwarp;    // the warp holds interior positions (runs (B))
     bool wface_b, wface_c;
     int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo, pstart, pend;
-    float ylo[3], yhi[3];
+    int x0, y0;
+    float g[8], gfx, gfy, gfz;  // template corners and cell fractions of the next plane (in flight)
     float qz[kRing];
     float A0[3], A1[3];
-    float4 rt;
     float dacc;
 
     __device__ __forceinline__ Lean(const FusedArgs<float>& a_, const Ctl& c_, Smem& sm_) : a(a_), c(c_), sm(sm_) {}
@@ -175,9 +201,83 @@ struct Lean {
         return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
-    // One plane step: (A) on p, (B) on p-1, (C) on p-2.  R = ring slot of plane p.  GEN: the
-    // generic step (chunk edges, volume faces: every condition tested on the uniform plane
-    // counter); otherwise a steady-state step whose events EV are known at compile time.
+    // (A1) for plane q: yhat = P y (the P_xy pair of this position in shared memory, a new
+    // pair when q starts a deformation cell), the cell lookup and the 8 template gathers,
+    // left in flight in g[] until (A2) of the next step.  q outside the chunk's A range:
+    // zeros (W = 0 and derivative 0).
+    template <bool GEN, bool NEWCELL>
+    __device__ __forceinline__ void a1(int q) {
+        if (GEN && (q < pa0 || q > pa1)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) g[k] = 0.f;
+            gfx = gfy = gfz = 0.f;
+            return;
+        }
+        float4 lo, hi;
+        const bool reload = GEN && q == pa0;
+        const bool shift = GEN ? (!reload && (c.zw[q - 1] & kAdv)) : NEWCELL;
+        if (reload || shift) {
+            const int zd = (int)(c.zw[q] & 0xffffu);
+            float v[3];
+            if (reload) {
+                load_yplane(zd, v);
+                lo = make_float4(v[0], v[1], v[2], 0.f);
+                sm.Y[0][P] = lo;
+            } else {
+                lo = sm.Y[1][P];
+                sm.Y[0][P] = lo;
+            }
+            load_yplane(min(zd + 1, a.ndz - 1), v);
+            hi = make_float4(v[0], v[1], v[2], 0.f);
+            sm.Y[1][P] = hi;
+        } else {
+            lo = sm.Y[0][P];
+            hi = sm.Y[1][P];
+        }
+        const float wz = c.w1[q], wz0 = __fsub_rn(1.0f, wz);
+        const float yh0 = __fadd_rn(__fmul_rn(lo.x, wz0), __fmul_rn(hi.x, wz));
+        const float yh1 = __fadd_rn(__fmul_rn(lo.y, wz0), __fmul_rn(hi.y, wz));
+        const float yh2 = __fadd_rn(__fmul_rn(lo.z, wz0), __fmul_rn(hi.z, wz));
+        bool in = fl & 8u;  // position inside the volume (x / y)
+        const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, gfx);
+        const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, gfy);
+        const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, gfz);
+        const unsigned nx = (unsigned)a.nx, nxy = nx * (unsigned)a.ny;
+        const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
+        const float* b = a.Tv + off;
+        const float* by = b + nx;
+        const float* bz = b + nxy;
+        const float* byz = bz + nx;
+        g[0] = __ldg(b);
+        g[1] = __ldg(b + 1);
+        g[2] = __ldg(by);
+        g[3] = __ldg(by + 1);
+        g[4] = __ldg(bz);
+        g[5] = __ldg(bz + 1);
+        g[6] = __ldg(byz);
+        g[7] = __ldg(byz + 1);
+    }
+
+    // reference terms of interior plane q into RTs[(q - z0) & 1]: TMA bulk copies of the
+    // tile's interior rows (32 x 16 B each, fewer at the x end), issued by one thread
+    __device__ __forceinline__ void rt_issue(int q) {
+        const int slot = (q - z0) & 1;
+        const int cols = min(32, a.nx - x0);
+        const int rows = min(kTYI, a.ny - y0);
+        const uint32_t rb = (uint32_t)cols * 16u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
+        mbar_expect_tx(&sm.mbar[slot], rb * (uint32_t)rows);
+        const float4* src = reinterpret_cast<const float4*>(a.RT) + ((size_t)q * a.ny + y0) * a.nx + x0;
+        for (int r = 0; r < rows; ++r) bulk_g2s(&sm.RTs[slot][(r + 1) * kE1X + 1], src + (size_t)r * a.nx, rb, &sm.mbar[slot]);
+    }
+    __device__ __forceinline__ void rt_wait(int q) {
+        mbar_wait(&sm.mbar[(q - z0) & 1], (uint32_t)((q - z0) >> 1) & 1u);
+    }
+
+    // One plane step: (A2) on p, (A1) on p+1, (B) on p-1, (C) on p-2.  R = ring slot of plane
+    // p.  GEN: the generic step (chunk edges, volume faces: every condition tested on the
+    // uniform plane counter); otherwise a steady-state step whose events EV are known at
+    // compile time.
     template <int R, bool GEN, unsigned EV>
     __device__ __forceinline__ void step(int p) {
         constexpr int RB = (R + 3) & 3;  // plane p-1
@@ -185,60 +285,28 @@ struct Lean {
         constexpr int RD = (R + 1) & 3;  // plane p-3
         if (GEN && (p < pstart || p >= pend)) return;  // alignment padding of the loop
 
-        // ------------------------------------------------------------- (A) plane p
-        float W = 0.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
-        if (!GEN || (p >= pa0 && p <= pa1)) {
-            if (GEN) {
-                const int zd = (int)(c.zw[p] & 0xffffu);
-                if (p == pa0) {
-                    load_yplane(zd, ylo);
-                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
-                } else if (c.zw[p - 1] & kAdv) {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
-                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
-                }
-            } else if (EV & kEvA) {
-                const int zd = (int)(c.zw[p] & 0xffffu);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
-                load_yplane(min(zd + 1, a.ndz - 1), yhi);
-            }
-            const float wz = c.w1[p], wz0 = __fsub_rn(1.0f, wz);
-            const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
-            const float yh1 = __fadd_rn(__fmul_rn(ylo[1], wz0), __fmul_rn(yhi[1], wz));
-            const float yh2 = __fadd_rn(__fmul_rn(ylo[2], wz0), __fmul_rn(yhi[2], wz));
-            bool in = fl & 8u;  // position inside the volume (x / y)
-            float fx_, fy_, fz_;
-            const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, fx_);
-            const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, fy_);
-            const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, fz_);
-            const unsigned nx = (unsigned)a.nx, nxy = nx * (unsigned)a.ny;
-            const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
-            const float* b = a.Tv + off;
-            const float* by = b + nx;
-            const float* bz = b + nxy;
-            const float* byz = bz + nx;
-            const float c0 = __ldg(b), c1 = __ldg(b + 1), c2 = __ldg(by), c3 = __ldg(by + 1);
-            const float c4 = __ldg(bz), c5 = __ldg(bz + 1), c6 = __ldg(byz), c7 = __ldg(byz + 1);
+        // ------------------------------------------------------------- (A2) plane p
+        {
             // trilinear value and derivative (times h) in lerp form (warp.py:79-85, :111-120)
-            const float e00 = c1 - c0, e10 = c3 - c2, e01 = c5 - c4, e11 = c7 - c6;
-            const float a00 = fmaf(fx_, e00, c0), a10 = fmaf(fx_, e10, c2);
-            const float a01 = fmaf(fx_, e01, c4), a11 = fmaf(fx_, e11, c6);
+            const float e00 = g[1] - g[0], e10 = g[3] - g[2], e01 = g[5] - g[4], e11 = g[7] - g[6];
+            const float a00 = fmaf(gfx, e00, g[0]), a10 = fmaf(gfx, e10, g[2]);
+            const float a01 = fmaf(gfx, e01, g[4]), a11 = fmaf(gfx, e11, g[6]);
             const float dy0 = a10 - a00, dy1 = a11 - a01;
-            const float b0 = fmaf(fy_, dy0, a00), b1 = fmaf(fy_, dy1, a01);
+            const float b0 = fmaf(gfy, dy0, a00), b1 = fmaf(gfy, dy1, a01);
             const float dz = b1 - b0;
-            W = fmaf(fz_, dz, b0);
-            const float ex0 = fmaf(fy_, e10 - e00, e00), ex1 = fmaf(fy_, e11 - e01, e01);
-            d0 = fmaf(fz_, ex1 - ex0, ex0);
-            d1 = fmaf(fz_, dy1 - dy0, dy0);
-            d2 = dz;
+            const float ex0 = fmaf(gfy, e10 - e00, e00), ex1 = fmaf(gfy, e11 - e01, e01);
+            sm.W[R][P] = fmaf(gfz, dz, b0);
+            sm.dT[R][0][P] = fmaf(gfz, ex1 - ex0, ex0);
+            sm.dT[R][1][P] = fmaf(gfz, dy1 - dy0, dy0);
+            sm.dT[R][2][P] = dz;
         }
-        sm.W[R][P] = W;
-        sm.dT[R][0][P] = d0;
-        sm.dT[R][1][P] = d1;
-        sm.dT[R][2][P] = d2;
+        // the reference terms (B) uses after this barrier have landed
+        if (threadIdx.x == 0 && (!GEN || (p - 1 >= z0 && p - 1 < z1))) rt_wait(p - 1);
         __syncthreads();
+        if (threadIdx.x == 0 && (!GEN || (p >= z0 && p < z1))) rt_issue(p);
+
+        // ------------------------------------------------------------- (A1) plane p+1
+        a1<GEN, (EV & kEvA) != 0>(p + 1);
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
@@ -270,7 +338,8 @@ struct Lean {
                     }
                 }
                 // NGF ratio, distance term, q = dD/d grad W (ngf.py:70-112); positions outside
-                // the interior carry rt = 0, hence q = 0, and m_in = 0
+                // the interior read rt = 0 (never copied), hence q = 0, and m_in = 0
+                const float4 rt = sm.RTs[(k - z0) & 1][P];
                 const float dot = fmaf(gx, rt.x, fmaf(gy, rt.y, gz * rt.z));
                 const float sq = fmaf(gx, gx, fmaf(gy, gy, fmaf(gz, gz, a.tau2)));
                 const float inv_nt = rsqrtf(sq);
@@ -281,8 +350,6 @@ struct Lean {
                 qz[RB] = cf * fmaf(-t1, gz, rt.z);
                 sm.Qx[RB][P + 1] = cf * fmaf(-t1, gx, rt.x);
                 sm.Qy[RB][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
-                // reference terms of plane p for the next step's (B)
-                if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
@@ -324,9 +391,9 @@ struct Lean {
         const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
-            const float g = sv * sm.dT[RC][q][P];
-            A0[q] = fmaf(w0, g, A0[q]);
-            A1[q] = fmaf(w1, g, A1[q]);
+            const float gg = sv * sm.dT[RC][q][P];
+            A0[q] = fmaf(w0, gg, A0[q]);
+            A1[q] = fmaf(w1, gg, A1[q]);
         }
         if (GEN ? flushes(j) : (EV & kEvF) != 0) {
             put_flush(A0);
@@ -351,16 +418,17 @@ struct Lean {
     // every RATIO-th plane, its predecessor flushed one step later, x and y passes one and
     // two steps after that)
     __device__ __forceinline__ void block(int p) {
+        // (kEvA: the (A1) plane p+1 of the step starts a cell)
         if constexpr (RATIO == 4) {
-            step<0, false, kEvA>(p);
+            step<0, false, 0>(p);
             step<1, false, kEvF>(p + 1);
             step<2, false, kEvX>(p + 2);
-            step<3, false, kEvY>(p + 3);
+            step<3, false, kEvY | kEvA>(p + 3);
         } else if constexpr (RATIO == 2) {
-            step<0, false, kEvA | kEvX>(p);
-            step<1, false, kEvF | kEvY>(p + 1);
-            step<2, false, kEvA | kEvX>(p + 2);
-            step<3, false, kEvF | kEvY>(p + 3);
+            step<0, false, kEvX>(p);
+            step<1, false, kEvF | kEvY | kEvA>(p + 1);
+            step<2, false, kEvX>(p + 2);
+            step<3, false, kEvF | kEvY | kEvA>(p + 3);
         } else {
             generic4(p);
         }
@@ -466,12 +534,19 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // ---- march state
     m.dacc = 0.f;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
+    for (int r = 0; r < 3; ++r) m.A0[r] = m.A1[r] = 0.f;
 #pragma unroll
     for (int r = 0; r < kRing; ++r) m.qz[r] = 0.f;
-    m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
+    m.x0 = x0;
+    m.y0 = y0;
+    // positions the reference-term copies never write (ring, outside the volume) read zeros
+    for (int t = tid; t < 2 * kPlane; t += kNT) (&sm.RTs[0][0])[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (tid == 0) {
+        mbar_init(&sm.mbar[0], 1);
+        mbar_init(&sm.mbar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
     __syncthreads();
-    if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
     // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
@@ -479,6 +554,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     m.pstart = m.z0 - 1;
     m.pend = m.z1 + 3;
     const int s0 = c.s0[tzc], s1 = c.s1[tzc];
+    m.template a1<true, false>(m.pstart);  // the first plane's gathers
     for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
         if (p >= s0 && p + 4 <= s1)
             m.block(p);
@@ -627,11 +703,12 @@ int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double
         int lo = std::max(z0 + 2, 4);
         lo += ((c->phase - lo) % 4 + 4) % 4;  // first group start = phase (mod 4)
         const int hi = std::min(z1 - 1, nz - 2);  // last plane a steady step may be on
-        // a group at s is valid when the z map follows the period on planes s-4 .. s+3 (the
-        // passes of steps s .. s+3 refer back to flushes after planes s-4 .. s-1) and its (B)
-        // / (C) planes use central z rows; the steady range is the first run of valid groups
+        // a group at s is valid when the z map follows the period on planes s-4 .. s+4 (the
+        // passes of steps s .. s+3 refer back to flushes after planes s-4 .. s-1, and (A1) of
+        // step s+3 works on plane s+4) and its (B) / (C) planes use central z rows; the
+        // steady range is the first run of valid groups
         auto valid = [&](int s) {
-            for (int p = s - 4; p < s + 4; ++p) {
+            for (int p = s - 4; p <= s + 4; ++p) {
                 const bool want = ((p - c->phase) % c->ratio + c->ratio) % c->ratio == 0;
                 if (adv(p - 1) != want) return false;
             }

@@ -1,0 +1,74 @@
+"""Config 5 as a registration on the device: `register_slab` runs the
+reference's multilevel driver (multilevel.py:179-247) with every level z-slab decomposed;
+per level each slab's reference terms are computed on its own planes only
+(ngf_level_create_zslab) and the L-BFGS state (lbfgs.py:94-181) is replicated.  On one
+GPU the G slabs of a level are evaluated in-process (`LocalSlabGroup`, the bit-for-bit
+single-process reference of a G-rank NCCL run; the gloo version of that identity is in
+tests/test_distributed_cpu.py)."""
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1812_06765_b200 as ngf  # noqa: E402
+from paper_1812_06765_b200.distributed import (DeviceSlab, LocalSlabGroup, register_slab,  # noqa: E402
+                                               slab_ranges)
+
+BAR_VOXEL = 0.05
+
+
+def _pair(n=64):
+    R, T, _ = ngf.ct_pair(n, seed=3, max_disp_vox=3.0)
+    return R, T
+
+
+def test_slab_register_world1_is_register():
+    R, T = _pair()
+    cfg = ngf.MultilevelConfig(num_levels=2, grid_ratio=4, precision="f32")
+    y_ref, rep_ref = ngf.register(R, T, cfg)
+    y, rep = register_slab(R, T, cfg, emulate_world=1)
+    assert [lv.iterations for lv in rep.levels] == [lv.iterations for lv in rep_ref.levels]
+    for a, b in zip(rep.levels, rep_ref.levels):
+        assert [r.J for r in a.records] == [r.J for r in b.records]
+    assert np.array_equal(y.field, y_ref.field)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_slab_register_matches_undivided(world):
+    R, T = _pair()
+    cfg = ngf.MultilevelConfig(num_levels=2, grid_ratio=4, precision="f32",
+                               lbfgs=ngf.LbfgsConfig(max_iterations=25))
+    y_ref, rep_ref = ngf.register(R, T, cfg)
+    y, rep = register_slab(R, T, cfg, emulate_world=world)
+    # the first accepted iterates agree to rounding (the slab sums reorder the P^T additions)
+    J0 = [r.J for r in rep.levels[0].records][:5]
+    J0r = [r.J for r in rep_ref.levels[0].records][:5]
+    assert np.allclose(J0, J0r, rtol=1e-5)
+    d = np.sqrt(np.sum((y.field.astype(np.float64) - y_ref.field) ** 2, axis=0))
+    print(f"world {world}: iterations {[lv.iterations for lv in rep.levels]} vs "
+          f"{[lv.iterations for lv in rep_ref.levels]}; field max {d.max():.4f} interior "
+          f"{d[2:-2, 2:-2, 2:-2].max():.4f} voxel")
+    assert d[2:-2, 2:-2, 2:-2].max() <= BAR_VOXEL
+
+
+def test_slab_level_terms_and_modes():
+    """A slab level evaluates only its slab partial; the sum of the slab partials of a
+    decomposition equals the undivided evaluation (gradient to rounding)."""
+    R, T = _pair()
+    gi = R.grid
+    gd = ngf.deformation_grid_for(gi, 4)
+    y = ngf.smooth_random_field(gd, seed=2, amplitude_mm=2.0).field.astype(np.float32)
+    T_dev, R_dev = torch.from_numpy(T.values).cuda(), torch.from_numpy(R.values).cuda()
+    full = ngf.LevelObjective.from_device(T_dev, R_dev, ngf.build_gather_plan(gd, gi), ngf.NgfParams(), 1.0)
+    J_ref, g_ref = full(y.ravel())
+    slabs = [DeviceSlab.create(gi, gd, T_dev, R_dev, ngf.NgfParams(), 1.0, lo, hi)
+             for lo, hi in slab_ranges(gi.dims[2], gd.dims[2], 3)]
+    J, g = LocalSlabGroup(slabs)(y.ravel())
+    assert abs(J - J_ref) <= 1e-5 * abs(J_ref)
+    assert np.linalg.norm(g - g_ref) <= 1e-5 * np.linalg.norm(g_ref)
+    # the full evaluation is not available on a slab level (only its partial is)
+    x = torch.from_numpy(y.ravel().copy()).cuda()
+    with pytest.raises(RuntimeError):
+        slabs[1].level.eval(x, torch.empty_like(x))
