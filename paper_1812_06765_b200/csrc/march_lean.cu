@@ -27,6 +27,8 @@
 // Determinism: every sum has a fixed order; no atomics.
 
 #include <algorithm>
+#include <cstddef>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -40,8 +42,12 @@ constexpr int kPlane = kE1Y * kE1X;  // 544 positions, row stride 34 for every p
 constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4, aligned with the
                                      // deformation cells at grid ratio 2 and 4 (steady blocks)
 
+// compile-time features of a march instance (NGF_LEAN_F selects one at run time; A/B)
+constexpr int kFTma = 1;   // reference terms by TMA bulk copies into shared memory (mbarrier)
+constexpr int kFPipe = 2;  // template gathers issued one step ahead (A1 after the barrier, A2 before)
+
 // events of a steady-state step (compile-time schedule, see Lean::block)
-constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8;
+constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16;
 
 struct Smem {
     float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
@@ -49,9 +55,6 @@ struct Smem {
     float Qx[kRing][kPlane + 2];          // q_x at [P + 1]: the ring columns (q = 0) pad the rows
     float Qy[kRing][kPlane + 2 * kE1X];   // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
-    float4 Y[2][kPlane];               // P_xy y of this position on deformation planes zd, zd + 1
-    float4 RTs[2][kPlane];             // reference terms of two interior planes (TMA bulk copies)
-    uint64_t mbar[2];                  // completion of the RTs slots
     float Xr[3][kE1Y][kWXM];           // x-reduced
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
@@ -60,7 +63,15 @@ struct Smem {
     float colPw[kE1X], rowPw[kE1Y];
     unsigned fa[kNT];                  // flush pass assignment per thread
     double red[kWarps];
+    // feature-dependent tail (the launch requests only what the instance uses)
+    uint64_t mbar[2];                  // TMA: completion of the RTs slots
+    float4 RTs[2][kPlane];             // TMA: reference terms of two interior planes
+    float4 Y[2][kPlane];               // PIPE: P_xy y of this position on deformation planes zd, zd + 1
 };
+
+__host__ __device__ constexpr size_t smem_for(int f) {
+    return (f & kFPipe) ? sizeof(Smem) : (f & kFTma) ? offsetof(Smem, Y) : offsetof(Smem, mbar);
+}
 
 __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
     // a0 * (1 - w) + a1 * w, each op correctly rounded (transfer.py:126)
@@ -95,9 +106,10 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int RATIO, int K>
+template <int RATIO, int K, int F>
 struct Lean {
     static constexpr int KX = K, KY = K;
+    static constexpr bool TMA = (F & kFTma) != 0, PIPE = (F & kFPipe) != 0;
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
@@ -109,7 +121,9 @@ struct Lean {
     bool wface_b, wface_c;
     int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo, pstart, pend;
     int x0, y0;
-    float g[8], gfx, gfy, gfz;  // template corners and cell fractions of the next plane (in flight)
+    float g[8], gfx, gfy, gfz;  // PIPE: template corners and cell fractions of the next plane (in flight)
+    float ylo[3], yhi[3];       // !PIPE: P_xy y of this position on deformation planes zd, zd + 1
+    float4 rt;                  // !TMA: reference terms of the next (B) plane (prefetched)
     float qz[kRing];
     float A0[3], A1[3];
     float dacc;
@@ -216,23 +230,37 @@ struct Lean {
         float4 lo, hi;
         const bool reload = GEN && q == pa0;
         const bool shift = GEN ? (!reload && (c.zw[q - 1] & kAdv)) : NEWCELL;
-        if (reload || shift) {
-            const int zd = (int)(c.zw[q] & 0xffffu);
-            float v[3];
-            if (reload) {
-                load_yplane(zd, v);
-                lo = make_float4(v[0], v[1], v[2], 0.f);
+        if constexpr (PIPE) {
+            if (reload || shift) {
+                const int zd = (int)(c.zw[q] & 0xffffu);
+                float v[3];
+                if (reload) {
+                    load_yplane(zd, v);
+                    lo = make_float4(v[0], v[1], v[2], 0.f);
+                } else {
+                    lo = sm.Y[1][P];
+                }
                 sm.Y[0][P] = lo;
+                load_yplane(min(zd + 1, a.ndz - 1), v);
+                hi = make_float4(v[0], v[1], v[2], 0.f);
+                sm.Y[1][P] = hi;
             } else {
-                lo = sm.Y[1][P];
-                sm.Y[0][P] = lo;
+                lo = sm.Y[0][P];
+                hi = sm.Y[1][P];
             }
-            load_yplane(min(zd + 1, a.ndz - 1), v);
-            hi = make_float4(v[0], v[1], v[2], 0.f);
-            sm.Y[1][P] = hi;
         } else {
-            lo = sm.Y[0][P];
-            hi = sm.Y[1][P];
+            if (reload || shift) {
+                const int zd = (int)(c.zw[q] & 0xffffu);
+                if (reload) {
+                    load_yplane(zd, ylo);
+                } else {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+                }
+                load_yplane(min(zd + 1, a.ndz - 1), yhi);
+            }
+            lo = make_float4(ylo[0], ylo[1], ylo[2], 0.f);
+            hi = make_float4(yhi[0], yhi[1], yhi[2], 0.f);
         }
         const float wz = c.w1[q], wz0 = __fsub_rn(1.0f, wz);
         const float yh0 = __fadd_rn(__fmul_rn(lo.x, wz0), __fmul_rn(hi.x, wz));
@@ -274,7 +302,7 @@ struct Lean {
         mbar_wait(&sm.mbar[(q - z0) & 1], (uint32_t)((q - z0) >> 1) & 1u);
     }
 
-    // One plane step: (A2) on p, (A1) on p+1, (B) on p-1, (C) on p-2.  R = ring slot of plane
+    // One plane step: (A) on p [PIPE: (A2) on p, (A1) on p+1], (B) on p-1, (C) on p-2.  R = ring slot of plane
     // p.  GEN: the generic step (chunk edges, volume faces: every condition tested on the
     // uniform plane counter); otherwise a steady-state step whose events EV are known at
     // compile time.
@@ -285,7 +313,9 @@ struct Lean {
         constexpr int RD = (R + 1) & 3;  // plane p-3
         if (GEN && (p < pstart || p >= pend)) return;  // alignment padding of the loop
 
-        // ------------------------------------------------------------- (A2) plane p
+        // ------------------------------------------------------------- (A) plane p
+        // PIPE: the gathers were issued by the previous step's (A1); else issue them now
+        if constexpr (!PIPE) a1<GEN, (EV & kEvA0) != 0>(p);
         {
             // trilinear value and derivative (times h) in lerp form (warp.py:79-85, :111-120)
             const float e00 = g[1] - g[0], e10 = g[3] - g[2], e01 = g[5] - g[4], e11 = g[7] - g[6];
@@ -300,13 +330,15 @@ struct Lean {
             sm.dT[R][1][P] = fmaf(gfz, dy1 - dy0, dy0);
             sm.dT[R][2][P] = dz;
         }
-        // the reference terms (B) uses after this barrier have landed
-        if (threadIdx.x == 0 && (!GEN || (p - 1 >= z0 && p - 1 < z1))) rt_wait(p - 1);
+        if constexpr (TMA) {
+            // the reference terms (B) uses after this barrier have landed
+            if (threadIdx.x == 0 && (!GEN || (p - 1 >= z0 && p - 1 < z1))) rt_wait(p - 1);
+        }
         __syncthreads();
-        if (threadIdx.x == 0 && (!GEN || (p >= z0 && p < z1))) rt_issue(p);
-
-        // ------------------------------------------------------------- (A1) plane p+1
-        a1<GEN, (EV & kEvA) != 0>(p + 1);
+        if constexpr (TMA) {
+            if (threadIdx.x == 0 && (!GEN || (p >= z0 && p < z1))) rt_issue(p);
+        }
+        if constexpr (PIPE) a1<GEN, (EV & kEvA) != 0>(p + 1);  // (A1) of plane p+1
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
@@ -338,8 +370,8 @@ struct Lean {
                     }
                 }
                 // NGF ratio, distance term, q = dD/d grad W (ngf.py:70-112); positions outside
-                // the interior read rt = 0 (never copied), hence q = 0, and m_in = 0
-                const float4 rt = sm.RTs[(k - z0) & 1][P];
+                // the interior carry rt = 0 (never loaded / copied), hence q = 0, and m_in = 0
+                const float4 rt = TMA ? sm.RTs[(k - z0) & 1][P] : this->rt;
                 const float dot = fmaf(gx, rt.x, fmaf(gy, rt.y, gz * rt.z));
                 const float sq = fmaf(gx, gx, fmaf(gy, gy, fmaf(gz, gz, a.tau2)));
                 const float inv_nt = rsqrtf(sq);
@@ -350,6 +382,9 @@ struct Lean {
                 qz[RB] = cf * fmaf(-t1, gz, rt.z);
                 sm.Qx[RB][P + 1] = cf * fmaf(-t1, gx, rt.x);
                 sm.Qy[RB][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
+                // !TMA: reference terms of plane p for the next step's (B)
+                if (!TMA && (!GEN || p < z1) && (fl & 4u))
+                    this->rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
@@ -419,15 +454,16 @@ struct Lean {
     // two steps after that)
     __device__ __forceinline__ void block(int p) {
         // (kEvA: the (A1) plane p+1 of the step starts a cell)
+        // (kEvA0: plane p of the step starts a cell; kEvA: plane p+1 does)
         if constexpr (RATIO == 4) {
-            step<0, false, 0>(p);
+            step<0, false, kEvA0>(p);
             step<1, false, kEvF>(p + 1);
             step<2, false, kEvX>(p + 2);
             step<3, false, kEvY | kEvA>(p + 3);
         } else if constexpr (RATIO == 2) {
-            step<0, false, kEvX>(p);
+            step<0, false, kEvA0 | kEvX>(p);
             step<1, false, kEvF | kEvY | kEvA>(p + 1);
-            step<2, false, kEvX>(p + 2);
+            step<2, false, kEvA0 | kEvX>(p + 2);
             step<3, false, kEvF | kEvY | kEvA>(p + 3);
         } else {
             generic4(p);
@@ -435,12 +471,12 @@ struct Lean {
     }
 };
 
-template <int RATIO, int K>
+template <int RATIO, int K, int F>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<RATIO, K> m(a, c, sm);
+    Lean<RATIO, K, F> m(a, c, sm);
     constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -539,14 +575,22 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     for (int r = 0; r < kRing; ++r) m.qz[r] = 0.f;
     m.x0 = x0;
     m.y0 = y0;
-    // positions the reference-term copies never write (ring, outside the volume) read zeros
-    for (int t = tid; t < 2 * kPlane; t += kNT) (&sm.RTs[0][0])[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (tid == 0) {
-        mbar_init(&sm.mbar[0], 1);
-        mbar_init(&sm.mbar[1], 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+#pragma unroll
+    for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = 0.f;
+    m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr ((F & kFTma) != 0) {
+        // positions the reference-term copies never write (ring, outside the volume) read zeros
+        for (int t = tid; t < 2 * kPlane; t += kNT) (&sm.RTs[0][0])[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (tid == 0) {
+            mbar_init(&sm.mbar[0], 1);
+            mbar_init(&sm.mbar[1], 1);
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        }
     }
     __syncthreads();
+    if constexpr ((F & kFTma) == 0) {
+        if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
+    }
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
     // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
@@ -554,7 +598,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     m.pstart = m.z0 - 1;
     m.pend = m.z1 + 3;
     const int s0 = c.s0[tzc], s1 = c.s1[tzc];
-    m.template a1<true, false>(m.pstart);  // the first plane's gathers
+    if constexpr ((F & kFPipe) != 0) m.template a1<true, false>(m.pstart);  // the first plane's gathers
     for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
         if (p >= s0 && p + 4 <= s1)
             m.block(p);
@@ -602,14 +646,27 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 }
 
+template <int RATIO, int K, int F>
+static cudaError_t set_smem1(size_t smem) {
+    return cudaFuncSetAttribute(k_march_lean<RATIO, K, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
 template <int RATIO, int K>
 static cudaError_t set_smem(size_t smem) {
-    return cudaFuncSetAttribute(k_march_lean<RATIO, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = set_smem1<RATIO, K, 0>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFTma>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFTma | kFPipe>(smem);
+    return e;
+}
+
+// instance feature set: NGF_LEAN_F (0, 1 = TMA, 3 = TMA + pipelined gathers), default 0
+int feature() {
+    static const int f = std::getenv("NGF_LEAN_F") ? std::atoi(std::getenv("NGF_LEAN_F")) : 0;
+    return (f == 1 || f == 3) ? f : 0;
 }
 
 }  // namespace lean
 
-size_t lean_smem(int, int) { return sizeof(lean::Smem); }
+size_t lean_smem(int, int) { return lean::smem_for(lean::feature()); }
 
 int lean_prepare(size_t smem) {
     static std::mutex mu;
@@ -628,14 +685,26 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
     const FusedPlan& fp = a.fp;
     const dim3 grid(fp.ntx, fp.nty, fp.ntz);
     const int k = (fp.kx <= 4 && fp.ky <= 4) ? 4 : 8;
+    const int f = lean::feature();
+    const size_t sb = fp.smem_bytes;
+#define NGF_LEAN_GO(R, K)                                                                        \
+    do {                                                                                         \
+        if (f == 3)                                                                              \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma | lean::kFPipe>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 1)                                                                         \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma>), grid, lean::kNT, sb, s, a, c);   \
+        else                                                                                     \
+            NGF_LAUNCH((lean::k_march_lean<R, K, 0>), grid, lean::kNT, sb, s, a, c);             \
+    } while (0)
     if (c.ratio == 4 && k == 8)
-        NGF_LAUNCH((lean::k_march_lean<4, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LEAN_GO(4, 8);
     else if (c.ratio == 2 && k == 4)
-        NGF_LAUNCH((lean::k_march_lean<2, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LEAN_GO(2, 4);
     else if (c.ratio == 2)
-        NGF_LAUNCH((lean::k_march_lean<2, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LEAN_GO(2, 8);
     else
-        NGF_LAUNCH((lean::k_march_lean<0, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LEAN_GO(0, 8);
+#undef NGF_LEAN_GO
 }
 
 // The per-level control block (kernel parameters) from the host plan.
