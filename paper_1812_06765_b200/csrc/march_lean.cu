@@ -45,6 +45,7 @@ constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4
 // compile-time features of a march instance (NGF_LEAN_F selects one at run time; A/B)
 constexpr int kFTma = 1;   // reference terms by TMA bulk copies into shared memory (mbarrier)
 constexpr int kFPipe = 2;  // template gathers issued one step ahead (A1 after the barrier, A2 before)
+constexpr int kFRing = 4;  // the P^T x / y passes run on the three warps without (B) work
 
 // events of a steady-state step (compile-time schedule, see Lean::block)
 constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16;
@@ -61,7 +62,8 @@ struct Smem {
     float colG[kE1X][3], colGt[kE1X][3], rowG[kE1Y][3], rowGt[kE1Y][3];
     int colP0[kE1X], colP1[kE1X], rowP0[kE1Y], rowP1[kE1Y];
     float colPw[kE1X], rowPw[kE1Y];
-    unsigned fa[kNT];                  // flush pass assignment per thread
+    unsigned short xo[kE1Y * kWXM];    // x pass outputs: row | window column << 8
+    unsigned short yo[kWYM * kWXM];    // y pass outputs: window row | window column << 8
     double red[kWarps];
     // feature-dependent tail (the launch requests only what the instance uses)
     uint64_t mbar[2];                  // TMA: completion of the RTs slots
@@ -159,47 +161,72 @@ struct Lean {
         return (int)fl;
     }
 
+    // this thread's first P^T pass output (then every kPassStride-th): all threads, or
+    // (kFRing) the 96 threads of warps 0 and kE1Y - 1 (ring rows) and kE1Y (ring columns)
+    static constexpr int kPassStride = (F & kFRing) ? 96 : kNT;
+    __device__ __forceinline__ int pass_first() const {
+        if constexpr ((F & kFRing) != 0) {
+            const int w = threadIdx.x >> 5;
+            const int rw = w == 0 ? 0 : w == kE1Y - 1 ? 1 : w == kE1Y ? 2 : -1;
+            return rw < 0 ? (1 << 30) : rw * 32 + (threadIdx.x & 31);
+        } else {
+            return threadIdx.x;
+        }
+    }
+
     // x pass of a completed deformation plane: Fb -> Xr (fixed entry order per output)
-    __device__ __forceinline__ void xpass() const {
-        const unsigned f = sm.fa[threadIdx.x];
-        const int xr_r = f & 0xff, xr_d = (f >> 8) & 0xff;
-        if (xr_r != 0xff) {
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-            const float* fb = &sm.Fb[0][0] + xr_r * kE1X;
+    __device__ __forceinline__ void xpass_one(int o) const {
+        const unsigned rd = sm.xo[o];
+        const int xr_r = rd & 0xff, xr_d = rd >> 8;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+        const float* fb = &sm.Fb[0][0] + xr_r * kE1X;
 #pragma unroll
-            for (int k = 0; k < KX; ++k) {
-                const int2 e = sm.xl[xr_d][k];
-                const float w = __int_as_float(e.y);
-                s0 = fmaf(w, fb[e.x], s0);
-                s1 = fmaf(w, fb[kPlane + e.x], s1);
-                s2 = fmaf(w, fb[2 * kPlane + e.x], s2);
-            }
-            sm.Xr[0][xr_r][xr_d] = s0;
-            sm.Xr[1][xr_r][xr_d] = s1;
-            sm.Xr[2][xr_r][xr_d] = s2;
+        for (int k = 0; k < KX; ++k) {
+            const int2 e = sm.xl[xr_d][k];
+            const float w = __int_as_float(e.y);
+            s0 = fmaf(w, fb[e.x], s0);
+            s1 = fmaf(w, fb[kPlane + e.x], s1);
+            s2 = fmaf(w, fb[2 * kPlane + e.x], s2);
+        }
+        sm.Xr[0][xr_r][xr_d] = s0;
+        sm.Xr[1][xr_r][xr_d] = s1;
+        sm.Xr[2][xr_r][xr_d] = s2;
+    }
+    __device__ __forceinline__ void xpass() const {
+        const int n = kE1Y * a.fp.wx;  // <= kNT
+        if constexpr ((F & kFRing) != 0) {
+            for (int o = pass_first(); o < n; o += kPassStride) xpass_one(o);
+        } else {
+            if ((int)threadIdx.x < n) xpass_one(threadIdx.x);
         }
     }
 
     // y pass: Xr -> the CTA's window partial of deformation plane slot zs (1/h applied)
-    __device__ __forceinline__ void ypass(int zs) const {
-        const unsigned f = sm.fa[threadIdx.x];
-        const int yp_dy = (f >> 16) & 0xff, yp_d = f >> 24;
-        if (yp_dy != 0xff) {
-            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    __device__ __forceinline__ void ypass_one(int o, int zs) const {
+        const int wx = a.fp.wx, wy = a.fp.wy;
+        const size_t win = (size_t)a.fp.wz * wy * wx;
+        const unsigned rd = sm.yo[o];
+        const int yp_dy = rd & 0xff, yp_d = rd >> 8;
+        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll
-            for (int k = 0; k < KY; ++k) {
-                const int2 e = sm.yl[yp_dy][k];
-                const float w = __int_as_float(e.y);
-                s0 = fmaf(w, sm.Xr[0][e.x][yp_d], s0);
-                s1 = fmaf(w, sm.Xr[1][e.x][yp_d], s1);
-                s2 = fmaf(w, sm.Xr[2][e.x][yp_d], s2);
-            }
-            const int wx = a.fp.wx, wy = a.fp.wy;
-            const size_t win = (size_t)a.fp.wz * wy * wx;
-            float* out = a.partial + (size_t)cta * 3 * win + (size_t)zs * wy * wx + yp_dy * wx + yp_d;
-            out[0] = s0 * a.ihx;
-            out[win] = s1 * a.ihy;
-            out[2 * win] = s2 * a.ihz;
+        for (int k = 0; k < KY; ++k) {
+            const int2 e = sm.yl[yp_dy][k];
+            const float w = __int_as_float(e.y);
+            s0 = fmaf(w, sm.Xr[0][e.x][yp_d], s0);
+            s1 = fmaf(w, sm.Xr[1][e.x][yp_d], s1);
+            s2 = fmaf(w, sm.Xr[2][e.x][yp_d], s2);
+        }
+        float* out = a.partial + (size_t)cta * 3 * win + (size_t)zs * wy * wx + yp_dy * wx + yp_d;
+        out[0] = s0 * a.ihx;
+        out[win] = s1 * a.ihy;
+        out[2 * win] = s2 * a.ihz;
+    }
+    __device__ __forceinline__ void ypass(int zs) const {
+        const int n = a.fp.wy * a.fp.wx;  // <= kNT
+        if constexpr ((F & kFRing) != 0) {
+            for (int o = pass_first(); o < n; o += kPassStride) ypass_one(o, zs);
+        } else {
+            if ((int)threadIdx.x < n) ypass_one(threadIdx.x, zs);
         }
     }
 
@@ -554,18 +581,17 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
         for (int t = tid; t < fp.wx * KX; t += kNT) sm.xl[t / KX][t % KX] = gx[t];
         for (int t = tid; t < fp.wy * KY; t += kNT) sm.yl[t / KY][t % KY] = gy[t];
-        // flush pass assignment: x pass (row, window column), y pass (window row, column)
-        unsigned xa = 0xffffu, ya = 0xffffu;
-        if (tid < kE1Y * fp.wx) {
-            const int r = tid / fp.wx;
-            xa = (unsigned)r | (unsigned)(tid - r * fp.wx) << 8;
+        // P^T pass output tables: x pass (row, window column), y pass (window row, column)
+        for (int t = tid; t < kE1Y * fp.wx; t += kNT) {
+            const int r = t / fp.wx;
+            sm.xo[t] = (unsigned short)(r | (t - r * fp.wx) << 8);
         }
-        if (tid < fp.wy * fp.wx) {
-            const int r = tid / fp.wx;
-            ya = (unsigned)r | (unsigned)(tid - r * fp.wx) << 8;
+        for (int t = tid; t < fp.wy * fp.wx; t += kNT) {
+            const int r = t / fp.wx;
+            sm.yo[t] = (unsigned short)(r | (t - r * fp.wx) << 8);
         }
-        sm.fa[tid] = xa | ya << 16;
     }
+
 
     // ---- march state
     m.dacc = 0.f;
@@ -655,13 +681,17 @@ static cudaError_t set_smem(size_t smem) {
     cudaError_t e = set_smem1<RATIO, K, 0>(smem);
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFTma>(smem);
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFTma | kFPipe>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFRing>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFRing | kFTma>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe | kFRing>(smem);
     return e;
 }
 
-// instance feature set: NGF_LEAN_F (0, 1 = TMA, 3 = TMA + pipelined gathers), default 0
+// instance feature set: NGF_LEAN_F = OR of kFTma (1), kFPipe (2), kFRing (4); default 0
 int feature() {
     static const int f = std::getenv("NGF_LEAN_F") ? std::atoi(std::getenv("NGF_LEAN_F")) : 0;
-    return (f == 1 || f == 3) ? f : 0;
+    return (f >= 1 && f <= 6) ? f : 0;
 }
 
 }  // namespace lean
@@ -691,6 +721,14 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
     do {                                                                                         \
         if (f == 3)                                                                              \
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma | lean::kFPipe>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 4)                                                                         \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFRing>), grid, lean::kNT, sb, s, a, c);  \
+        else if (f == 5)                                                                         \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFRing | lean::kFTma>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 2)                                                                         \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPipe>), grid, lean::kNT, sb, s, a, c);  \
+        else if (f == 6)                                                                         \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPipe | lean::kFRing>), grid, lean::kNT, sb, s, a, c); \
         else if (f == 1)                                                                         \
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma>), grid, lean::kNT, sb, s, a, c);   \
         else                                                                                     \
