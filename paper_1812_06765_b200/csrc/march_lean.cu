@@ -53,8 +53,8 @@ constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16;
 struct Smem {
     float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
     float dT[kRing][3][kPlane];           // interpolant derivative (times h), same ring
-    float Qx[kRing][kPlane + 2];          // q_x at [P + 1]: the ring columns (q = 0) pad the rows
-    float Qy[kRing][kPlane + 2 * kE1X];   // q_y at [P + 34]: one zero row each side
+    float Qx[2][kPlane + 2];              // q_x at [P + 1] (ring columns, q = 0, pad the rows), by plane parity
+    float Qy[2][kPlane + 2 * kE1X];       // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
     float Xr[3][kE1Y][kWXM];           // x-reduced
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
@@ -407,16 +407,16 @@ struct Lean {
                 const float t1 = r * inv_nt;
                 const float cf = a.neg_hbar * t1;
                 qz[RB] = cf * fmaf(-t1, gz, rt.z);
-                sm.Qx[RB][P + 1] = cf * fmaf(-t1, gx, rt.x);
-                sm.Qy[RB][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
+                sm.Qx[RB & 1][P + 1] = cf * fmaf(-t1, gx, rt.x);
+                sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
                 // !TMA: reference terms of plane p for the next step's (B)
                 if (!TMA && (!GEN || p < z1) && (fl & 4u))
                     this->rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
-            sm.Qx[RB][P + 1] = 0.f;
-            sm.Qy[RB][P + kE1X] = 0.f;
+            sm.Qx[RB & 1][P + 1] = 0.f;
+            sm.Qy[RB & 1][P + kE1X] = 0.f;
         }
         // staggered P^T passes of the deformation planes completed two and one steps ago
         if (GEN ? flushes(p - 4) : (EV & kEvY) != 0) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
@@ -425,8 +425,8 @@ struct Lean {
         // ------------------------------------------------------------- (C) j = p-2
         const int j = p - 2;
         if (GEN && (j < jfirst || j > jlast)) return;
-        const float* qxj = &sm.Qx[RC][P + 1];
-        const float* qyj = &sm.Qy[RC][P + kE1X];
+        const float* qxj = &sm.Qx[RC & 1][P + 1];
+        const float* qyj = &sm.Qy[RC & 1][P + kE1X];
         const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
         float sx = (ql - qr) * c.hx2;
         float sy = (qu - qd) * c.hy2;
@@ -574,8 +574,8 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : 0.f;
     }
-    for (int t = tid; t < kRing * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
-    for (int t = tid; t < kRing * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
+    for (int t = tid; t < 2 * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
+    for (int t = tid; t < 2 * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
     {
         const int2* gx = reinterpret_cast<const int2*>(fp.lx) + (size_t)tx * fp.wx * KX;
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
