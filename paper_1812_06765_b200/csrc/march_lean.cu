@@ -46,6 +46,8 @@ constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4
 constexpr int kFTma = 1;   // reference terms by TMA bulk copies into shared memory (mbarrier)
 constexpr int kFPipe = 2;  // template gathers issued one step ahead (A1 after the barrier, A2 before)
 constexpr int kFRing = 4;  // the P^T x / y passes run on the three warps without (B) work
+constexpr int kFLag = 8;   // (C) on plane p-3 BEFORE the plane barrier, between issuing the
+                           // template gathers of plane p and using them (covers their latency)
 
 // events of a steady-state step (compile-time schedule, see Lean::block)
 constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16;
@@ -111,7 +113,8 @@ constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: centra
 template <int RATIO, int K, int F>
 struct Lean {
     static constexpr int KX = K, KY = K;
-    static constexpr bool TMA = (F & kFTma) != 0, PIPE = (F & kFPipe) != 0;
+    static constexpr bool TMA = (F & kFTma) != 0, PIPE = (F & kFPipe) != 0, LAG = (F & kFLag) != 0;
+    static_assert(!(PIPE && LAG), "the lagged (C) and the pipelined gathers are alternatives");
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
@@ -329,6 +332,54 @@ struct Lean {
         mbar_wait(&sm.mbar[(q - z0) & 1], (uint32_t)((q - z0) >> 1) & 1u);
     }
 
+    // (C) on plane j, ring slot SJ: s = G^T q (warp.py:159-184), ghat = s * derivative, and its
+    // z interpolation onto the two deformation planes of j (transfer.py:151-192, z first)
+    template <int SJ, bool GEN, bool FLUSH>
+    __device__ __forceinline__ void phaseC(int j) {
+        constexpr int SM1 = (SJ + 3) & 3, SP1 = (SJ + 1) & 3;  // planes j-1, j+1
+        if (GEN && (j < jfirst || j > jlast)) return;
+        const float* qxj = &sm.Qx[SJ & 1][P + 1];
+        const float* qyj = &sm.Qy[SJ & 1][P + kE1X];
+        const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
+        float sx = (ql - qr) * c.hx2;
+        float sy = (qu - qd) * c.hy2;
+        if (wface_c) {
+            const int ey = P / kE1X, ex = P - ey * kE1X;
+            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
+                const float* ct = sm.colGt[ex];
+                sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
+            }
+            if (fl & 2u) {
+                const float* rg = sm.rowGt[ey];
+                sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
+            }
+        }
+        float sz = (qz[SM1] - qz[SP1]) * c.hz2;
+        if (GEN) {
+            const unsigned fz = c.zw[j] >> kFaceShift;
+            if (fz) {
+                const float* zc = c.faceG[fz - 1];
+                sz = fmaf(zc[3], qz[SM1], fmaf(zc[4], qz[SJ], zc[5] * qz[SP1]));
+            }
+        }
+        const float sv = sx + sy + sz;
+        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float gg = sv * sm.dT[SJ][q][P];
+            A0[q] = fmaf(w0, gg, A0[q]);
+            A1[q] = fmaf(w1, gg, A1[q]);
+        }
+        if (GEN ? flushes(j) : FLUSH) {
+            put_flush(A0);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                A0[q] = A1[q];
+                A1[q] = 0.f;
+            }
+        }
+    }
+
     // One plane step: (A) on p [PIPE: (A2) on p, (A1) on p+1], (B) on p-1, (C) on p-2.  R = ring slot of plane
     // p.  GEN: the generic step (chunk edges, volume faces: every condition tested on the
     // uniform plane counter); otherwise a steady-state step whose events EV are known at
@@ -343,6 +394,8 @@ struct Lean {
         // ------------------------------------------------------------- (A) plane p
         // PIPE: the gathers were issued by the previous step's (A1); else issue them now
         if constexpr (!PIPE) a1<GEN, (EV & kEvA0) != 0>(p);
+        // LAG: (C) on p-3 while the gathers are in flight
+        if constexpr (LAG) phaseC<RD, GEN, (EV & kEvF) != 0>(p - 3);
         {
             // trilinear value and derivative (times h) in lerp form (warp.py:79-85, :111-120)
             const float e00 = g[1] - g[0], e10 = g[3] - g[2], e01 = g[5] - g[4], e11 = g[7] - g[6];
@@ -418,53 +471,13 @@ struct Lean {
             sm.Qx[RB & 1][P + 1] = 0.f;
             sm.Qy[RB & 1][P + kE1X] = 0.f;
         }
-        // staggered P^T passes of the deformation planes completed two and one steps ago
+        // staggered P^T passes of the deformation planes completed after (C) on planes p-4 and
+        // p-3 (the previous / this step's barrier made them visible)
         if (GEN ? flushes(p - 4) : (EV & kEvY) != 0) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
         if (GEN ? flushes(p - 3) : (EV & kEvX) != 0) xpass();
 
         // ------------------------------------------------------------- (C) j = p-2
-        const int j = p - 2;
-        if (GEN && (j < jfirst || j > jlast)) return;
-        const float* qxj = &sm.Qx[RC & 1][P + 1];
-        const float* qyj = &sm.Qy[RC & 1][P + kE1X];
-        const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
-        float sx = (ql - qr) * c.hx2;
-        float sy = (qu - qd) * c.hy2;
-        if (wface_c) {
-            const int ey = P / kE1X, ex = P - ey * kE1X;
-            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
-                const float* ct = sm.colGt[ex];
-                sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
-            }
-            if (fl & 2u) {
-                const float* rg = sm.rowGt[ey];
-                sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
-            }
-        }
-        float sz = (qz[RD] - qz[RB]) * c.hz2;
-        if (GEN) {
-            const unsigned fz = c.zw[j] >> kFaceShift;
-            if (fz) {
-                const float* zc = c.faceG[fz - 1];
-                sz = fmaf(zc[3], qz[RD], fmaf(zc[4], qz[RC], zc[5] * qz[RB]));
-            }
-        }
-        const float sv = sx + sy + sz;
-        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const float gg = sv * sm.dT[RC][q][P];
-            A0[q] = fmaf(w0, gg, A0[q]);
-            A1[q] = fmaf(w1, gg, A1[q]);
-        }
-        if (GEN ? flushes(j) : (EV & kEvF) != 0) {
-            put_flush(A0);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                A0[q] = A1[q];
-                A1[q] = 0.f;
-            }
-        }
+        if constexpr (!LAG) phaseC<RC, GEN, (EV & kEvF) != 0>(p - 2);
     }
 
     // four steps from plane p (p = phase mod 4)
@@ -481,8 +494,19 @@ struct Lean {
     // two steps after that)
     __device__ __forceinline__ void block(int p) {
         // (kEvA: the (A1) plane p+1 of the step starts a cell)
-        // (kEvA0: plane p of the step starts a cell; kEvA: plane p+1 does)
-        if constexpr (RATIO == 4) {
+        // (kEvA0: plane p of the step starts a cell; kEvA: plane p+1 does; LAG: (C) runs on
+        // p-3, so its flushes come one step later)
+        if constexpr (RATIO == 4 && LAG) {
+            step<0, false, kEvA0>(p);
+            step<1, false, 0>(p + 1);
+            step<2, false, kEvF | kEvX>(p + 2);
+            step<3, false, kEvY>(p + 3);
+        } else if constexpr (RATIO == 2 && LAG) {
+            step<0, false, kEvA0 | kEvF | kEvX>(p);
+            step<1, false, kEvY>(p + 1);
+            step<2, false, kEvA0 | kEvF | kEvX>(p + 2);
+            step<3, false, kEvY>(p + 3);
+        } else if constexpr (RATIO == 4) {
             step<0, false, kEvA0>(p);
             step<1, false, kEvF>(p + 1);
             step<2, false, kEvX>(p + 2);
@@ -622,7 +646,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
     // steady range [s0, s1) run the compile-time event schedule
     m.pstart = m.z0 - 1;
-    m.pend = m.z1 + 3;
+    m.pend = m.z1 + ((F & kFLag) ? 4 : 3);  // (C) reaches plane z1
     const int s0 = c.s0[tzc], s1 = c.s1[tzc];
     if constexpr ((F & kFPipe) != 0) m.template a1<true, false>(m.pstart);  // the first plane's gathers
     for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
@@ -685,13 +709,15 @@ static cudaError_t set_smem(size_t smem) {
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFRing | kFTma>(smem);
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe>(smem);
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe | kFRing>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFLag>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFLag | kFRing>(smem);
     return e;
 }
 
-// instance feature set: NGF_LEAN_F = OR of kFTma (1), kFPipe (2), kFRing (4); default 0
+// instance feature set: NGF_LEAN_F = OR of kFTma (1), kFPipe (2), kFRing (4), kFLag (8); default 0
 int feature() {
     static const int f = std::getenv("NGF_LEAN_F") ? std::atoi(std::getenv("NGF_LEAN_F")) : 0;
-    return (f >= 1 && f <= 6) ? f : 0;
+    return ((f >= 1 && f <= 6) || f == 8 || f == 12) ? f : 0;
 }
 
 }  // namespace lean
@@ -729,6 +755,10 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPipe>), grid, lean::kNT, sb, s, a, c);  \
         else if (f == 6)                                                                         \
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPipe | lean::kFRing>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 8)                                                                         \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFLag>), grid, lean::kNT, sb, s, a, c);   \
+        else if (f == 12)                                                                        \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFLag | lean::kFRing>), grid, lean::kNT, sb, s, a, c); \
         else if (f == 1)                                                                         \
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma>), grid, lean::kNT, sb, s, a, c);   \
         else                                                                                     \
