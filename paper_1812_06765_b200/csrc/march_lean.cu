@@ -48,9 +48,14 @@ constexpr int kFPipe = 2;  // template gathers issued one step ahead (A1 after t
 constexpr int kFRing = 4;  // the P^T x / y passes run on the three warps without (B) work
 constexpr int kFLag = 8;   // (C) on plane p-3 BEFORE the plane barrier, between issuing the
                            // template gathers of plane p and using them (covers their latency)
+constexpr int kFStage = 16;  // P_xy of a new deformation plane from x-interpolated rows staged
+                             // cooperatively in shared memory one step ahead
+constexpr int kXsRows = 12;  // staged deformation rows (a 16-row tile + ring at grid ratio >= 2)
+constexpr int kFPref = 32;   // L2 prefetch of the template rows the gathers reach kPrefPlanes later
+constexpr int kPrefPlanes = 3;
 
 // events of a steady-state step (compile-time schedule, see Lean::block)
-constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16;
+constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16, kEvS = 32;
 
 struct Smem {
     float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
@@ -59,6 +64,7 @@ struct Smem {
     float Qy[2][kPlane + 2 * kE1X];       // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
     float Xr[3][kE1Y][kWXM];           // x-reduced
+    float Xs[3][kXsRows][kE1X];        // kFStage: x-interpolated y rows of the next deformation plane
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
     float colG[kE1X][3], colGt[kE1X][3], rowG[kE1Y][3], rowGt[kE1Y][3];
@@ -114,7 +120,9 @@ template <int RATIO, int K, int F>
 struct Lean {
     static constexpr int KX = K, KY = K;
     static constexpr bool TMA = (F & kFTma) != 0, PIPE = (F & kFPipe) != 0, LAG = (F & kFLag) != 0;
+    static constexpr bool STAGE = (F & kFStage) != 0;
     static_assert(!(PIPE && LAG), "the lagged (C) and the pipelined gathers are alternatives");
+    static_assert(!(PIPE && STAGE), "staged P_xy is implemented for the register pair only");
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
@@ -126,6 +134,7 @@ struct Lean {
     bool wface_b, wface_c;
     int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo, pstart, pend;
     int x0, y0;
+    int ry0, nrows;  // kFStage: first deformation row of the tile's P_xy and the row count
     float g[8], gfx, gfy, gfz;  // PIPE: template corners and cell fractions of the next plane (in flight)
     float ylo[3], yhi[3];       // !PIPE: P_xy y of this position on deformation planes zd, zd + 1
     float4 rt;                  // !TMA: reference terms of the next (B) plane (prefetched)
@@ -245,6 +254,27 @@ struct Lean {
         return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
+    // kFStage: x-interpolated rows (transfer.py:136-142, x first) of deformation plane zd for
+    // the tile's columns, written cooperatively before a barrier and read after it
+    __device__ __forceinline__ void stage_rows(int zd) {
+        const int per = nrows * kE1X, n = 3 * per;
+        const unsigned mm = (unsigned)(a.ndx * a.ndy * a.ndz);
+        for (int t = threadIdx.x; t < n; t += kNT) {
+            const int comp = t / per, rem = t - comp * per, r = rem / kE1X, ex = rem - r * kE1X;
+            const float wx = sm.colPw[ex], wx0 = __fsub_rn(1.0f, wx);
+            const unsigned o = (unsigned)comp * mm + (unsigned)zd * (unsigned)(a.ndx * a.ndy) +
+                               (unsigned)((ry0 + r) * a.ndx);
+            sm.Xs[comp][r][ex] = lerp_x(__ldg(a.y + o + sm.colP0[ex]), __ldg(a.y + o + sm.colP1[ex]), wx, wx0);
+        }
+    }
+    __device__ __forceinline__ void staged_yplane(float (&out)[3]) const {
+        const int ey = P / kE1X, ex = P - ey * kE1X;
+        const int r0 = sm.rowP0[ey] - ry0, r1 = sm.rowP1[ey] - ry0;
+        const float wy = sm.rowPw[ey], wy0 = __fsub_rn(1.0f, wy);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) out[k] = lerp_x(sm.Xs[k][r0][ex], sm.Xs[k][r1][ex], wy, wy0);
+    }
+
     // (A1) for plane q: yhat = P y (the P_xy pair of this position in shared memory, a new
     // pair when q starts a deformation cell), the cell lookup and the 8 template gathers,
     // left in flight in g[] until (A2) of the next step.  q outside the chunk's A range:
@@ -283,11 +313,15 @@ struct Lean {
                 const int zd = (int)(c.zw[q] & 0xffffu);
                 if (reload) {
                     load_yplane(zd, ylo);
+                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
                 } else {
 #pragma unroll
                     for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+                    if constexpr (STAGE)
+                        staged_yplane(yhi);  // staged by the previous step
+                    else
+                        load_yplane(min(zd + 1, a.ndz - 1), yhi);
                 }
-                load_yplane(min(zd + 1, a.ndz - 1), yhi);
             }
             lo = make_float4(ylo[0], ylo[1], ylo[2], 0.f);
             hi = make_float4(yhi[0], yhi[1], yhi[2], 0.f);
@@ -306,6 +340,15 @@ struct Lean {
         const float* by = b + nx;
         const float* bz = b + nxy;
         const float* byz = bz + nx;
+        if constexpr ((F & kFPref) != 0) {
+            // the template planes a few steps ahead (the cell moves about one plane per step):
+            // first touches of a plane come from HBM, so bring them to L2 before the gathers
+            if (in && iz + kPrefPlanes + 1 < a.nz) {
+                const float* pf = b + kPrefPlanes * nxy;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + nx));
+            }
+        }
         g[0] = __ldg(b);
         g[1] = __ldg(b + 1);
         g[2] = __ldg(by);
@@ -410,6 +453,12 @@ struct Lean {
             sm.dT[R][1][P] = fmaf(gfz, dy1 - dy0, dy0);
             sm.dT[R][2][P] = dz;
         }
+        if constexpr (STAGE) {
+            // plane p+1 starts a deformation cell: stage the rows of its upper plane for the
+            // next step's (A)
+            const bool st = GEN ? (p + 1 > pa0 && p + 1 <= pa1 && (c.zw[p] & kAdv)) : (EV & kEvS) != 0;
+            if (st) stage_rows(min((int)(c.zw[p + 1] & 0xffffu) + 1, a.ndz - 1));
+        }
         if constexpr (TMA) {
             // the reference terms (B) uses after this barrier have landed
             if (threadIdx.x == 0 && (!GEN || (p - 1 >= z0 && p - 1 < z1))) rt_wait(p - 1);
@@ -496,26 +545,27 @@ struct Lean {
         // (kEvA: the (A1) plane p+1 of the step starts a cell)
         // (kEvA0: plane p of the step starts a cell; kEvA: plane p+1 does; LAG: (C) runs on
         // p-3, so its flushes come one step later)
+        // (kEvS: stage the rows of the deformation plane the next step's cell needs)
         if constexpr (RATIO == 4 && LAG) {
             step<0, false, kEvA0>(p);
             step<1, false, 0>(p + 1);
             step<2, false, kEvF | kEvX>(p + 2);
-            step<3, false, kEvY>(p + 3);
+            step<3, false, kEvY | kEvS>(p + 3);
         } else if constexpr (RATIO == 2 && LAG) {
             step<0, false, kEvA0 | kEvF | kEvX>(p);
-            step<1, false, kEvY>(p + 1);
+            step<1, false, kEvY | kEvS>(p + 1);
             step<2, false, kEvA0 | kEvF | kEvX>(p + 2);
-            step<3, false, kEvY>(p + 3);
+            step<3, false, kEvY | kEvS>(p + 3);
         } else if constexpr (RATIO == 4) {
             step<0, false, kEvA0>(p);
             step<1, false, kEvF>(p + 1);
             step<2, false, kEvX>(p + 2);
-            step<3, false, kEvY | kEvA>(p + 3);
+            step<3, false, kEvY | kEvA | kEvS>(p + 3);
         } else if constexpr (RATIO == 2) {
             step<0, false, kEvA0 | kEvX>(p);
-            step<1, false, kEvF | kEvY | kEvA>(p + 1);
+            step<1, false, kEvF | kEvY | kEvA | kEvS>(p + 1);
             step<2, false, kEvA0 | kEvX>(p + 2);
-            step<3, false, kEvF | kEvY | kEvA>(p + 3);
+            step<3, false, kEvF | kEvY | kEvA | kEvS>(p + 3);
         } else {
             generic4(p);
         }
@@ -617,6 +667,10 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 
 
+    __syncthreads();
+    m.ry0 = sm.rowP0[0];
+    m.nrows = min(sm.rowP1[kE1Y - 1] - m.ry0 + 1, kXsRows);
+
     // ---- march state
     m.dacc = 0.f;
 #pragma unroll
@@ -711,13 +765,17 @@ static cudaError_t set_smem(size_t smem) {
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe | kFRing>(smem);
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFLag>(smem);
     if (e == cudaSuccess) e = set_smem1<RATIO, K, kFLag | kFRing>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFStage>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFStage | kFLag>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPref>(smem);
+    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPref | kFStage>(smem);
     return e;
 }
 
 // instance feature set: NGF_LEAN_F = OR of kFTma (1), kFPipe (2), kFRing (4), kFLag (8); default 0
 int feature() {
     static const int f = std::getenv("NGF_LEAN_F") ? std::atoi(std::getenv("NGF_LEAN_F")) : 0;
-    return ((f >= 1 && f <= 6) || f == 8 || f == 12) ? f : 0;
+    return ((f >= 1 && f <= 6) || f == 8 || f == 12 || f == 16 || f == 24 || f == 32 || f == 48) ? f : 0;
 }
 
 }  // namespace lean
@@ -759,6 +817,14 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFLag>), grid, lean::kNT, sb, s, a, c);   \
         else if (f == 12)                                                                        \
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFLag | lean::kFRing>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 16)                                                                        \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFStage>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 24)                                                                        \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFStage | lean::kFLag>), grid, lean::kNT, sb, s, a, c); \
+        else if (f == 32)                                                                        \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPref>), grid, lean::kNT, sb, s, a, c);  \
+        else if (f == 48)                                                                        \
+            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPref | lean::kFStage>), grid, lean::kNT, sb, s, a, c); \
         else if (f == 1)                                                                         \
             NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma>), grid, lean::kNT, sb, s, a, c);   \
         else                                                                                     \
