@@ -484,6 +484,7 @@ def run_ours(args):
     k_ms = float(np.mean(kms))
     info = (ctypes.c_int64 * 9)()
     _lib.check(_lib.lib().ngf_level_info(level.handle, info), "info")
+    variant = int(_lib.lib().ngf_level_variant(level.handle))
     N, M = gi.dims[0] * gi.dims[1] * (zhi - zlo), gd.num_points  # this rank's slab
     bytes_kernel = es * (5 * N + 3 * M)     # T + packed reference terms + y
     bytes_eval = es * (5 * N + 6 * M)       # + grad J written (B_eval: 20N + 24M in f32)
@@ -560,22 +561,12 @@ def run_ours(args):
                "paper_gtx1080ti_s": 1.99,
                "pairs_per_s": ws / reg_s,
                "probe_error": registration_probe(yr, gi, mapping)}
-        # the reference's own run of this pair (tests/golden/make_golden_large.py)
-        fx = os.path.join(ROOT, "tests", "golden", f"register_{args.workload}.npz")
-        if os.path.exists(fx) and rank == 0 and f"y_{args.precision}" in np.load(fx).files:
-            z = np.load(fx)
-            if str(z["R_sha"]) == _sha(R.values.astype(np.float32)) and \
-                    str(z["T_sha"]) == _sha(T.values.astype(np.float32)):
-                mx, inner, mean = field_stats(yr.field, z[f"y_{args.precision}"], gi.spacing[0])
-                reg["vs_reference_run"] = {
-                    "source": f"tests/golden/register_{args.workload}.npz (ngfreg.register, "
-                              f"{int(z['workers'])} CPU workers, build container)",
-                    "max_voxel": mx, "interior_max_voxel": inner, "mean_voxel": mean,
-                    "bar_interior_voxel": BAR_VOXEL, "pass": inner <= BAR_VOXEL,
-                    "iterations": [lv.iterations for lv in rep.levels],
-                    "iterations_reference": [int(v) for v in z[f"iters_{args.precision}"]],
-                    "reference_probe_error_mean_mm": float(z[f"probe_mean_{args.precision}"]),
-                    "reference_seconds": float(z[f"seconds_{args.precision}"])}
+        # the reference's own runs of this pair (tests/golden/make_golden_large.py): with the
+        # default stopping rules (the iteration a relative tolerance fires at is chaotic in the
+        # last bits of the gradient, so those are compared on accuracy) and converged
+        # (tolerances off, fixed budget, ended by the line search): the 0.05-voxel bar
+        if rank == 0:
+            reg["vs_reference_run"] = reference_run_parity(args, R, T, gi, rep, yr, mapping, cfg, ngf)
         # the same with the volumes in page-locked host memory, as the CLI reads them
         pin = []
         for im in (R, T):
@@ -620,10 +611,6 @@ def run_ours(args):
                                        "evals_per_s": 1.0 / s})
             if not args.no_register:
                 regs = same_box_registrations(ref, cores)
-            if reg is not None and "vs_reference_run" in reg:
-                reg["cpu_reference_seconds_note"] = (
-                    "the reference's 256^3 4-level run is ~5 min on 8 cores; its time above is from "
-                    "the build container (not this host); configs 1-2 below are timed on this host")
 
     if rank == 0:
         line = {
@@ -645,8 +632,10 @@ def run_ours(args):
                                        if strong else f"replicas x{ws} (one independent pair per GPU)")},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
-                         "traffic": ncu_traffic(args.workload + ("" if args.precision == "f32" else "_f64")),
-                         "kernel": "k_eval_fused", "kernel_ms": k_ms,
+                         "traffic": ncu_traffic(args.workload + ("" if args.precision == "f32" else "_f64")
+                                                + ("" if variant == 6 else "_classic")),
+                         "kernel": ("k_march_lean" if variant == 6 else "k_eval_fused"), "variant": variant,
+                         "kernel_ms": k_ms,
                          "bytes_per_launch": bytes_kernel, "peak_kind": peak_kind,
                          "eval_frac": bytes_eval / (eval_ms / 1000.0) / 1e9 / peak,
                          "launch": {"ctas": info[0], "smem_bytes": info[1], "z_chunk": info[2]}},
@@ -718,6 +707,48 @@ def run_pairs(args, n_pairs, ws, rank, n, ratio, npdt, cfg, barrier, max_over_ra
             "distinct_pairs_per_rank": distinct,
             "inputs": "pageable host" if args.pairs_pageable else "page-locked host",
             "seconds": batch_s, "pairs_per_s": n_pairs / batch_s, "scaling": "weak (replicas)"}
+
+
+def reference_run_parity(args, R, T, gi, rep, yr, mapping, cfg, ngf):
+    """Final-field parity of the full registration against the reference's own runs of the
+    same pair (tests/golden/register_<workload>[conv].npz)."""
+    out = {}
+    for tag, conv in (("default_rules", ""), ("converged", "conv")):
+        fx = os.path.join(ROOT, "tests", "golden", f"register_{args.workload}{conv}.npz")
+        if not os.path.exists(fx):
+            continue
+        z = np.load(fx)
+        if f"y_{args.precision}" not in z.files:
+            continue
+        if str(z["R_sha"]) != _sha(R.values.astype(np.float32)) or str(z["T_sha"]) != _sha(T.values.astype(np.float32)):
+            out[tag] = {"skipped": "synthetic pair differs from the fixture's"}
+            continue
+        if conv:
+            tol = float(z["tol"])
+            c2 = ngf.MultilevelConfig(num_levels=cfg.num_levels, grid_ratio=cfg.grid_ratio, precision=cfg.precision,
+                                      lbfgs=ngf.LbfgsConfig(max_iterations=int(z["max_iterations"])),
+                                      stopping=ngf.StoppingRules(tol_J=tol, tol_grad=tol, tol_step=tol))
+            t0 = time.perf_counter()
+            yc, repc = ngf.register(R, T, c2)
+            secs = time.perf_counter() - t0
+        else:
+            yc, repc, secs = yr, rep, None
+        mx, inner, mean = field_stats(yc.field, z[f"y_{args.precision}"], gi.spacing[0])
+        probe = registration_probe(yc, gi, mapping)
+        ref_probe = float(z[f"probe_mean_{args.precision}"])
+        gate = inner <= BAR_VOXEL if conv else (probe["mean_mm"] <= ref_probe + 0.05 and mean <= BAR_VOXEL)
+        out[tag] = {"source": f"tests/golden/register_{args.workload}{conv}.npz (ngfreg.register, "
+                              f"{int(z['workers'])} CPU workers, build container, {float(z[f'seconds_{args.precision}']):.0f} s)",
+                    "max_voxel": mx, "interior_max_voxel": inner, "mean_voxel": mean,
+                    "iterations": [lv.iterations for lv in repc.levels],
+                    "iterations_reference": [int(v) for v in z[f"iters_{args.precision}"]],
+                    "probe_error_mean_mm": probe["mean_mm"], "reference_probe_error_mean_mm": ref_probe,
+                    "gate": ("interior max <= 0.05 voxel" if conv else
+                             "probe error within 0.05 mm of the reference's, mean field difference <= 0.05 voxel"),
+                    "pass": bool(gate)}
+        if secs is not None:
+            out[tag]["gpu_seconds"] = secs
+    return out
 
 
 def same_box_registrations(ref, cores):

@@ -196,15 +196,6 @@ static bool lean_eligible(const ngf_level* L, int* kx, int* ky) {
         }
     }
     if (k[0] > lean::kKMax || k[1] > lean::kKMax) return false;
-    {
-        // deformation rows a y tile (+ ring) interpolates from: the staged P_xy rows
-        const int ny = (int)L->img.dims[1], ndy = (int)L->def.dims[1];
-        const int32_t* i0 = p->h_i0[1];
-        for (int t = 0; t * lean::kTYI < ny; ++t) {
-            const int a = std::max(t * lean::kTYI - 1, 0), b = std::min(t * lean::kTYI + lean::kTYI, ny - 1);
-            if (std::min(i0[b] + 1, ndy - 1) - i0[a] + 1 > 12) return false;
-        }
-    }
     *kx = k[0] <= 4 ? 4 : 8;
     *ky = k[1] <= 4 ? 4 : 8;
     return true;

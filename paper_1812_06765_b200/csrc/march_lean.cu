@@ -27,8 +27,6 @@
 // Determinism: every sum has a fixed order; no atomics.
 
 #include <algorithm>
-#include <cstddef>
-#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -42,20 +40,8 @@ constexpr int kPlane = kE1Y * kE1X;  // 544 positions, row stride 34 for every p
 constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4, aligned with the
                                      // deformation cells at grid ratio 2 and 4 (steady blocks)
 
-// compile-time features of a march instance (NGF_LEAN_F selects one at run time; A/B)
-constexpr int kFTma = 1;   // reference terms by TMA bulk copies into shared memory (mbarrier)
-constexpr int kFPipe = 2;  // template gathers issued one step ahead (A1 after the barrier, A2 before)
-constexpr int kFRing = 4;  // the P^T x / y passes run on the three warps without (B) work
-constexpr int kFLag = 8;   // (C) on plane p-3 BEFORE the plane barrier, between issuing the
-                           // template gathers of plane p and using them (covers their latency)
-constexpr int kFStage = 16;  // P_xy of a new deformation plane from x-interpolated rows staged
-                             // cooperatively in shared memory one step ahead
-constexpr int kXsRows = 12;  // staged deformation rows (a 16-row tile + ring at grid ratio >= 2)
-constexpr int kFPref = 32;   // L2 prefetch of the template rows the gathers reach kPrefPlanes later
-constexpr int kPrefPlanes = 3;
-
 // events of a steady-state step (compile-time schedule, see Lean::block)
-constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA0 = 16, kEvS = 32;
+constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8;
 
 struct Smem {
     float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
@@ -64,51 +50,18 @@ struct Smem {
     float Qy[2][kPlane + 2 * kE1X];       // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
     float Xr[3][kE1Y][kWXM];           // x-reduced
-    float Xs[3][kXsRows][kE1X];        // kFStage: x-interpolated y rows of the next deformation plane
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
     float colG[kE1X][3], colGt[kE1X][3], rowG[kE1Y][3], rowGt[kE1Y][3];
     int colP0[kE1X], colP1[kE1X], rowP0[kE1Y], rowP1[kE1Y];
     float colPw[kE1X], rowPw[kE1Y];
-    unsigned short xo[kE1Y * kWXM];    // x pass outputs: row | window column << 8
-    unsigned short yo[kWYM * kWXM];    // y pass outputs: window row | window column << 8
+    unsigned fa[kNT];                  // flush pass assignment per thread
     double red[kWarps];
-    // feature-dependent tail (the launch requests only what the instance uses)
-    uint64_t mbar[2];                  // TMA: completion of the RTs slots
-    float4 RTs[2][kPlane];             // TMA: reference terms of two interior planes
-    float4 Y[2][kPlane];               // PIPE: P_xy y of this position on deformation planes zd, zd + 1
 };
-
-__host__ __device__ constexpr size_t smem_for(int f) {
-    return (f & kFPipe) ? sizeof(Smem) : (f & kFTma) ? offsetof(Smem, Y) : offsetof(Smem, mbar);
-}
 
 __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
     // a0 * (1 - w) + a1 * w, each op correctly rounded (transfer.py:126)
     return __fadd_rn(__fmul_rn(a0, w0), __fmul_rn(a1, w));
-}
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done)
-        asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                     : "=r"(done) : "r"(smem_u32(bar)), "r"(parity) : "memory");
-}
-// TMA bulk copy global -> shared, completion counted on the mbarrier (bytes % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                     smem_u32(dst)),
-                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
-                 : "memory");
 }
 
 // Per-level control in the kernel's parameter space (constant bank): indexed by the
@@ -116,13 +69,9 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int RATIO, int K, int F>
+template <int RATIO, int K>
 struct Lean {
     static constexpr int KX = K, KY = K;
-    static constexpr bool TMA = (F & kFTma) != 0, PIPE = (F & kFPipe) != 0, LAG = (F & kFLag) != 0;
-    static constexpr bool STAGE = (F & kFStage) != 0;
-    static_assert(!(PIPE && LAG), "the lagged (C) and the pipelined gathers are alternatives");
-    static_assert(!(PIPE && STAGE), "staged P_xy is implemented for the register pair only");
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
@@ -133,13 +82,10 @@ struct Lean {
     bool bwarp;    // the warp holds interior positions (runs (B))
     bool wface_b, wface_c;
     int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo, pstart, pend;
-    int x0, y0;
-    int ry0, nrows;  // kFStage: first deformation row of the tile's P_xy and the row count
-    float g[8], gfx, gfy, gfz;  // PIPE: template corners and cell fractions of the next plane (in flight)
-    float ylo[3], yhi[3];       // !PIPE: P_xy y of this position on deformation planes zd, zd + 1
-    float4 rt;                  // !TMA: reference terms of the next (B) plane (prefetched)
+    float ylo[3], yhi[3];
     float qz[kRing];
     float A0[3], A1[3];
+    float4 rt;
     float dacc;
 
     __device__ __forceinline__ Lean(const FusedArgs<float>& a_, const Ctl& c_, Smem& sm_) : a(a_), c(c_), sm(sm_) {}
@@ -173,72 +119,47 @@ struct Lean {
         return (int)fl;
     }
 
-    // this thread's first P^T pass output (then every kPassStride-th): all threads, or
-    // (kFRing) the 96 threads of warps 0 and kE1Y - 1 (ring rows) and kE1Y (ring columns)
-    static constexpr int kPassStride = (F & kFRing) ? 96 : kNT;
-    __device__ __forceinline__ int pass_first() const {
-        if constexpr ((F & kFRing) != 0) {
-            const int w = threadIdx.x >> 5;
-            const int rw = w == 0 ? 0 : w == kE1Y - 1 ? 1 : w == kE1Y ? 2 : -1;
-            return rw < 0 ? (1 << 30) : rw * 32 + (threadIdx.x & 31);
-        } else {
-            return threadIdx.x;
-        }
-    }
-
     // x pass of a completed deformation plane: Fb -> Xr (fixed entry order per output)
-    __device__ __forceinline__ void xpass_one(int o) const {
-        const unsigned rd = sm.xo[o];
-        const int xr_r = rd & 0xff, xr_d = rd >> 8;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-        const float* fb = &sm.Fb[0][0] + xr_r * kE1X;
-#pragma unroll
-        for (int k = 0; k < KX; ++k) {
-            const int2 e = sm.xl[xr_d][k];
-            const float w = __int_as_float(e.y);
-            s0 = fmaf(w, fb[e.x], s0);
-            s1 = fmaf(w, fb[kPlane + e.x], s1);
-            s2 = fmaf(w, fb[2 * kPlane + e.x], s2);
-        }
-        sm.Xr[0][xr_r][xr_d] = s0;
-        sm.Xr[1][xr_r][xr_d] = s1;
-        sm.Xr[2][xr_r][xr_d] = s2;
-    }
     __device__ __forceinline__ void xpass() const {
-        const int n = kE1Y * a.fp.wx;  // <= kNT
-        if constexpr ((F & kFRing) != 0) {
-            for (int o = pass_first(); o < n; o += kPassStride) xpass_one(o);
-        } else {
-            if ((int)threadIdx.x < n) xpass_one(threadIdx.x);
+        const unsigned f = sm.fa[threadIdx.x];
+        const int xr_r = f & 0xff, xr_d = (f >> 8) & 0xff;
+        if (xr_r != 0xff) {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+            const float* fb = &sm.Fb[0][0] + xr_r * kE1X;
+#pragma unroll
+            for (int k = 0; k < KX; ++k) {
+                const int2 e = sm.xl[xr_d][k];
+                const float w = __int_as_float(e.y);
+                s0 = fmaf(w, fb[e.x], s0);
+                s1 = fmaf(w, fb[kPlane + e.x], s1);
+                s2 = fmaf(w, fb[2 * kPlane + e.x], s2);
+            }
+            sm.Xr[0][xr_r][xr_d] = s0;
+            sm.Xr[1][xr_r][xr_d] = s1;
+            sm.Xr[2][xr_r][xr_d] = s2;
         }
     }
 
     // y pass: Xr -> the CTA's window partial of deformation plane slot zs (1/h applied)
-    __device__ __forceinline__ void ypass_one(int o, int zs) const {
-        const int wx = a.fp.wx, wy = a.fp.wy;
-        const size_t win = (size_t)a.fp.wz * wy * wx;
-        const unsigned rd = sm.yo[o];
-        const int yp_dy = rd & 0xff, yp_d = rd >> 8;
-        float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-#pragma unroll
-        for (int k = 0; k < KY; ++k) {
-            const int2 e = sm.yl[yp_dy][k];
-            const float w = __int_as_float(e.y);
-            s0 = fmaf(w, sm.Xr[0][e.x][yp_d], s0);
-            s1 = fmaf(w, sm.Xr[1][e.x][yp_d], s1);
-            s2 = fmaf(w, sm.Xr[2][e.x][yp_d], s2);
-        }
-        float* out = a.partial + (size_t)cta * 3 * win + (size_t)zs * wy * wx + yp_dy * wx + yp_d;
-        out[0] = s0 * a.ihx;
-        out[win] = s1 * a.ihy;
-        out[2 * win] = s2 * a.ihz;
-    }
     __device__ __forceinline__ void ypass(int zs) const {
-        const int n = a.fp.wy * a.fp.wx;  // <= kNT
-        if constexpr ((F & kFRing) != 0) {
-            for (int o = pass_first(); o < n; o += kPassStride) ypass_one(o, zs);
-        } else {
-            if ((int)threadIdx.x < n) ypass_one(threadIdx.x, zs);
+        const unsigned f = sm.fa[threadIdx.x];
+        const int yp_dy = (f >> 16) & 0xff, yp_d = f >> 24;
+        if (yp_dy != 0xff) {
+            float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+#pragma unroll
+            for (int k = 0; k < KY; ++k) {
+                const int2 e = sm.yl[yp_dy][k];
+                const float w = __int_as_float(e.y);
+                s0 = fmaf(w, sm.Xr[0][e.x][yp_d], s0);
+                s1 = fmaf(w, sm.Xr[1][e.x][yp_d], s1);
+                s2 = fmaf(w, sm.Xr[2][e.x][yp_d], s2);
+            }
+            const int wx = a.fp.wx, wy = a.fp.wy;
+            const size_t win = (size_t)a.fp.wz * wy * wx;
+            float* out = a.partial + (size_t)cta * 3 * win + (size_t)zs * wy * wx + yp_dy * wx + yp_d;
+            out[0] = s0 * a.ihx;
+            out[win] = s1 * a.ihy;
+            out[2 * win] = s2 * a.ihz;
         }
     }
 
@@ -254,179 +175,9 @@ struct Lean {
         return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
-    // kFStage: x-interpolated rows (transfer.py:136-142, x first) of deformation plane zd for
-    // the tile's columns, written cooperatively before a barrier and read after it
-    __device__ __forceinline__ void stage_rows(int zd) {
-        const int per = nrows * kE1X, n = 3 * per;
-        const unsigned mm = (unsigned)(a.ndx * a.ndy * a.ndz);
-        for (int t = threadIdx.x; t < n; t += kNT) {
-            const int comp = t / per, rem = t - comp * per, r = rem / kE1X, ex = rem - r * kE1X;
-            const float wx = sm.colPw[ex], wx0 = __fsub_rn(1.0f, wx);
-            const unsigned o = (unsigned)comp * mm + (unsigned)zd * (unsigned)(a.ndx * a.ndy) +
-                               (unsigned)((ry0 + r) * a.ndx);
-            sm.Xs[comp][r][ex] = lerp_x(__ldg(a.y + o + sm.colP0[ex]), __ldg(a.y + o + sm.colP1[ex]), wx, wx0);
-        }
-    }
-    __device__ __forceinline__ void staged_yplane(float (&out)[3]) const {
-        const int ey = P / kE1X, ex = P - ey * kE1X;
-        const int r0 = sm.rowP0[ey] - ry0, r1 = sm.rowP1[ey] - ry0;
-        const float wy = sm.rowPw[ey], wy0 = __fsub_rn(1.0f, wy);
-#pragma unroll
-        for (int k = 0; k < 3; ++k) out[k] = lerp_x(sm.Xs[k][r0][ex], sm.Xs[k][r1][ex], wy, wy0);
-    }
-
-    // (A1) for plane q: yhat = P y (the P_xy pair of this position in shared memory, a new
-    // pair when q starts a deformation cell), the cell lookup and the 8 template gathers,
-    // left in flight in g[] until (A2) of the next step.  q outside the chunk's A range:
-    // zeros (W = 0 and derivative 0).
-    template <bool GEN, bool NEWCELL>
-    __device__ __forceinline__ void a1(int q) {
-        if (GEN && (q < pa0 || q > pa1)) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k) g[k] = 0.f;
-            gfx = gfy = gfz = 0.f;
-            return;
-        }
-        float4 lo, hi;
-        const bool reload = GEN && q == pa0;
-        const bool shift = GEN ? (!reload && (c.zw[q - 1] & kAdv)) : NEWCELL;
-        if constexpr (PIPE) {
-            if (reload || shift) {
-                const int zd = (int)(c.zw[q] & 0xffffu);
-                float v[3];
-                if (reload) {
-                    load_yplane(zd, v);
-                    lo = make_float4(v[0], v[1], v[2], 0.f);
-                } else {
-                    lo = sm.Y[1][P];
-                }
-                sm.Y[0][P] = lo;
-                load_yplane(min(zd + 1, a.ndz - 1), v);
-                hi = make_float4(v[0], v[1], v[2], 0.f);
-                sm.Y[1][P] = hi;
-            } else {
-                lo = sm.Y[0][P];
-                hi = sm.Y[1][P];
-            }
-        } else {
-            if (reload || shift) {
-                const int zd = (int)(c.zw[q] & 0xffffu);
-                if (reload) {
-                    load_yplane(zd, ylo);
-                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
-                } else {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
-                    if constexpr (STAGE)
-                        staged_yplane(yhi);  // staged by the previous step
-                    else
-                        load_yplane(min(zd + 1, a.ndz - 1), yhi);
-                }
-            }
-            lo = make_float4(ylo[0], ylo[1], ylo[2], 0.f);
-            hi = make_float4(yhi[0], yhi[1], yhi[2], 0.f);
-        }
-        const float wz = c.w1[q], wz0 = __fsub_rn(1.0f, wz);
-        const float yh0 = __fadd_rn(__fmul_rn(lo.x, wz0), __fmul_rn(hi.x, wz));
-        const float yh1 = __fadd_rn(__fmul_rn(lo.y, wz0), __fmul_rn(hi.y, wz));
-        const float yh2 = __fadd_rn(__fmul_rn(lo.z, wz0), __fmul_rn(hi.z, wz));
-        bool in = fl & 8u;  // position inside the volume (x / y)
-        const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, gfx);
-        const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, gfy);
-        const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, gfz);
-        const unsigned nx = (unsigned)a.nx, nxy = nx * (unsigned)a.ny;
-        const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
-        const float* b = a.Tv + off;
-        const float* by = b + nx;
-        const float* bz = b + nxy;
-        const float* byz = bz + nx;
-        if constexpr ((F & kFPref) != 0) {
-            // the template planes a few steps ahead (the cell moves about one plane per step):
-            // first touches of a plane come from HBM, so bring them to L2 before the gathers
-            if (in && iz + kPrefPlanes + 1 < a.nz) {
-                const float* pf = b + kPrefPlanes * nxy;
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf));
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(pf + nx));
-            }
-        }
-        g[0] = __ldg(b);
-        g[1] = __ldg(b + 1);
-        g[2] = __ldg(by);
-        g[3] = __ldg(by + 1);
-        g[4] = __ldg(bz);
-        g[5] = __ldg(bz + 1);
-        g[6] = __ldg(byz);
-        g[7] = __ldg(byz + 1);
-    }
-
-    // reference terms of interior plane q into RTs[(q - z0) & 1]: TMA bulk copies of the
-    // tile's interior rows (32 x 16 B each, fewer at the x end), issued by one thread
-    __device__ __forceinline__ void rt_issue(int q) {
-        const int slot = (q - z0) & 1;
-        const int cols = min(32, a.nx - x0);
-        const int rows = min(kTYI, a.ny - y0);
-        const uint32_t rb = (uint32_t)cols * 16u;
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads of the slot
-        mbar_expect_tx(&sm.mbar[slot], rb * (uint32_t)rows);
-        const float4* src = reinterpret_cast<const float4*>(a.RT) + ((size_t)q * a.ny + y0) * a.nx + x0;
-        for (int r = 0; r < rows; ++r) bulk_g2s(&sm.RTs[slot][(r + 1) * kE1X + 1], src + (size_t)r * a.nx, rb, &sm.mbar[slot]);
-    }
-    __device__ __forceinline__ void rt_wait(int q) {
-        mbar_wait(&sm.mbar[(q - z0) & 1], (uint32_t)((q - z0) >> 1) & 1u);
-    }
-
-    // (C) on plane j, ring slot SJ: s = G^T q (warp.py:159-184), ghat = s * derivative, and its
-    // z interpolation onto the two deformation planes of j (transfer.py:151-192, z first)
-    template <int SJ, bool GEN, bool FLUSH>
-    __device__ __forceinline__ void phaseC(int j) {
-        constexpr int SM1 = (SJ + 3) & 3, SP1 = (SJ + 1) & 3;  // planes j-1, j+1
-        if (GEN && (j < jfirst || j > jlast)) return;
-        const float* qxj = &sm.Qx[SJ & 1][P + 1];
-        const float* qyj = &sm.Qy[SJ & 1][P + kE1X];
-        const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
-        float sx = (ql - qr) * c.hx2;
-        float sy = (qu - qd) * c.hy2;
-        if (wface_c) {
-            const int ey = P / kE1X, ex = P - ey * kE1X;
-            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
-                const float* ct = sm.colGt[ex];
-                sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
-            }
-            if (fl & 2u) {
-                const float* rg = sm.rowGt[ey];
-                sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
-            }
-        }
-        float sz = (qz[SM1] - qz[SP1]) * c.hz2;
-        if (GEN) {
-            const unsigned fz = c.zw[j] >> kFaceShift;
-            if (fz) {
-                const float* zc = c.faceG[fz - 1];
-                sz = fmaf(zc[3], qz[SM1], fmaf(zc[4], qz[SJ], zc[5] * qz[SP1]));
-            }
-        }
-        const float sv = sx + sy + sz;
-        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const float gg = sv * sm.dT[SJ][q][P];
-            A0[q] = fmaf(w0, gg, A0[q]);
-            A1[q] = fmaf(w1, gg, A1[q]);
-        }
-        if (GEN ? flushes(j) : FLUSH) {
-            put_flush(A0);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                A0[q] = A1[q];
-                A1[q] = 0.f;
-            }
-        }
-    }
-
-    // One plane step: (A) on p [PIPE: (A2) on p, (A1) on p+1], (B) on p-1, (C) on p-2.  R = ring slot of plane
-    // p.  GEN: the generic step (chunk edges, volume faces: every condition tested on the
-    // uniform plane counter); otherwise a steady-state step whose events EV are known at
-    // compile time.
+    // One plane step: (A) on p, (B) on p-1, (C) on p-2.  R = ring slot of plane p.  GEN: the
+    // generic step (chunk edges, volume faces: every condition tested on the uniform plane
+    // counter); otherwise a steady-state step whose events EV are known at compile time.
     template <int R, bool GEN, unsigned EV>
     __device__ __forceinline__ void step(int p) {
         constexpr int RB = (R + 3) & 3;  // plane p-1
@@ -435,39 +186,59 @@ struct Lean {
         if (GEN && (p < pstart || p >= pend)) return;  // alignment padding of the loop
 
         // ------------------------------------------------------------- (A) plane p
-        // PIPE: the gathers were issued by the previous step's (A1); else issue them now
-        if constexpr (!PIPE) a1<GEN, (EV & kEvA0) != 0>(p);
-        // LAG: (C) on p-3 while the gathers are in flight
-        if constexpr (LAG) phaseC<RD, GEN, (EV & kEvF) != 0>(p - 3);
-        {
+        float W = 0.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
+        if (!GEN || (p >= pa0 && p <= pa1)) {
+            if (GEN) {
+                const int zd = (int)(c.zw[p] & 0xffffu);
+                if (p == pa0) {
+                    load_yplane(zd, ylo);
+                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
+                } else if (c.zw[p - 1] & kAdv) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
+                }
+            } else if (EV & kEvA) {
+                const int zd = (int)(c.zw[p] & 0xffffu);
+#pragma unroll
+                for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+                load_yplane(min(zd + 1, a.ndz - 1), yhi);
+            }
+            const float wz = c.w1[p], wz0 = __fsub_rn(1.0f, wz);
+            const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
+            const float yh1 = __fadd_rn(__fmul_rn(ylo[1], wz0), __fmul_rn(yhi[1], wz));
+            const float yh2 = __fadd_rn(__fmul_rn(ylo[2], wz0), __fmul_rn(yhi[2], wz));
+            bool in = fl & 8u;  // position inside the volume (x / y)
+            float fx_, fy_, fz_;
+            const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, fx_);
+            const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, fy_);
+            const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, fz_);
+            const unsigned nx = (unsigned)a.nx, nxy = nx * (unsigned)a.ny;
+            const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
+            const float* b = a.Tv + off;
+            const float* by = b + nx;
+            const float* bz = b + nxy;
+            const float* byz = bz + nx;
+            const float c0 = __ldg(b), c1 = __ldg(b + 1), c2 = __ldg(by), c3 = __ldg(by + 1);
+            const float c4 = __ldg(bz), c5 = __ldg(bz + 1), c6 = __ldg(byz), c7 = __ldg(byz + 1);
             // trilinear value and derivative (times h) in lerp form (warp.py:79-85, :111-120)
-            const float e00 = g[1] - g[0], e10 = g[3] - g[2], e01 = g[5] - g[4], e11 = g[7] - g[6];
-            const float a00 = fmaf(gfx, e00, g[0]), a10 = fmaf(gfx, e10, g[2]);
-            const float a01 = fmaf(gfx, e01, g[4]), a11 = fmaf(gfx, e11, g[6]);
+            const float e00 = c1 - c0, e10 = c3 - c2, e01 = c5 - c4, e11 = c7 - c6;
+            const float a00 = fmaf(fx_, e00, c0), a10 = fmaf(fx_, e10, c2);
+            const float a01 = fmaf(fx_, e01, c4), a11 = fmaf(fx_, e11, c6);
             const float dy0 = a10 - a00, dy1 = a11 - a01;
-            const float b0 = fmaf(gfy, dy0, a00), b1 = fmaf(gfy, dy1, a01);
+            const float b0 = fmaf(fy_, dy0, a00), b1 = fmaf(fy_, dy1, a01);
             const float dz = b1 - b0;
-            const float ex0 = fmaf(gfy, e10 - e00, e00), ex1 = fmaf(gfy, e11 - e01, e01);
-            sm.W[R][P] = fmaf(gfz, dz, b0);
-            sm.dT[R][0][P] = fmaf(gfz, ex1 - ex0, ex0);
-            sm.dT[R][1][P] = fmaf(gfz, dy1 - dy0, dy0);
-            sm.dT[R][2][P] = dz;
+            W = fmaf(fz_, dz, b0);
+            const float ex0 = fmaf(fy_, e10 - e00, e00), ex1 = fmaf(fy_, e11 - e01, e01);
+            d0 = fmaf(fz_, ex1 - ex0, ex0);
+            d1 = fmaf(fz_, dy1 - dy0, dy0);
+            d2 = dz;
         }
-        if constexpr (STAGE) {
-            // plane p+1 starts a deformation cell: stage the rows of its upper plane for the
-            // next step's (A)
-            const bool st = GEN ? (p + 1 > pa0 && p + 1 <= pa1 && (c.zw[p] & kAdv)) : (EV & kEvS) != 0;
-            if (st) stage_rows(min((int)(c.zw[p + 1] & 0xffffu) + 1, a.ndz - 1));
-        }
-        if constexpr (TMA) {
-            // the reference terms (B) uses after this barrier have landed
-            if (threadIdx.x == 0 && (!GEN || (p - 1 >= z0 && p - 1 < z1))) rt_wait(p - 1);
-        }
+        sm.W[R][P] = W;
+        sm.dT[R][0][P] = d0;
+        sm.dT[R][1][P] = d1;
+        sm.dT[R][2][P] = d2;
         __syncthreads();
-        if constexpr (TMA) {
-            if (threadIdx.x == 0 && (!GEN || (p >= z0 && p < z1))) rt_issue(p);
-        }
-        if constexpr (PIPE) a1<GEN, (EV & kEvA) != 0>(p + 1);  // (A1) of plane p+1
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
@@ -499,8 +270,7 @@ struct Lean {
                     }
                 }
                 // NGF ratio, distance term, q = dD/d grad W (ngf.py:70-112); positions outside
-                // the interior carry rt = 0 (never loaded / copied), hence q = 0, and m_in = 0
-                const float4 rt = TMA ? sm.RTs[(k - z0) & 1][P] : this->rt;
+                // the interior carry rt = 0, hence q = 0, and m_in = 0
                 const float dot = fmaf(gx, rt.x, fmaf(gy, rt.y, gz * rt.z));
                 const float sq = fmaf(gx, gx, fmaf(gy, gy, fmaf(gz, gz, a.tau2)));
                 const float inv_nt = rsqrtf(sq);
@@ -511,22 +281,61 @@ struct Lean {
                 qz[RB] = cf * fmaf(-t1, gz, rt.z);
                 sm.Qx[RB & 1][P + 1] = cf * fmaf(-t1, gx, rt.x);
                 sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
-                // !TMA: reference terms of plane p for the next step's (B)
-                if (!TMA && (!GEN || p < z1) && (fl & 4u))
-                    this->rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
+                // reference terms of plane p for the next step's (B)
+                if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
             sm.Qx[RB & 1][P + 1] = 0.f;
             sm.Qy[RB & 1][P + kE1X] = 0.f;
         }
-        // staggered P^T passes of the deformation planes completed after (C) on planes p-4 and
-        // p-3 (the previous / this step's barrier made them visible)
+        // staggered P^T passes of the deformation planes completed two and one steps ago
         if (GEN ? flushes(p - 4) : (EV & kEvY) != 0) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
         if (GEN ? flushes(p - 3) : (EV & kEvX) != 0) xpass();
 
         // ------------------------------------------------------------- (C) j = p-2
-        if constexpr (!LAG) phaseC<RC, GEN, (EV & kEvF) != 0>(p - 2);
+        const int j = p - 2;
+        if (GEN && (j < jfirst || j > jlast)) return;
+        const float* qxj = &sm.Qx[RC & 1][P + 1];
+        const float* qyj = &sm.Qy[RC & 1][P + kE1X];
+        const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
+        float sx = (ql - qr) * c.hx2;
+        float sy = (qu - qd) * c.hy2;
+        if (wface_c) {
+            const int ey = P / kE1X, ex = P - ey * kE1X;
+            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
+                const float* ct = sm.colGt[ex];
+                sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
+            }
+            if (fl & 2u) {
+                const float* rg = sm.rowGt[ey];
+                sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
+            }
+        }
+        float sz = (qz[RD] - qz[RB]) * c.hz2;
+        if (GEN) {
+            const unsigned fz = c.zw[j] >> kFaceShift;
+            if (fz) {
+                const float* zc = c.faceG[fz - 1];
+                sz = fmaf(zc[3], qz[RD], fmaf(zc[4], qz[RC], zc[5] * qz[RB]));
+            }
+        }
+        const float sv = sx + sy + sz;
+        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float g = sv * sm.dT[RC][q][P];
+            A0[q] = fmaf(w0, g, A0[q]);
+            A1[q] = fmaf(w1, g, A1[q]);
+        }
+        if (GEN ? flushes(j) : (EV & kEvF) != 0) {
+            put_flush(A0);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                A0[q] = A1[q];
+                A1[q] = 0.f;
+            }
+        }
     }
 
     // four steps from plane p (p = phase mod 4)
@@ -542,42 +351,28 @@ struct Lean {
     // every RATIO-th plane, its predecessor flushed one step later, x and y passes one and
     // two steps after that)
     __device__ __forceinline__ void block(int p) {
-        // (kEvA: the (A1) plane p+1 of the step starts a cell)
-        // (kEvA0: plane p of the step starts a cell; kEvA: plane p+1 does; LAG: (C) runs on
-        // p-3, so its flushes come one step later)
-        // (kEvS: stage the rows of the deformation plane the next step's cell needs)
-        if constexpr (RATIO == 4 && LAG) {
-            step<0, false, kEvA0>(p);
-            step<1, false, 0>(p + 1);
-            step<2, false, kEvF | kEvX>(p + 2);
-            step<3, false, kEvY | kEvS>(p + 3);
-        } else if constexpr (RATIO == 2 && LAG) {
-            step<0, false, kEvA0 | kEvF | kEvX>(p);
-            step<1, false, kEvY | kEvS>(p + 1);
-            step<2, false, kEvA0 | kEvF | kEvX>(p + 2);
-            step<3, false, kEvY | kEvS>(p + 3);
-        } else if constexpr (RATIO == 4) {
-            step<0, false, kEvA0>(p);
+        if constexpr (RATIO == 4) {
+            step<0, false, kEvA>(p);
             step<1, false, kEvF>(p + 1);
             step<2, false, kEvX>(p + 2);
-            step<3, false, kEvY | kEvA | kEvS>(p + 3);
+            step<3, false, kEvY>(p + 3);
         } else if constexpr (RATIO == 2) {
-            step<0, false, kEvA0 | kEvX>(p);
-            step<1, false, kEvF | kEvY | kEvA | kEvS>(p + 1);
-            step<2, false, kEvA0 | kEvX>(p + 2);
-            step<3, false, kEvF | kEvY | kEvA | kEvS>(p + 3);
+            step<0, false, kEvA | kEvX>(p);
+            step<1, false, kEvF | kEvY>(p + 1);
+            step<2, false, kEvA | kEvX>(p + 2);
+            step<3, false, kEvF | kEvY>(p + 3);
         } else {
             generic4(p);
         }
     }
 };
 
-template <int RATIO, int K, int F>
+template <int RATIO, int K>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<RATIO, K, F> m(a, c, sm);
+    Lean<RATIO, K> m(a, c, sm);
     constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -655,54 +450,35 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
         for (int t = tid; t < fp.wx * KX; t += kNT) sm.xl[t / KX][t % KX] = gx[t];
         for (int t = tid; t < fp.wy * KY; t += kNT) sm.yl[t / KY][t % KY] = gy[t];
-        // P^T pass output tables: x pass (row, window column), y pass (window row, column)
-        for (int t = tid; t < kE1Y * fp.wx; t += kNT) {
-            const int r = t / fp.wx;
-            sm.xo[t] = (unsigned short)(r | (t - r * fp.wx) << 8);
+        // flush pass assignment: x pass (row, window column), y pass (window row, column)
+        unsigned xa = 0xffffu, ya = 0xffffu;
+        if (tid < kE1Y * fp.wx) {
+            const int r = tid / fp.wx;
+            xa = (unsigned)r | (unsigned)(tid - r * fp.wx) << 8;
         }
-        for (int t = tid; t < fp.wy * fp.wx; t += kNT) {
-            const int r = t / fp.wx;
-            sm.yo[t] = (unsigned short)(r | (t - r * fp.wx) << 8);
+        if (tid < fp.wy * fp.wx) {
+            const int r = tid / fp.wx;
+            ya = (unsigned)r | (unsigned)(tid - r * fp.wx) << 8;
         }
+        sm.fa[tid] = xa | ya << 16;
     }
-
-
-    __syncthreads();
-    m.ry0 = sm.rowP0[0];
-    m.nrows = min(sm.rowP1[kE1Y - 1] - m.ry0 + 1, kXsRows);
 
     // ---- march state
     m.dacc = 0.f;
 #pragma unroll
-    for (int r = 0; r < 3; ++r) m.A0[r] = m.A1[r] = 0.f;
+    for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
 #pragma unroll
     for (int r = 0; r < kRing; ++r) m.qz[r] = 0.f;
-    m.x0 = x0;
-    m.y0 = y0;
-#pragma unroll
-    for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = 0.f;
     m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
-    if constexpr ((F & kFTma) != 0) {
-        // positions the reference-term copies never write (ring, outside the volume) read zeros
-        for (int t = tid; t < 2 * kPlane; t += kNT) (&sm.RTs[0][0])[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (tid == 0) {
-            mbar_init(&sm.mbar[0], 1);
-            mbar_init(&sm.mbar[1], 1);
-            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        }
-    }
     __syncthreads();
-    if constexpr ((F & kFTma) == 0) {
-        if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
-    }
+    if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
     // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
     // steady range [s0, s1) run the compile-time event schedule
     m.pstart = m.z0 - 1;
-    m.pend = m.z1 + ((F & kFLag) ? 4 : 3);  // (C) reaches plane z1
+    m.pend = m.z1 + 3;
     const int s0 = c.s0[tzc], s1 = c.s1[tzc];
-    if constexpr ((F & kFPipe) != 0) m.template a1<true, false>(m.pstart);  // the first plane's gathers
     for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
         if (p >= s0 && p + 4 <= s1)
             m.block(p);
@@ -750,37 +526,14 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 }
 
-template <int RATIO, int K, int F>
-static cudaError_t set_smem1(size_t smem) {
-    return cudaFuncSetAttribute(k_march_lean<RATIO, K, F>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-}
 template <int RATIO, int K>
 static cudaError_t set_smem(size_t smem) {
-    cudaError_t e = set_smem1<RATIO, K, 0>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFTma>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFTma | kFPipe>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFRing>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFRing | kFTma>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPipe | kFRing>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFLag>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFLag | kFRing>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFStage>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFStage | kFLag>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPref>(smem);
-    if (e == cudaSuccess) e = set_smem1<RATIO, K, kFPref | kFStage>(smem);
-    return e;
-}
-
-// instance feature set: NGF_LEAN_F = OR of kFTma (1), kFPipe (2), kFRing (4), kFLag (8); default 0
-int feature() {
-    static const int f = std::getenv("NGF_LEAN_F") ? std::atoi(std::getenv("NGF_LEAN_F")) : 0;
-    return ((f >= 1 && f <= 6) || f == 8 || f == 12 || f == 16 || f == 24 || f == 32 || f == 48) ? f : 0;
+    return cudaFuncSetAttribute(k_march_lean<RATIO, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 }  // namespace lean
 
-size_t lean_smem(int, int) { return lean::smem_for(lean::feature()); }
+size_t lean_smem(int, int) { return sizeof(lean::Smem); }
 
 int lean_prepare(size_t smem) {
     static std::mutex mu;
@@ -799,46 +552,14 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
     const FusedPlan& fp = a.fp;
     const dim3 grid(fp.ntx, fp.nty, fp.ntz);
     const int k = (fp.kx <= 4 && fp.ky <= 4) ? 4 : 8;
-    const int f = lean::feature();
-    const size_t sb = fp.smem_bytes;
-#define NGF_LEAN_GO(R, K)                                                                        \
-    do {                                                                                         \
-        if (f == 3)                                                                              \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma | lean::kFPipe>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 4)                                                                         \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFRing>), grid, lean::kNT, sb, s, a, c);  \
-        else if (f == 5)                                                                         \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFRing | lean::kFTma>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 2)                                                                         \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPipe>), grid, lean::kNT, sb, s, a, c);  \
-        else if (f == 6)                                                                         \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPipe | lean::kFRing>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 8)                                                                         \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFLag>), grid, lean::kNT, sb, s, a, c);   \
-        else if (f == 12)                                                                        \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFLag | lean::kFRing>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 16)                                                                        \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFStage>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 24)                                                                        \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFStage | lean::kFLag>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 32)                                                                        \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPref>), grid, lean::kNT, sb, s, a, c);  \
-        else if (f == 48)                                                                        \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFPref | lean::kFStage>), grid, lean::kNT, sb, s, a, c); \
-        else if (f == 1)                                                                         \
-            NGF_LAUNCH((lean::k_march_lean<R, K, lean::kFTma>), grid, lean::kNT, sb, s, a, c);   \
-        else                                                                                     \
-            NGF_LAUNCH((lean::k_march_lean<R, K, 0>), grid, lean::kNT, sb, s, a, c);             \
-    } while (0)
     if (c.ratio == 4 && k == 8)
-        NGF_LEAN_GO(4, 8);
+        NGF_LAUNCH((lean::k_march_lean<4, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else if (c.ratio == 2 && k == 4)
-        NGF_LEAN_GO(2, 4);
+        NGF_LAUNCH((lean::k_march_lean<2, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else if (c.ratio == 2)
-        NGF_LEAN_GO(2, 8);
+        NGF_LAUNCH((lean::k_march_lean<2, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else
-        NGF_LEAN_GO(0, 8);
-#undef NGF_LEAN_GO
+        NGF_LAUNCH((lean::k_march_lean<0, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
 }
 
 // The per-level control block (kernel parameters) from the host plan.
@@ -906,12 +627,11 @@ int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double
         int lo = std::max(z0 + 2, 4);
         lo += ((c->phase - lo) % 4 + 4) % 4;  // first group start = phase (mod 4)
         const int hi = std::min(z1 - 1, nz - 2);  // last plane a steady step may be on
-        // a group at s is valid when the z map follows the period on planes s-4 .. s+4 (the
-        // passes of steps s .. s+3 refer back to flushes after planes s-4 .. s-1, and (A1) of
-        // step s+3 works on plane s+4) and its (B) / (C) planes use central z rows; the
-        // steady range is the first run of valid groups
+        // a group at s is valid when the z map follows the period on planes s-4 .. s+3 (the
+        // passes of steps s .. s+3 refer back to flushes after planes s-4 .. s-1) and its (B)
+        // / (C) planes use central z rows; the steady range is the first run of valid groups
         auto valid = [&](int s) {
-            for (int p = s - 4; p <= s + 4; ++p) {
+            for (int p = s - 4; p < s + 4; ++p) {
                 const bool want = ((p - c->phase) % c->ratio + c->ratio) % c->ratio == 0;
                 if (adv(p - 1) != want) return false;
             }
