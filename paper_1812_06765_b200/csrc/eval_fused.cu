@@ -381,6 +381,7 @@ void fused_variant_geom(int v, int* ty, int* nt) {
         case 4: *ty = V4::TY; *nt = V4::NT; return;
         case 5: *ty = V5::TY; *nt = V5::NT; return;
         case kLeanVariant: *ty = lean::kTYI; *nt = lean::kNT; return;
+        case kWsVariant: *ty = kWsTYI; *nt = kWsNT; return;
         default: *ty = V0::TY; *nt = V0::NT; return;
     }
 }
@@ -397,6 +398,8 @@ size_t fused_smem(int v, int wx, int wy) {
         case 5: return smem_bytes_cfg<T, V5>(wx, wy);
         case kLeanVariant: return std::is_same<T, float>::value && wx <= lean::kWXM && wy <= lean::kWYM
                                       ? lean_smem(0, 0) : size_t(1) << 30;
+        case kWsVariant: return std::is_same<T, float>::value && wx <= lean::kWXM && wy <= lean::kWYM
+                                    ? ws_smem() : size_t(1) << 30;
         default: return smem_bytes_cfg<T, V0>(wx, wy);
     }
 }
@@ -410,6 +413,7 @@ int fused_prepare<float>(int v, size_t smem) {
         case 4: return march_prepare<float, V4>(smem);
         case 5: return march_prepare<float, V5>(smem);
         case kLeanVariant: return lean_prepare(smem);
+        case kWsVariant: return ws_prepare(smem);
         default: return march_prepare<float, V0>(smem);
     }
 }
@@ -435,6 +439,7 @@ void launch_variant<float>(const FusedArgs<float>& a, cudaStream_t s) {
         case 4: march_launch<float, V4>(a, s); return;
         case 5: march_launch<float, V5>(a, s); return;
         case kLeanVariant: lean_launch(a, *static_cast<const lean::Ctl*>(a.fp.lean_ctl), s); return;
+        case kWsVariant: ws_launch(a, *static_cast<const lean::Ctl*>(a.fp.lean_ctl), s); return;
         default: march_launch<float, V0>(a, s); return;
     }
 }

@@ -43,6 +43,7 @@ struct FusedPlan {
     const void* lean_ctl;  // HOST pointer to the level's lean::Ctl (launch parameters)
 };
 constexpr int kLeanVariant = 6;
+constexpr int kWsVariant = 7;
 constexpr int kCover = 8;
 
 struct LevelDev;  // defined in level.cu

@@ -161,7 +161,7 @@ static bool build_cover(const std::vector<int>& lo, const std::vector<int>& hi, 
 // reciprocal in the cell lookup), the z index map advancing by <= 1 node per image plane
 // and never on two consecutive planes (the staggered P^T flush), and windows / entry counts
 // within the kernel's compile-time bounds.  Returns the entries per window output (x, y).
-static bool lean_eligible(const ngf_level* L, int* kx, int* ky) {
+static bool lean_eligible(const ngf_level* L, int* kx, int* ky, int tyi = lean::kTYI) {
     const ngf_plan_t* p = L->plan;
     if (L->dtype != NGF_F32 || std::getenv("NGF_NO_LEAN")) return false;
     for (int ax = 0; ax < 3; ++ax) {
@@ -177,7 +177,7 @@ static bool lean_eligible(const ngf_level* L, int* kx, int* ky) {
     }
     // entries per window output: image columns (rows) of a tile + ring feeding one node
     int k[2] = {0, 0};
-    const int tile[2] = {kTX, lean::kTYI};
+    const int tile[2] = {kTX, tyi};
     for (int ax = 0; ax < 2; ++ax) {
         const int n = (int)L->img.dims[ax], nd = (int)L->def.dims[ax];
         const int32_t* i0 = p->h_i0[ax];
@@ -220,13 +220,15 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
     // threads with the derivative ring in shared memory take 1.16x the time of 32 x 12
     // tiles of 256 threads per plane for 1.33x the voxels).  Every
     // chunking must keep each def node covered by at most kCover chunks (k_post's sum).
-    static const int kMinBlocks[] = {2, 2, 2, 2, 1, 1, 2};
-    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5, 1.0, 1.14, 1.0};  // f64 (4, 5) relative to 4; lean alone
+    static const int kMinBlocks[] = {2, 2, 2, 2, 1, 1, 2, 1};
+    static const double kPlaneCost[] = {1.6, 1.0, 1.16, 1.5, 1.0, 1.14, 1.0, 1.0};  // f64 (4, 5) relative to 4; lean / ws alone
     // the search depends only on the geometry (dims, slab, index maps), the dtype and the
     // tuning overrides: memoised per process, so repeated registrations of one size (a
     // batch of pairs, config 4) skip it (1.4 ms at 256^3, 4.9 ms at 512^3)
     int lean_kx = 8, lean_ky = 8;
-    const bool lean_ok = sizeof(T) == 4 && lean_eligible(L, &lean_kx, &lean_ky);
+    const char* fv = std::getenv("NGF_FUSED_VARIANT");
+    const bool want_ws = fv && std::atoi(fv) % 8 == kWsVariant;
+    const bool lean_ok = sizeof(T) == 4 && lean_eligible(L, &lean_kx, &lean_ky, want_ws ? kWsTYI : lean::kTYI);
     std::string key = lean_ok ? "lean:" : "classic:";
     {
         const char* ev[] = {"NGF_FUSED_VARIANT", "NGF_FUSED_CZ", "NGF_CHUNK_OVERHEAD"};
@@ -259,8 +261,8 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
         if (sizeof(T) == 8) {  // f64 shapes: 0, 4, 5
             const int v = env ? std::atoi(env) : -1;
             cand = (v == 0 || v == 4 || v == 5) ? std::vector<int>{v} : std::vector<int>{4, 5};
-        } else if (env && (std::atoi(env) % 7 != kLeanVariant || lean_ok)) {
-            const int v = std::atoi(env) % 7;  // f32 shapes: 0 .. 5, 6 = lean
+        } else if (env && ((std::atoi(env) % 8 != kLeanVariant && std::atoi(env) % 8 != kWsVariant) || lean_ok)) {
+            const int v = std::atoi(env) % 8;  // f32 shapes: 0 .. 5, 6 = lean, 7 = warp-specialised
             cand = {v};
         } else if (lean_ok) {
             cand = {kLeanVariant};
@@ -433,7 +435,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
                 }
             }
     };
-    if (variant == kLeanVariant) {
+    if (variant == kLeanVariant || variant == kWsVariant) {
         fp.kx = lean_kx;
         fp.ky = lean_ky;
         if (!L->ctl) L->ctl = new lean::Ctl();
@@ -536,7 +538,7 @@ static FusedArgs<T> fused_args(const ngf_level* L, const void* y) {
     a.hix = (T)(a.nx > 2 ? a.nx - 2 : 0);
     a.hiy = (T)(a.ny > 2 ? a.ny - 2 : 0);
     a.hiz = (T)(a.nz > 2 ? a.nz - 2 : 0);
-    a.Tv = (const T*)(L->fp.variant == kLeanVariant ? L->Tpad : L->T);
+    a.Tv = (const T*)(L->fp.variant == kLeanVariant || L->fp.variant == kWsVariant ? L->Tpad : L->T);
     a.RT = (const V4T<T>*)L->RT;
     a.y = (const T*)y;
     a.partial = (T*)L->partial;

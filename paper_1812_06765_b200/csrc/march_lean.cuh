@@ -48,6 +48,11 @@ struct Ctl {
 }  // namespace lean
 
 int lean_prepare(size_t smem);
+// warp-specialised march (march_ws.cu): same eligibility and control block, 32 x 13 tiles
+constexpr int kWsTYI = 13, kWsNT = 1024;
+size_t ws_smem();
+int ws_prepare(size_t smem);
+void ws_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s);
 size_t lean_smem(int kx, int ky);
 void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s);
 int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double hz, const std::vector<int>& bounds,

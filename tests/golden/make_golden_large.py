@@ -10,6 +10,7 @@ The pairs come from `paper_1812_06765_b200.synthetic.ct_pair` (host numpy, no de
 the fixture stores a SHA-256 of R and T so the GPU test can prove it rebuilt the same
 bytes.  Stored per case: the final field (as float32 for both precisions: ample for a
 0.05-voxel bar, and half the fixture size), per-level iterations / stop reasons, the
+accepted-iterate J trace of every level, the
 reference's probe error against the known mapping (synthetic.py:72-80 lattice,
 evaluation.py:68-90 style mean/max) and the reference's wall time on this host.
 """
@@ -80,6 +81,8 @@ def run(name: str, workers: int):
         out[f"gd_{p}"] = np.array([*y.grid.dims, *y.grid.spacing, *y.grid.origin])
         out[f"iters_{p}"] = np.array([lv.iterations for lv in rep.levels])
         out[f"stops_{p}"] = np.array([lv.stop_reason for lv in rep.levels])
+        for li, lv in enumerate(rep.levels):  # accepted-iterate objective per level (trajectory)
+            out[f"Jtrace_{p}_{li}"] = np.array([r.J for r in lv.records], dtype=np.float64)
         out[f"probe_mean_{p}"] = np.array(err.mean())
         out[f"probe_max_{p}"] = np.array(err.max())
         out[f"seconds_{p}"] = np.array(dt)
