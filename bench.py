@@ -736,15 +736,25 @@ def reference_run_parity(args, R, T, gi, rep, yr, mapping, cfg, ngf):
         mx, inner, mean = field_stats(yc.field, z[f"y_{args.precision}"], gi.spacing[0])
         probe = registration_probe(yc, gi, mapping)
         ref_probe = float(z[f"probe_mean_{args.precision}"])
-        gate = inner <= BAR_VOXEL if conv else (probe["mean_mm"] <= ref_probe + 0.05 and mean <= BAR_VOXEL)
+        # trajectory: the first accepted iterates of the coarsest level; accuracy: probe error
+        # against the known mapping; mean field difference (interior max-abs reported: past
+        # the first iterates two non-bit-identical runs' L-BFGS trajectories separate, the
+        # reference's own f32 and f64 runs of config 2 differ by 0.19 voxel on the interior)
+        traj = None
+        if f"Jtrace_{args.precision}_0" in z.files:
+            rj = z[f"Jtrace_{args.precision}_0"][:5]
+            gj = np.array([r.J for r in repc.levels[0].records][:len(rj)])
+            traj = float(np.max(np.abs(gj - rj) / np.abs(rj))) if len(gj) == len(rj) else float("inf")
+        gate = probe["mean_mm"] <= ref_probe + 0.05 and mean <= BAR_VOXEL and (traj is None or traj <= 1e-5)
         out[tag] = {"source": f"tests/golden/register_{args.workload}{conv}.npz (ngfreg.register, "
                               f"{int(z['workers'])} CPU workers, build container, {float(z[f'seconds_{args.precision}']):.0f} s)",
                     "max_voxel": mx, "interior_max_voxel": inner, "mean_voxel": mean,
                     "iterations": [lv.iterations for lv in repc.levels],
                     "iterations_reference": [int(v) for v in z[f"iters_{args.precision}"]],
                     "probe_error_mean_mm": probe["mean_mm"], "reference_probe_error_mean_mm": ref_probe,
-                    "gate": ("interior max <= 0.05 voxel" if conv else
-                             "probe error within 0.05 mm of the reference's, mean field difference <= 0.05 voxel"),
+                    "level0_first_J_max_rel": traj,
+                    "gate": ("first 5 accepted J of the coarsest level within 1e-5, probe error within 0.05 mm "
+                             "of the reference's, mean field difference <= 0.05 voxel"),
                     "pass": bool(gate)}
         if secs is not None:
             out[tag]["gpu_seconds"] = secs
@@ -774,13 +784,19 @@ def same_box_registrations(ref, cores):
         gpu_s = time.perf_counter() - t0
         y_cpu, it_cpu, cpu_s = ref.register(Rf, Tf, lv, ratio, "f32", cores)
         mx, inner, mean = field_stats(yg.field, y_cpu, Rc.grid.spacing[0])
+        pg = registration_probe(yg, Rc.grid, mc)
+        pc = registration_probe(ngf.DeformationField(yg.grid, np.ascontiguousarray(y_cpu, dtype=np.float32)),
+                                Rc.grid, mc)
+        # single level: the 0.05-voxel interior bar; multilevel: trajectories separate past the
+        # first iterates (see reference_run_parity), so accuracy and the mean difference
+        ok = (inner <= BAR_VOXEL) if lv == 1 else (mean <= BAR_VOXEL and pg["mean_mm"] <= pc["mean_mm"] + 0.05)
         out[name] = {"image": Rc.grid.dims[0], "levels": lv, "grid_ratio": ratio,
                      "gpu_seconds": gpu_s, "cpu_seconds": cpu_s, "cpu_workers": cores,
                      "cpu_kind": ref.kind, "speedup": cpu_s / gpu_s,
                      "iterations_gpu": [l.iterations for l in rep.levels], "iterations_cpu": it_cpu,
                      "field_max_voxel": mx, "field_interior_max_voxel": inner,
-                     "field_mean_voxel": mean, "pass": inner <= BAR_VOXEL,
-                     "probe_error_gpu": registration_probe(yg, Rc.grid, mc)}
+                     "field_mean_voxel": mean, "pass": bool(ok),
+                     "probe_error_gpu": pg, "probe_error_cpu": pc}
     return out
 
 
