@@ -46,9 +46,8 @@ constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8;
 struct Smem {
     float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
     float dT[kRing][3][kPlane];           // interpolant derivative (times h), same ring
-    float Qx[kRing][kPlane + 2];          // q_x at [P + 1] (the ring columns, q = 0, pad the rows)
-    float Qy[kRing][kPlane + 2 * kE1X];   // q_y at [P + 34]: one zero row each side
-    uint64_t mbar;                        // the split plane barrier (one phase per plane)
+    float Qx[2][kPlane + 2];              // q_x at [P + 1] (ring columns, q = 0, pad the rows), by plane parity
+    float Qy[2][kPlane + 2 * kE1X];       // q_y at [P + 34]: one zero row each side
     float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
     float Xr[3][kE1Y][kWXM];           // x-reduced
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
@@ -88,7 +87,6 @@ struct Lean {
     float A0[3], A1[3];
     float4 rt;
     float dacc;
-    uint32_t phase;  // parity of the split plane barrier's current phase
 
     __device__ __forceinline__ Lean(const FusedArgs<float>& a_, const Ctl& c_, Smem& sm_) : a(a_), c(c_), sm(sm_) {}
 
@@ -177,74 +175,7 @@ struct Lean {
         return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
-    // (C) on plane j, ring slot SJ: s = G^T q (warp.py:159-184), ghat = s * derivative, and
-    // its z interpolation onto the two deformation planes of j (transfer.py:151-192, z first)
-    template <int SJ, bool GEN, bool FLUSH>
-    __device__ __forceinline__ void phaseC(int j) {
-        constexpr int SM1 = (SJ + 3) & 3, SP1 = (SJ + 1) & 3;  // planes j-1, j+1
-        if (GEN && (j < jfirst || j > jlast)) return;
-        const float* qxj = &sm.Qx[SJ][P + 1];
-        const float* qyj = &sm.Qy[SJ][P + kE1X];
-        const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
-        float sx = (ql - qr) * c.hx2;
-        float sy = (qu - qd) * c.hy2;
-        if (wface_c) {
-            const int ey = P / kE1X, ex = P - ey * kE1X;
-            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
-                const float* ct = sm.colGt[ex];
-                sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
-            }
-            if (fl & 2u) {
-                const float* rg = sm.rowGt[ey];
-                sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
-            }
-        }
-        float sz = (qz[SM1] - qz[SP1]) * c.hz2;
-        if (GEN) {
-            const unsigned fz = c.zw[j] >> kFaceShift;
-            if (fz) {
-                const float* zc = c.faceG[fz - 1];
-                sz = fmaf(zc[3], qz[SM1], fmaf(zc[4], qz[SJ], zc[5] * qz[SP1]));
-            }
-        }
-        const float sv = sx + sy + sz;
-        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
-#pragma unroll
-        for (int q = 0; q < 3; ++q) {
-            const float gg = sv * sm.dT[SJ][q][P];
-            A0[q] = fmaf(w0, gg, A0[q]);
-            A1[q] = fmaf(w1, gg, A1[q]);
-        }
-        if (GEN ? flushes(j) : FLUSH) {
-            put_flush(A0);
-#pragma unroll
-            for (int q = 0; q < 3; ++q) {
-                A0[q] = A1[q];
-                A1[q] = 0.f;
-            }
-        }
-    }
-
-    // the plane barrier, split: every warp arrives once its W / derivative of plane p are in
-    // shared memory, runs (C) on plane p-3 (which needs nothing written in this step), and
-    // only then waits for the other warps before (B) reads its neighbours' W
-    __device__ __forceinline__ void plane_arrive() {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0)
-            asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(
-                             static_cast<uint32_t>(__cvta_generic_to_shared(&sm.mbar)))
-                         : "memory");
-    }
-    __device__ __forceinline__ void plane_wait() {
-        const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&sm.mbar));
-        uint32_t done = 0;
-        while (!done)
-            asm volatile("{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}"
-                         : "=r"(done) : "r"(bar), "r"(phase) : "memory");
-        phase ^= 1u;
-    }
-
-    // One plane step: (A) on p, (C) on p-3, (B) on p-1.  R = ring slot of plane p.  GEN: the
+    // One plane step: (A) on p, (B) on p-1, (C) on p-2.  R = ring slot of plane p.  GEN: the
     // generic step (chunk edges, volume faces: every condition tested on the uniform plane
     // counter); otherwise a steady-state step whose events EV are known at compile time.
     template <int R, bool GEN, unsigned EV>
@@ -307,10 +238,7 @@ struct Lean {
         sm.dT[R][0][P] = d0;
         sm.dT[R][1][P] = d1;
         sm.dT[R][2][P] = d2;
-        plane_arrive();
-        // ------------------------------------------------------------- (C) j = p-3
-        phaseC<RD, GEN, (EV & kEvF) != 0>(p - 3);
-        plane_wait();
+        __syncthreads();
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
@@ -351,20 +279,63 @@ struct Lean {
                 const float t1 = r * inv_nt;
                 const float cf = a.neg_hbar * t1;
                 qz[RB] = cf * fmaf(-t1, gz, rt.z);
-                sm.Qx[RB][P + 1] = cf * fmaf(-t1, gx, rt.x);
-                sm.Qy[RB][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
+                sm.Qx[RB & 1][P + 1] = cf * fmaf(-t1, gx, rt.x);
+                sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
                 // reference terms of plane p for the next step's (B)
                 if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
-            sm.Qx[RB][P + 1] = 0.f;
-            sm.Qy[RB][P + kE1X] = 0.f;
+            sm.Qx[RB & 1][P + 1] = 0.f;
+            sm.Qy[RB & 1][P + kE1X] = 0.f;
         }
         // staggered P^T passes of the deformation planes completed two and one steps ago
         if (GEN ? flushes(p - 4) : (EV & kEvY) != 0) ypass((int)(c.zw[p - 4] & 0xffffu) - wzlo);
         if (GEN ? flushes(p - 3) : (EV & kEvX) != 0) xpass();
 
+        // ------------------------------------------------------------- (C) j = p-2
+        const int j = p - 2;
+        if (GEN && (j < jfirst || j > jlast)) return;
+        const float* qxj = &sm.Qx[RC & 1][P + 1];
+        const float* qyj = &sm.Qy[RC & 1][P + kE1X];
+        const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
+        float sx = (ql - qr) * c.hx2;
+        float sy = (qu - qd) * c.hy2;
+        if (wface_c) {
+            const int ey = P / kE1X, ex = P - ey * kE1X;
+            if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
+                const float* ct = sm.colGt[ex];
+                sx = fmaf(ct[0], ql, fmaf(ct[1], qxj[0], ct[2] * qr));
+            }
+            if (fl & 2u) {
+                const float* rg = sm.rowGt[ey];
+                sy = fmaf(rg[0], qu, fmaf(rg[1], qyj[0], rg[2] * qd));
+            }
+        }
+        float sz = (qz[RD] - qz[RB]) * c.hz2;
+        if (GEN) {
+            const unsigned fz = c.zw[j] >> kFaceShift;
+            if (fz) {
+                const float* zc = c.faceG[fz - 1];
+                sz = fmaf(zc[3], qz[RD], fmaf(zc[4], qz[RC], zc[5] * qz[RB]));
+            }
+        }
+        const float sv = sx + sy + sz;
+        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+            const float g = sv * sm.dT[RC][q][P];
+            A0[q] = fmaf(w0, g, A0[q]);
+            A1[q] = fmaf(w1, g, A1[q]);
+        }
+        if (GEN ? flushes(j) : (EV & kEvF) != 0) {
+            put_flush(A0);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) {
+                A0[q] = A1[q];
+                A1[q] = 0.f;
+            }
+        }
     }
 
     // four steps from plane p (p = phase mod 4)
@@ -380,18 +351,16 @@ struct Lean {
     // every RATIO-th plane, its predecessor flushed one step later, x and y passes one and
     // two steps after that)
     __device__ __forceinline__ void block(int p) {
-        // ((C) runs on p-3: the flush after plane j happens in step j+3, its x pass after that
-        // step's barrier, its y pass one step later)
         if constexpr (RATIO == 4) {
             step<0, false, kEvA>(p);
-            step<1, false, 0>(p + 1);
-            step<2, false, kEvF | kEvX>(p + 2);
+            step<1, false, kEvF>(p + 1);
+            step<2, false, kEvX>(p + 2);
             step<3, false, kEvY>(p + 3);
         } else if constexpr (RATIO == 2) {
-            step<0, false, kEvA | kEvF | kEvX>(p);
-            step<1, false, kEvY>(p + 1);
-            step<2, false, kEvA | kEvF | kEvX>(p + 2);
-            step<3, false, kEvY>(p + 3);
+            step<0, false, kEvA | kEvX>(p);
+            step<1, false, kEvF | kEvY>(p + 1);
+            step<2, false, kEvA | kEvX>(p + 2);
+            step<3, false, kEvF | kEvY>(p + 3);
         } else {
             generic4(p);
         }
@@ -474,14 +443,8 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : 0.f;
     }
-    for (int t = tid; t < kRing * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
-    for (int t = tid; t < kRing * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
-    if (tid == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(&sm.mbar))),
-                     "r"(kWarps)
-                     : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    for (int t = tid; t < 2 * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
+    for (int t = tid; t < 2 * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
     {
         const int2* gx = reinterpret_cast<const int2*>(fp.lx) + (size_t)tx * fp.wx * KX;
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
@@ -502,7 +465,6 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
 
     // ---- march state
     m.dacc = 0.f;
-    m.phase = 0u;
 #pragma unroll
     for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
 #pragma unroll
@@ -515,7 +477,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
     // steady range [s0, s1) run the compile-time event schedule
     m.pstart = m.z0 - 1;
-    m.pend = m.z1 + 4;  // (C) on p-3 reaches plane z1
+    m.pend = m.z1 + 3;
     const int s0 = c.s0[tzc], s1 = c.s1[tzc];
     for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
         if (p >= s0 && p + 4 <= s1)

@@ -97,3 +97,19 @@ def test_benchmark_subcommand(tmp_path):
                  "--reps", "3", "--out", out]) == EXIT_OK
     text = open(out).read()
     assert "redblack" in text and text.count("\n") == 1 + 5
+
+
+def test_benchmark_checksums_equal_the_reference():
+    """The device harness and the reference's (ngfreg.benchmark.run_benchmark, staged in
+    oracle/_ref) hash identical results for the exact operators on the same inputs."""
+    from oracle import ref as oref
+    from paper_1812_06765_b200.benchmark import run_benchmark
+    mod = oref.load()
+    if mod is None:
+        pytest.skip("reference not staged (oracle/build_ref.py)")
+    from ngfreg import benchmark as rb
+    kw = dict(dims=(16, 16, 16), workers_list=(1,), precisions=("f64",), variants=("gather", "redblack"), reps=3)
+    ours = {(r.operation, r.variant): r.checksum for r in run_benchmark(**kw)}
+    ref = {(r.operation, r.variant): r.checksum for r in rb.run_benchmark(**kw)}
+    for key in [("apply_P", "-"), ("apply_Pt", "gather"), ("apply_Pt", "redblack"), ("ngf_value_grad", "gather")]:
+        assert ours[key] == ref[key], key
