@@ -69,9 +69,16 @@ __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int RATIO, int K>
+template <int RATIO, int K, int NXY = 0>
 struct Lean {
     static constexpr int KX = K, KY = K;
+    // NXY > 0: a square NXY x NXY image plane known at compile time, so the 8 template
+    // corners of a position are one address plus immediate offsets and the plane stride of
+    // the reference terms is a constant
+    __device__ __forceinline__ unsigned nx_() const { return NXY ? (unsigned)NXY : (unsigned)a.nx; }
+    __device__ __forceinline__ unsigned nxy_() const {
+        return NXY ? (unsigned)NXY * (unsigned)NXY : (unsigned)a.nx * (unsigned)a.ny;
+    }
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
@@ -213,7 +220,7 @@ struct Lean {
             const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, fx_);
             const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, fy_);
             const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, fz_);
-            const unsigned nx = (unsigned)a.nx, nxy = nx * (unsigned)a.ny;
+            const unsigned nx = nx_(), nxy = nxy_();
             const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
             const float* b = a.Tv + off;
             const float* by = b + nx;
@@ -282,7 +289,7 @@ struct Lean {
                 sm.Qx[RB & 1][P + 1] = cf * fmaf(-t1, gx, rt.x);
                 sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
                 // reference terms of plane p for the next step's (B)
-                if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * ((size_t)a.nx * a.ny) + ij);
+                if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * nxy_() + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
@@ -367,12 +374,12 @@ struct Lean {
     }
 };
 
-template <int RATIO, int K>
+template <int RATIO, int K, int NXY>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<RATIO, K> m(a, c, sm);
+    Lean<RATIO, K, NXY> m(a, c, sm);
     constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -526,9 +533,35 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 }
 
-template <int RATIO, int K>
+template <int RATIO, int K, int NXY>
 static cudaError_t set_smem(size_t smem) {
-    return cudaFuncSetAttribute(k_march_lean<RATIO, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_march_lean<RATIO, K, NXY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+}
+
+// square power-of-two image planes with a compile-time size (the pyramid levels of the
+// configurations: 32 .. 512); any other plane runs the runtime-size instance
+template <int RATIO, int K>
+static cudaError_t set_smem_all(size_t smem) {
+    cudaError_t e = set_smem<RATIO, K, 0>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 32>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 64>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 128>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 256>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 512>(smem);
+    return e;
+}
+
+template <int RATIO, int K>
+static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, size_t sb, cudaStream_t s) {
+    const int n = a.nx == a.ny ? a.nx : 0;
+    switch (n) {
+        case 32: NGF_LAUNCH((k_march_lean<RATIO, K, 32>), grid, kNT, sb, s, a, c); break;
+        case 64: NGF_LAUNCH((k_march_lean<RATIO, K, 64>), grid, kNT, sb, s, a, c); break;
+        case 128: NGF_LAUNCH((k_march_lean<RATIO, K, 128>), grid, kNT, sb, s, a, c); break;
+        case 256: NGF_LAUNCH((k_march_lean<RATIO, K, 256>), grid, kNT, sb, s, a, c); break;
+        case 512: NGF_LAUNCH((k_march_lean<RATIO, K, 512>), grid, kNT, sb, s, a, c); break;
+        default: NGF_LAUNCH((k_march_lean<RATIO, K, 0>), grid, kNT, sb, s, a, c); break;
+    }
 }
 
 }  // namespace lean
@@ -540,10 +573,10 @@ int lean_prepare(size_t smem) {
     static size_t granted = 0;
     std::lock_guard<std::mutex> lk(mu);
     if (smem <= granted) return 0;
-    cudaError_t e = lean::set_smem<4, 8>(smem);
-    if (e == cudaSuccess) e = lean::set_smem<2, 4>(smem);
-    if (e == cudaSuccess) e = lean::set_smem<2, 8>(smem);
-    if (e == cudaSuccess) e = lean::set_smem<0, 8>(smem);
+    cudaError_t e = lean::set_smem_all<4, 8>(smem);
+    if (e == cudaSuccess) e = lean::set_smem_all<2, 4>(smem);
+    if (e == cudaSuccess) e = lean::set_smem<2, 8, 0>(smem);
+    if (e == cudaSuccess) e = lean::set_smem<0, 8, 0>(smem);
     if (e == cudaSuccess) granted = smem;
     return (int)e;
 }
@@ -553,13 +586,13 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
     const dim3 grid(fp.ntx, fp.nty, fp.ntz);
     const int k = (fp.kx <= 4 && fp.ky <= 4) ? 4 : 8;
     if (c.ratio == 4 && k == 8)
-        NGF_LAUNCH((lean::k_march_lean<4, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        lean::launch_sized<4, 8>(a, c, grid, fp.smem_bytes, s);
     else if (c.ratio == 2 && k == 4)
-        NGF_LAUNCH((lean::k_march_lean<2, 4>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        lean::launch_sized<2, 4>(a, c, grid, fp.smem_bytes, s);
     else if (c.ratio == 2)
-        NGF_LAUNCH((lean::k_march_lean<2, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LAUNCH((lean::k_march_lean<2, 8, 0>), grid, lean::kNT, fp.smem_bytes, s, a, c);
     else
-        NGF_LAUNCH((lean::k_march_lean<0, 8>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        NGF_LAUNCH((lean::k_march_lean<0, 8, 0>), grid, lean::kNT, fp.smem_bytes, s, a, c);
 }
 
 // The per-level control block (kernel parameters) from the host plan.
