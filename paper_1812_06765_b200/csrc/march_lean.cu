@@ -27,6 +27,7 @@
 // Determinism: every sum has a fixed order; no atomics.
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -69,7 +70,7 @@ __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int RATIO, int K, int NXY = 0>
+template <int RATIO, int K, int NXY = 0, bool PACK = false>
 struct Lean {
     static constexpr int KX = K, KY = K;
     // NXY > 0: a square NXY x NXY image plane known at compile time, so the 8 template
@@ -229,17 +230,35 @@ struct Lean {
             const float c0 = __ldg(b), c1 = __ldg(b + 1), c2 = __ldg(by), c3 = __ldg(by + 1);
             const float c4 = __ldg(bz), c5 = __ldg(bz + 1), c6 = __ldg(byz), c7 = __ldg(byz + 1);
             // trilinear value and derivative (times h) in lerp form (warp.py:79-85, :111-120)
-            const float e00 = c1 - c0, e10 = c3 - c2, e01 = c5 - c4, e11 = c7 - c6;
-            const float a00 = fmaf(fx_, e00, c0), a10 = fmaf(fx_, e10, c2);
-            const float a01 = fmaf(fx_, e01, c4), a11 = fmaf(fx_, e11, c6);
-            const float dy0 = a10 - a00, dy1 = a11 - a01;
-            const float b0 = fmaf(fy_, dy0, a00), b1 = fmaf(fy_, dy1, a01);
-            const float dz = b1 - b0;
-            W = fmaf(fz_, dz, b0);
-            const float ex0 = fmaf(fy_, e10 - e00, e00), ex1 = fmaf(fy_, e11 - e01, e01);
-            d0 = fmaf(fz_, ex1 - ex0, ex0);
-            d1 = fmaf(fz_, dy1 - dy0, dy0);
-            d2 = dz;
+            if constexpr (PACK) {
+                // the bottom / top z corner pairs as f32x2: one FFMA2 / FADD2 per pair of lerps
+                const float2 m1 = make_float2(-1.f, -1.f);
+                const float2 z0 = make_float2(c0, c4), z1 = make_float2(c1, c5);
+                const float2 z2 = make_float2(c2, c6), z3 = make_float2(c3, c7);
+                const float2 fx2 = make_float2(fx_, fx_), fy2 = make_float2(fy_, fy_);
+                const float2 e0 = __ffma2_rn(z0, m1, z1), e1 = __ffma2_rn(z2, m1, z3);  // (e00, e01), (e10, e11)
+                const float2 a0 = __ffma2_rn(fx2, e0, z0), a1 = __ffma2_rn(fx2, e1, z2);
+                const float2 dy = __ffma2_rn(a0, m1, a1);                                // (dy0, dy1)
+                const float2 bb = __ffma2_rn(fy2, dy, a0);                               // (b0, b1)
+                const float2 ex = __ffma2_rn(fy2, __ffma2_rn(e0, m1, e1), e0);           // (ex0, ex1)
+                const float dz = bb.y - bb.x;
+                W = fmaf(fz_, dz, bb.x);
+                d0 = fmaf(fz_, ex.y - ex.x, ex.x);
+                d1 = fmaf(fz_, dy.y - dy.x, dy.x);
+                d2 = dz;
+            } else {
+                const float e00 = c1 - c0, e10 = c3 - c2, e01 = c5 - c4, e11 = c7 - c6;
+                const float a00 = fmaf(fx_, e00, c0), a10 = fmaf(fx_, e10, c2);
+                const float a01 = fmaf(fx_, e01, c4), a11 = fmaf(fx_, e11, c6);
+                const float dy0 = a10 - a00, dy1 = a11 - a01;
+                const float b0 = fmaf(fy_, dy0, a00), b1 = fmaf(fy_, dy1, a01);
+                const float dz = b1 - b0;
+                W = fmaf(fz_, dz, b0);
+                const float ex0 = fmaf(fy_, e10 - e00, e00), ex1 = fmaf(fy_, e11 - e01, e01);
+                d0 = fmaf(fz_, ex1 - ex0, ex0);
+                d1 = fmaf(fz_, dy1 - dy0, dy0);
+                d2 = dz;
+            }
         }
         sm.W[R][P] = W;
         sm.dT[R][0][P] = d0;
@@ -374,12 +393,12 @@ struct Lean {
     }
 };
 
-template <int RATIO, int K, int NXY>
+template <int RATIO, int K, int NXY, bool PACK = false>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<RATIO, K, NXY> m(a, c, sm);
+    Lean<RATIO, K, NXY, PACK> m(a, c, sm);
     constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -548,12 +567,29 @@ static cudaError_t set_smem_all(size_t smem) {
     if (e == cudaSuccess) e = set_smem<RATIO, K, 128>(smem);
     if (e == cudaSuccess) e = set_smem<RATIO, K, 256>(smem);
     if (e == cudaSuccess) e = set_smem<RATIO, K, 512>(smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return e;
+}
+
+static bool packed() {
+    static const bool on = std::getenv("NGF_LEAN_PACK") && std::atoi(std::getenv("NGF_LEAN_PACK")) != 0;
+    return on;
 }
 
 template <int RATIO, int K>
 static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, size_t sb, cudaStream_t s) {
     const int n = a.nx == a.ny ? a.nx : 0;
+    if (packed() && n == 256) {
+        NGF_LAUNCH((k_march_lean<RATIO, K, 256, true>), grid, kNT, sb, s, a, c);
+        return;
+    }
+    if (packed() && n == 128) {
+        NGF_LAUNCH((k_march_lean<RATIO, K, 128, true>), grid, kNT, sb, s, a, c);
+        return;
+    }
     switch (n) {
         case 32: NGF_LAUNCH((k_march_lean<RATIO, K, 32>), grid, kNT, sb, s, a, c); break;
         case 64: NGF_LAUNCH((k_march_lean<RATIO, K, 64>), grid, kNT, sb, s, a, c); break;
