@@ -37,7 +37,9 @@
 namespace ngf {
 namespace lean {
 
-constexpr int kPlane = kE1Y * kE1X;  // 544 positions, row stride 34 for every per-position plane
+constexpr int kPlane = kE1Y * kE1X;  // positions, row stride 34 for every per-position plane
+constexpr int kSink = kPlane;        // the position of ring-column lanes beyond 2 * kE1Y
+constexpr int kPl = kPlane + kE1X + 2;  // per-position plane incl. the sink and its neighbours
 constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4, aligned with the
                                      // deformation cells at grid ratio 2 and 4 (steady blocks)
 
@@ -45,11 +47,11 @@ constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4
 constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8;
 
 struct Smem {
-    float W[kRing][kPlane];               // W of planes p-3 .. p (ring by (plane - phase) mod 4)
-    float dT[kRing][3][kPlane];           // interpolant derivative (times h), same ring
-    float Qx[2][kPlane + 2];              // q_x at [P + 1] (ring columns, q = 0, pad the rows), by plane parity
-    float Qy[2][kPlane + 2 * kE1X];       // q_y at [P + 34]: one zero row each side
-    float Fb[3][kPlane];               // completed deformation plane (z-reduced ghat / h)
+    float W[kRing][kPl];                  // W of planes p-3 .. p (ring by (plane - phase) mod 4)
+    float dT[kRing][3][kPl];              // interpolant derivative (times h), same ring
+    float Qx[2][kPl + 2];                 // q_x at [P + 1] (ring columns, q = 0, pad the rows), by plane parity
+    float Qy[2][kPl + 2 * kE1X];          // q_y at [P + 34]: one zero row each side
+    float Fb[3][kPl];                     // completed deformation plane (z-reduced ghat / h)
     float Xr[3][kE1Y][kWXM];           // x-reduced
     int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
@@ -100,7 +102,8 @@ struct Lean {
 
     __device__ __forceinline__ void load_yplane(int zd, float (&out)[3]) const {
         // P_xy y on def plane zd at this position's image (x, y): x then y (transfer.py:136-142)
-        const int ey = P / kE1X, ex = P - ey * kE1X;
+        // (the sink lanes read a valid table entry; their samples are redirected to the pad)
+        const int ey = min(P / kE1X, kE1Y - 1), ex = P - (P / kE1X) * kE1X;
         const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
         const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
         const float wx = sm.colPw[ex], wy = sm.rowPw[ey];
@@ -139,8 +142,8 @@ struct Lean {
                 const int2 e = sm.xl[xr_d][k];
                 const float w = __int_as_float(e.y);
                 s0 = fmaf(w, fb[e.x], s0);
-                s1 = fmaf(w, fb[kPlane + e.x], s1);
-                s2 = fmaf(w, fb[2 * kPlane + e.x], s2);
+                s1 = fmaf(w, fb[kPl + e.x], s1);
+                s2 = fmaf(w, fb[2 * kPl + e.x], s2);
             }
             sm.Xr[0][xr_r][xr_d] = s0;
             sm.Xr[1][xr_r][xr_d] = s1;
@@ -418,16 +421,18 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // ---- this thread's position: row warps own columns 1..32 of one row, the last warp
     // the ring columns 0 and 33 of all rows
     int ex, ey;
+    bool has = true;  // ring-column lanes beyond 2 * kE1Y hold no position (the sink)
     if (warp < kE1Y) {
         ey = warp;
         ex = lane + 1;
     } else {
-        ey = lane & 15;
-        ex = lane < 16 ? 0 : kE1X - 1;
+        has = lane < 2 * kE1Y;
+        ey = has ? (lane < kE1Y ? lane : lane - kE1Y) : 0;
+        ex = lane < kE1Y ? 0 : kE1X - 1;
     }
-    m.P = ey * kE1X + ex;
+    m.P = has ? ey * kE1X + ex : kSink;
     const int x = x0 - 1 + ex, yy = y0 - 1 + ey;
-    const bool vol = x >= 0 && x < a.nx && yy >= 0 && yy < a.ny;
+    const bool vol = has && x >= 0 && x < a.nx && yy >= 0 && yy < a.ny;
     const bool inter = vol && warp >= 1 && warp <= kTYI;
     m.ij = vol ? (unsigned)(yy * a.nx + x) : 0u;
     bool fx, fy;
@@ -469,8 +474,8 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         sm.rowP1[e] = min(i0 + 1, a.ndy - 1);
         sm.rowPw[e] = in ? a.w1y[jj] : 0.f;
     }
-    for (int t = tid; t < 2 * (kPlane + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
-    for (int t = tid; t < 2 * (kPlane + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
+    for (int t = tid; t < 2 * (kPl + 2); t += kNT) (&sm.Qx[0][0])[t] = 0.f;
+    for (int t = tid; t < 2 * (kPl + 2 * kE1X); t += kNT) (&sm.Qy[0][0])[t] = 0.f;
     {
         const int2* gx = reinterpret_cast<const int2*>(fp.lx) + (size_t)tx * fp.wx * KX;
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;

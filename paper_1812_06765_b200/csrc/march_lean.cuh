@@ -12,9 +12,13 @@ namespace lean {
 // positions).  Row warps 0..TYI+1 own the 32 columns x0..x0+31 of one E1 row each; one
 // ring-column warp owns columns x0-1 and x0+32 of all TYI+2 rows (16 + 16 lanes), so
 // every lane of every warp holds a position and the tile is exactly 32 wide in x.
-constexpr int kTYI = 14;
+#ifndef NGF_LEAN_TYI
+#define NGF_LEAN_TYI 13
+#endif
+constexpr int kTYI = NGF_LEAN_TYI;
 constexpr int kE1X = 34, kE1Y = kTYI + 2;
-constexpr int kWarps = kE1Y + 1;  // 17
+constexpr int kWarps = kE1Y + 1;  // the row warps + the ring-column warp
+static_assert(2 * kE1Y <= 32, "the ring columns of all rows fit one warp");
 constexpr int kNT = 32 * kWarps;  // 544
 constexpr int kWXM = 20;          // max P^T window outputs in x (34 columns at grid ratio >= 2)
 constexpr int kWYM = 12;          // max window outputs in y (16 rows at ratio >= 2)
