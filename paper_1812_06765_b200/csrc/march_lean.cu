@@ -44,7 +44,7 @@ constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4
                                      // deformation cells at grid ratio 2 and 4 (steady blocks)
 
 // events of a steady-state step (compile-time schedule, see Lean::block)
-constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8;
+constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA1 = 16;  // kEvA1: plane p+1 starts a cell
 
 struct Smem {
     float W[kRing][kPl];                  // W of planes p-3 .. p (ring by (plane - phase) mod 4)
@@ -72,7 +72,7 @@ __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int RATIO, int K, int NXY = 0, bool PACK = false>
+template <int RATIO, int K, int NXY = 0, bool PACK = false, bool PIPE = false>
 struct Lean {
     static constexpr int KX = K, KY = K;
     // NXY > 0: a square NXY x NXY image plane known at compile time, so the 8 template
@@ -93,6 +93,7 @@ struct Lean {
     bool wface_b, wface_c;
     int cta, z0, z1, pa0, pa1, jfirst, jlast, wzlo, pstart, pend;
     float ylo[3], yhi[3];
+    float g[8], gfx, gfy, gfz;  // the template corners and cell fractions of the next (A2)
     float qz[kRing];
     float A0[3], A1[3];
     float4 rt;
@@ -186,6 +187,87 @@ struct Lean {
         return j >= jfirst && j < jlast && (c.zw[j] & kAdv);
     }
 
+    // (A1) plane q: yhat = P y (the P_xy pair of the position in registers, shifted /
+    // reloaded when q starts a deformation cell), the cell lookup and the 8 template corner
+    // reads (outside the hull: the zero pad), left in g[] / f*; q outside the chunk's A
+    // range gives zeros (W = 0, derivative 0)
+    template <bool GEN, bool NEWCELL>
+    __device__ __forceinline__ void a1(int q) {
+        if (GEN && (q < pa0 || q > pa1)) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k) g[k] = 0.f;
+            gfx = gfy = gfz = 0.f;
+            return;
+        }
+        const bool reload = GEN && q == pa0;
+        if (reload || (GEN ? (c.zw[q - 1] & kAdv) != 0 : NEWCELL)) {
+            const int zd = (int)(c.zw[q] & 0xffffu);
+            if (reload) {
+                load_yplane(zd, ylo);
+            } else {
+#pragma unroll
+                for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
+            }
+            load_yplane(min(zd + 1, a.ndz - 1), yhi);
+        }
+        const float wz = c.w1[q], wz0 = __fsub_rn(1.0f, wz);
+        const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
+        const float yh1 = __fadd_rn(__fmul_rn(ylo[1], wz0), __fmul_rn(yhi[1], wz));
+        const float yh2 = __fadd_rn(__fmul_rn(ylo[2], wz0), __fmul_rn(yhi[2], wz));
+        bool in = fl & 8u;  // position inside the volume (x / y)
+        const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, gfx);
+        const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, gfy);
+        const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, gfz);
+        const unsigned nx = nx_(), nxy = nxy_();
+        const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
+        const float* b = a.Tv + off;
+        const float* by = b + nx;
+        const float* bz = b + nxy;
+        const float* byz = bz + nx;
+        g[0] = __ldg(b);
+        g[1] = __ldg(b + 1);
+        g[2] = __ldg(by);
+        g[3] = __ldg(by + 1);
+        g[4] = __ldg(bz);
+        g[5] = __ldg(bz + 1);
+        g[6] = __ldg(byz);
+        g[7] = __ldg(byz + 1);
+    }
+
+    // (A2): the trilinear value and derivative (times h) from g[] / f* in lerp form
+    // (warp.py:79-85, :111-120)
+    __device__ __forceinline__ void a2(float& W, float& d0, float& d1, float& d2) const {
+        if constexpr (PACK) {
+            // the bottom / top z corner pairs as f32x2: one FFMA2 per pair of lerps
+            const float2 m1 = make_float2(-1.f, -1.f);
+            const float2 z0 = make_float2(g[0], g[4]), z1 = make_float2(g[1], g[5]);
+            const float2 z2 = make_float2(g[2], g[6]), z3 = make_float2(g[3], g[7]);
+            const float2 fx2 = make_float2(gfx, gfx), fy2 = make_float2(gfy, gfy);
+            const float2 e0 = __ffma2_rn(z0, m1, z1), e1 = __ffma2_rn(z2, m1, z3);
+            const float2 a0 = __ffma2_rn(fx2, e0, z0), a1v = __ffma2_rn(fx2, e1, z2);
+            const float2 dy = __ffma2_rn(a0, m1, a1v);
+            const float2 bb = __ffma2_rn(fy2, dy, a0);
+            const float2 ex = __ffma2_rn(fy2, __ffma2_rn(e0, m1, e1), e0);
+            const float dz = bb.y - bb.x;
+            W = fmaf(gfz, dz, bb.x);
+            d0 = fmaf(gfz, ex.y - ex.x, ex.x);
+            d1 = fmaf(gfz, dy.y - dy.x, dy.x);
+            d2 = dz;
+        } else {
+            const float e00 = g[1] - g[0], e10 = g[3] - g[2], e01 = g[5] - g[4], e11 = g[7] - g[6];
+            const float a00 = fmaf(gfx, e00, g[0]), a10 = fmaf(gfx, e10, g[2]);
+            const float a01 = fmaf(gfx, e01, g[4]), a11 = fmaf(gfx, e11, g[6]);
+            const float dy0 = a10 - a00, dy1 = a11 - a01;
+            const float b0 = fmaf(gfy, dy0, a00), b1 = fmaf(gfy, dy1, a01);
+            const float dz = b1 - b0;
+            W = fmaf(gfz, dz, b0);
+            const float ex0 = fmaf(gfy, e10 - e00, e00), ex1 = fmaf(gfy, e11 - e01, e01);
+            d0 = fmaf(gfz, ex1 - ex0, ex0);
+            d1 = fmaf(gfz, dy1 - dy0, dy0);
+            d2 = dz;
+        }
+    }
+
     // One plane step: (A) on p, (B) on p-1, (C) on p-2.  R = ring slot of plane p.  GEN: the
     // generic step (chunk edges, volume faces: every condition tested on the uniform plane
     // counter); otherwise a steady-state step whose events EV are known at compile time.
@@ -197,77 +279,16 @@ struct Lean {
         if (GEN && (p < pstart || p >= pend)) return;  // alignment padding of the loop
 
         // ------------------------------------------------------------- (A) plane p
-        float W = 0.f, d0 = 0.f, d1 = 0.f, d2 = 0.f;
-        if (!GEN || (p >= pa0 && p <= pa1)) {
-            if (GEN) {
-                const int zd = (int)(c.zw[p] & 0xffffu);
-                if (p == pa0) {
-                    load_yplane(zd, ylo);
-                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
-                } else if (c.zw[p - 1] & kAdv) {
-#pragma unroll
-                    for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
-                    load_yplane(min(zd + 1, a.ndz - 1), yhi);
-                }
-            } else if (EV & kEvA) {
-                const int zd = (int)(c.zw[p] & 0xffffu);
-#pragma unroll
-                for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
-                load_yplane(min(zd + 1, a.ndz - 1), yhi);
-            }
-            const float wz = c.w1[p], wz0 = __fsub_rn(1.0f, wz);
-            const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
-            const float yh1 = __fadd_rn(__fmul_rn(ylo[1], wz0), __fmul_rn(yhi[1], wz));
-            const float yh2 = __fadd_rn(__fmul_rn(ylo[2], wz0), __fmul_rn(yhi[2], wz));
-            bool in = fl & 8u;  // position inside the volume (x / y)
-            float fx_, fy_, fz_;
-            const int ix = cell(yh0, a.ox, a.ihx, a.nm1x, a.hix, in, fx_);
-            const int iy = cell(yh1, a.oy, a.ihy, a.nm1y, a.hiy, in, fy_);
-            const int iz = cell(yh2, a.oz, a.ihz, a.nm1z, a.hiz, in, fz_);
-            const unsigned nx = nx_(), nxy = nxy_();
-            const unsigned off = in ? (unsigned)iz * nxy + (unsigned)iy * nx + (unsigned)ix : a.fp.pad_off;
-            const float* b = a.Tv + off;
-            const float* by = b + nx;
-            const float* bz = b + nxy;
-            const float* byz = bz + nx;
-            const float c0 = __ldg(b), c1 = __ldg(b + 1), c2 = __ldg(by), c3 = __ldg(by + 1);
-            const float c4 = __ldg(bz), c5 = __ldg(bz + 1), c6 = __ldg(byz), c7 = __ldg(byz + 1);
-            // trilinear value and derivative (times h) in lerp form (warp.py:79-85, :111-120)
-            if constexpr (PACK) {
-                // the bottom / top z corner pairs as f32x2: one FFMA2 / FADD2 per pair of lerps
-                const float2 m1 = make_float2(-1.f, -1.f);
-                const float2 z0 = make_float2(c0, c4), z1 = make_float2(c1, c5);
-                const float2 z2 = make_float2(c2, c6), z3 = make_float2(c3, c7);
-                const float2 fx2 = make_float2(fx_, fx_), fy2 = make_float2(fy_, fy_);
-                const float2 e0 = __ffma2_rn(z0, m1, z1), e1 = __ffma2_rn(z2, m1, z3);  // (e00, e01), (e10, e11)
-                const float2 a0 = __ffma2_rn(fx2, e0, z0), a1 = __ffma2_rn(fx2, e1, z2);
-                const float2 dy = __ffma2_rn(a0, m1, a1);                                // (dy0, dy1)
-                const float2 bb = __ffma2_rn(fy2, dy, a0);                               // (b0, b1)
-                const float2 ex = __ffma2_rn(fy2, __ffma2_rn(e0, m1, e1), e0);           // (ex0, ex1)
-                const float dz = bb.y - bb.x;
-                W = fmaf(fz_, dz, bb.x);
-                d0 = fmaf(fz_, ex.y - ex.x, ex.x);
-                d1 = fmaf(fz_, dy.y - dy.x, dy.x);
-                d2 = dz;
-            } else {
-                const float e00 = c1 - c0, e10 = c3 - c2, e01 = c5 - c4, e11 = c7 - c6;
-                const float a00 = fmaf(fx_, e00, c0), a10 = fmaf(fx_, e10, c2);
-                const float a01 = fmaf(fx_, e01, c4), a11 = fmaf(fx_, e11, c6);
-                const float dy0 = a10 - a00, dy1 = a11 - a01;
-                const float b0 = fmaf(fy_, dy0, a00), b1 = fmaf(fy_, dy1, a01);
-                const float dz = b1 - b0;
-                W = fmaf(fz_, dz, b0);
-                const float ex0 = fmaf(fy_, e10 - e00, e00), ex1 = fmaf(fy_, e11 - e01, e01);
-                d0 = fmaf(fz_, ex1 - ex0, ex0);
-                d1 = fmaf(fz_, dy1 - dy0, dy0);
-                d2 = dz;
-            }
-        }
+        // PIPE: its gathers were issued by the previous step's (A1); else issue them now
+        if constexpr (!PIPE) a1<GEN, (EV & kEvA) != 0>(p);
+        float W, d0, d1, d2;
+        a2(W, d0, d1, d2);
         sm.W[R][P] = W;
         sm.dT[R][0][P] = d0;
         sm.dT[R][1][P] = d1;
         sm.dT[R][2][P] = d2;
         __syncthreads();
+        if constexpr (PIPE) a1<GEN, (EV & kEvA1) != 0>(p + 1);  // plane p+1's gathers in flight during (B), (C)
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
@@ -384,24 +405,24 @@ struct Lean {
             step<0, false, kEvA>(p);
             step<1, false, kEvF>(p + 1);
             step<2, false, kEvX>(p + 2);
-            step<3, false, kEvY>(p + 3);
+            step<3, false, kEvY | kEvA1>(p + 3);
         } else if constexpr (RATIO == 2) {
             step<0, false, kEvA | kEvX>(p);
-            step<1, false, kEvF | kEvY>(p + 1);
+            step<1, false, kEvF | kEvY | kEvA1>(p + 1);
             step<2, false, kEvA | kEvX>(p + 2);
-            step<3, false, kEvF | kEvY>(p + 3);
+            step<3, false, kEvF | kEvY | kEvA1>(p + 3);
         } else {
             generic4(p);
         }
     }
 };
 
-template <int RATIO, int K, int NXY, bool PACK = false>
+template <int RATIO, int K, int NXY, bool PACK = false, bool PIPE = false>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<RATIO, K, NXY, PACK> m(a, c, sm);
+    Lean<RATIO, K, NXY, PACK, PIPE> m(a, c, sm);
     constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -510,6 +531,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     m.pstart = m.z0 - 1;
     m.pend = m.z1 + 3;
     const int s0 = c.s0[tzc], s1 = c.s1[tzc];
+    if constexpr (PIPE) m.template a1<true, false>(m.pstart);  // the first plane's gathers
     for (int p = m.pstart - ((m.pstart - c.phase) & 3); p < m.pend; p += 4) {
         if (p >= s0 && p + 4 <= s1)
             m.block(p);
@@ -576,6 +598,10 @@ static cudaError_t set_smem_all(size_t smem) {
         e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess)
         e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 128, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     return e;
 }
 
@@ -583,10 +609,22 @@ static bool packed() {
     static const bool on = std::getenv("NGF_LEAN_PACK") && std::atoi(std::getenv("NGF_LEAN_PACK")) != 0;
     return on;
 }
+static bool piped() {
+    static const bool on = std::getenv("NGF_LEAN_PIPE") && std::atoi(std::getenv("NGF_LEAN_PIPE")) != 0;
+    return on;
+}
 
 template <int RATIO, int K>
 static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, size_t sb, cudaStream_t s) {
     const int n = a.nx == a.ny ? a.nx : 0;
+    if (piped() && n == 256) {
+        NGF_LAUNCH((k_march_lean<RATIO, K, 256, false, true>), grid, kNT, sb, s, a, c);
+        return;
+    }
+    if (piped() && n == 128) {
+        NGF_LAUNCH((k_march_lean<RATIO, K, 128, false, true>), grid, kNT, sb, s, a, c);
+        return;
+    }
     if (packed() && n == 256) {
         NGF_LAUNCH((k_march_lean<RATIO, K, 256, true>), grid, kNT, sb, s, a, c);
         return;
@@ -705,7 +743,7 @@ int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double
         // passes of steps s .. s+3 refer back to flushes after planes s-4 .. s-1) and its (B)
         // / (C) planes use central z rows; the steady range is the first run of valid groups
         auto valid = [&](int s) {
-            for (int p = s - 4; p < s + 4; ++p) {
+            for (int p = s - 4; p <= s + 4; ++p) {
                 const bool want = ((p - c->phase) % c->ratio + c->ratio) % c->ratio == 0;
                 if (adv(p - 1) != want) return false;
             }
