@@ -389,14 +389,19 @@ def run_ours(args):
     plan = ngf.build_gather_plan(gd, gi)
     T_dev = torch.from_numpy(T.values).cuda()
     R_dev = torch.from_numpy(R.values).cuda()
-    obj = ngf.LevelObjective.from_device(T_dev, R_dev, plan, ngf.NgfParams(10.0, 10.0), 1.0)
-    level = obj.level
     zlo, zhi = 0, gi.dims[2]
-    evaluator = obj
     if strong:
+        # this rank's slab level: reference terms on its own planes only (R is replicated)
         from paper_1812_06765_b200.distributed import DeviceSlab, SlabObjective, slab_ranges
         zlo, zhi = slab_ranges(gi.dims[2], gd.dims[2], ws)[rank]
-        evaluator = SlabObjective(DeviceSlab(level, zlo, zhi))
+        slab = DeviceSlab.create(gi, gd, T_dev, R_dev, ngf.NgfParams(10.0, 10.0), 1.0, zlo, zhi)
+        evaluator = SlabObjective(slab)
+        level = slab.level
+        obj = None
+    else:
+        obj = ngf.LevelObjective.from_device(T_dev, R_dev, plan, ngf.NgfParams(10.0, 10.0), 1.0)
+        level = obj.level
+        evaluator = obj
     x = torch.from_numpy(y.ravel().copy()).cuda()
     g = torch.empty_like(x)
     sc = torch.zeros(3, dtype=torch.float64, device="cuda")

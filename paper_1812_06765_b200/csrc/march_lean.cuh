@@ -13,7 +13,7 @@ namespace lean {
 // ring-column warp owns columns x0-1 and x0+32 of all TYI+2 rows (16 + 16 lanes), so
 // every lane of every warp holds a position and the tile is exactly 32 wide in x.
 #ifndef NGF_LEAN_TYI
-#define NGF_LEAN_TYI 13
+#define NGF_LEAN_TYI 14
 #endif
 constexpr int kTYI = NGF_LEAN_TYI;
 constexpr int kE1X = 34, kE1Y = kTYI + 2;
