@@ -143,6 +143,12 @@ int ngf_level_eval(ngf_level_t* level, const void* y, void* grad, double* scalar
  * that hold numpy / host memory. */
 int ngf_level_eval_host(ngf_level_t* level, const void* y_host, void* grad_host,
                         double* scalars_host, int mode, void* stream);
+/* Pipelining of ngf_level_eval_host (mode 0, lean march, both host arrays page-locked):
+ * the level's z chunks run as `parts` groups on their own streams, each group starting
+ * once its deformation planes are uploaded, and the planes a group finalises go down
+ * while later groups march.  Results are bit-identical to the serial call.  parts 0 =
+ * the default (4, or NGF_PIPE_PARTS), 1 = serial, at most 8. */
+int ngf_level_set_host_pipeline(ngf_level_t* level, int parts);
 /* Host <-> device copies staged through page-locked memory by the library's copy threads
  * (a pageable cudaMemcpy runs at a fraction of the PCIe bandwidth).  ngf_host_upload is
  * stream-ordered; a pageable src_host may be reused when it returns, a page-locked one is

@@ -78,6 +78,7 @@ _PROTOS = {
     "ngf_level_kernel_ms": (_i, [_vp, ctypes.POINTER(ctypes.c_float)]),
     "ngf_level_info": (_i, [_vp, ctypes.POINTER(ctypes.c_int64)]),
     "ngf_level_variant": (_i, [_vp]),
+    "ngf_level_set_host_pipeline": (_i, [_vp, _i]),
     "ngf_level_set_zrange": (_i, [_vp, _i64, _i64]),
     "ngf_level_add_curvature": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "ngf_vec_dot": (_i, [_i, _vp, _vp, _i64, _vp, _vp]),

@@ -15,7 +15,9 @@ namespace ngf {
 // One kernel after the march: grad = grad D (fixed-order sum of the covering tiles'
 // partials) + alpha * vol * L^T L u (curvature.py:74-81), the per-block partial sums of
 // (L u)^2, and -- in the last block to finish -- the fixed-order totals J, D, S.
-// Grid: x/y tiles of 32 x 8 deformation nodes, blockIdx.z = comp * nchunk + z chunk.
+// Grid: x/y tiles of 32 x 8 deformation nodes, blockIdx.z = comp * (chunks of the launch)
+// + z chunk - pc0; a launch may cover a range of the chunks (pipelined host evaluation), the
+// block index and the finished-block count are over all of them.
 template <typename T>
 struct PostArgs {
     GridK<T> g;
@@ -33,6 +35,8 @@ struct PostArgs {
     double* out;
     int mode;          // 0 full, 1 slab partial, 2 add curvature (see post_finalize)
     int nchunk;        // z chunks of kPostKZ planes per component
+    int pc0;           // first z chunk of this launch (grid z = 3 x its chunk count)
+    int count;         // blocks counted for the totals: all post blocks of the evaluation
     T ihx2, ihy2, ihz2;  // 1 / h^2 in the working dtype (curvature.py:28-29)
 };
 
@@ -109,7 +113,6 @@ __device__ __forceinline__ T d2t_at(T lm, T l0, T lp, int i, int n, T ih2) {
 // kernel waits for the fused march (programmatic dependent launch, so this part overlaps
 // the march's last wave); then the covering tiles' partials of all KZ planes are loaded
 // together and summed in a fixed order.
-constexpr int kPostKZ = 4;
 constexpr int kPostUX = 36, kPostUY = 12, kPostLX = 34, kPostLY = 10;
 
 template <typename T>
@@ -145,9 +148,10 @@ __global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArg
     const GridK<T>& g = p.g;
     const FusedPlan& fp = p.fp;
     const int tid = threadIdx.y * 32 + threadIdx.x;
-    const int nblk = gridDim.x * gridDim.y * gridDim.z;
-    const int bid = (blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
-    const int comp = blockIdx.z / p.nchunk, chunk = blockIdx.z - comp * p.nchunk;
+    const int nblk = gridDim.x * gridDim.y * 3 * p.nchunk;  // (L u)^2 partials of all launches
+    const int pcn = gridDim.z / 3;
+    const int comp = blockIdx.z / pcn, chunk = p.pc0 + (blockIdx.z - comp * pcn);
+    const int bid = ((comp * p.nchunk + chunk) * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
     const int x0 = blockIdx.x * 32, y0 = blockIdx.y * 8;
     const int k0 = chunk * KZ;
     const int i = x0 + threadIdx.x, j = y0 + threadIdx.y;
@@ -362,7 +366,7 @@ __global__ void __launch_bounds__(256, 3) k_post(const __grid_constant__ PostArg
     // last block done: fixed-order totals
     if (tid == 0) {
         __threadfence();
-        last = atomicAdd(p.flag + 1, 1) == nblk - 1;
+        last = atomicAdd(p.flag + 1, 1) == p.count - 1;
     }
     __syncthreads();
     if (last) {
@@ -454,21 +458,9 @@ void launch_variant<double>(const FusedArgs<double>& a, cudaStream_t s) {
 }
 
 template <typename T>
-int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns,
-                      int* flag, T* grad, double* scalars, cudaStream_t s, cudaEvent_t ev0,
-                      cudaEvent_t ev1, int part) {
-    // part 0: full evaluation; 1: NGF partial of the level's z-slab (grad <- grad D_slab,
-    // scalars <- D_slab); 2: add curvature to an all-reduced (grad D, D) in place
-    const int nchunk = (int)((dg.dims[2] + kPostKZ - 1) / kPostKZ);
-    const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * nchunk);
-    const int nsb = (int)(cgrid.x * cgrid.y * cgrid.z);
-    if (nsb > ns) return NGF_EARG;
+static PostArgs<T> post_args(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int* flag,
+                             T* grad, double* scalars, int part, int nchunk) {
     const double vol = dg.spacing[0] * dg.spacing[1] * dg.spacing[2];
-    if (part != 2) {
-        if (ev0) cudaEventRecord(ev0, s);
-        launch_variant<T>(a, s);
-        if (ev1) cudaEventRecord(ev1, s);
-    }
     PostArgs<T> p;
     p.g = make_gridk<T>(dg);
     p.fp = a.fp;
@@ -488,9 +480,32 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
     p.out = scalars;
     p.mode = part;
     p.nchunk = nchunk;
+    p.pc0 = 0;
+    p.count = (int)(((dg.dims[0] + 31) / 32) * ((dg.dims[1] + 7) / 8)) * 3 * nchunk;
     p.ihx2 = (T)1 / (p.g.hx * p.g.hx);
     p.ihy2 = (T)1 / (p.g.hy * p.g.hy);
     p.ihz2 = (T)1 / (p.g.hz * p.g.hz);
+    return p;
+}
+
+static int post_chunks(const ngf_grid_t& dg) { return (int)((dg.dims[2] + kPostKZ - 1) / kPostKZ); }
+
+template <typename T>
+int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns,
+                      int* flag, T* grad, double* scalars, cudaStream_t s, cudaEvent_t ev0,
+                      cudaEvent_t ev1, int part) {
+    // part 0: full evaluation; 1: NGF partial of the level's z-slab (grad <- grad D_slab,
+    // scalars <- D_slab); 2: add curvature to an all-reduced (grad D, D) in place
+    const int nchunk = post_chunks(dg);
+    const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * nchunk);
+    const int nsb = (int)(cgrid.x * cgrid.y * cgrid.z);
+    if (nsb > ns) return NGF_EARG;
+    if (part != 2) {
+        if (ev0) cudaEventRecord(ev0, s);
+        launch_variant<T>(a, s);
+        if (ev1) cudaEventRecord(ev1, s);
+    }
+    const PostArgs<T> p = post_args<T>(a, dg, alpha, spart, flag, grad, scalars, part, nchunk);
     // programmatic dependent launch edges inside conditional graph bodies are opt-in
     // (NGF_GRAPH_PDL=1); a captured evaluation launches k_post plainly by default
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
@@ -517,6 +532,22 @@ int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha,
     NGF_CHECK_LAUNCH();
     return 0;
 }
+
+template <typename T>
+int fused_post_range(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns, int* flag,
+                     T* grad, double* scalars, cudaStream_t s, int pc0, int pc1) {
+    const int nchunk = post_chunks(dg);
+    if (pc0 < 0 || pc1 > nchunk || pc0 >= pc1) return NGF_EARG;
+    const dim3 cgrid((dg.dims[0] + 31) / 32, (dg.dims[1] + 7) / 8, 3 * (pc1 - pc0));
+    if ((int)(cgrid.x * cgrid.y) * 3 * nchunk > ns) return NGF_EARG;
+    PostArgs<T> p = post_args<T>(a, dg, alpha, spart, flag, grad, scalars, 0, nchunk);
+    p.pc0 = pc0;
+    NGF_LAUNCH(k_post<T>, cgrid, dim3(32, 8), 0, s, p);
+    NGF_CHECK_LAUNCH();
+    return 0;
+}
+
+void fused_march_launch(const FusedArgs<float>& a, cudaStream_t s) { launch_variant<float>(a, s); }
 
 // packed reference terms (gR / nR, 1 / nR) from the exact ones
 template <typename T>
@@ -550,6 +581,8 @@ template int fused_eval_launch<float>(const FusedArgs<float>&, const ngf_grid_t&
 template int fused_eval_launch<double>(const FusedArgs<double>&, const ngf_grid_t&, double, double*,
                                        int, int*, double*, double*, cudaStream_t, cudaEvent_t,
                                        cudaEvent_t, int);
+template int fused_post_range<float>(const FusedArgs<float>&, const ngf_grid_t&, double, double*, int, int*,
+                                     float*, double*, cudaStream_t, int, int);
 template size_t fused_smem<float>(int, int, int);
 template size_t fused_smem<double>(int, int, int);
 template int pack_rt<float>(const float*, const float*, int64_t, void*, cudaStream_t, int64_t, int64_t);

@@ -63,6 +63,7 @@ struct FusedArgs {
     T tau2, taurho, neg_hbar;
     double half_hbar;
     FusedPlan fp;
+    int chunk0, nchunks;  // lean march: z chunks [chunk0, chunk0 + nchunks) (nchunks 0: all)
 };
 
 __device__ __forceinline__ float lerp_exact(float a0, float a1, float w) {
@@ -140,6 +141,14 @@ template <typename T>
 int fused_eval_launch(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns,
                       int* flag, T* grad, double* scalars, cudaStream_t s, cudaEvent_t ev0 = nullptr,
                       cudaEvent_t ev1 = nullptr, int part = 0);
+// the post-march kernel alone over post chunks [pc0, pc1) of kPostKZ deformation planes
+// (the pipelined host evaluation; no programmatic dependent launch).  The block counter
+// spans all post launches of the evaluation: the last block to finish forms J, D, S.
+template <typename T>
+int fused_post_range(const FusedArgs<T>& a, const ngf_grid_t& dg, double alpha, double* spart, int ns, int* flag,
+                     T* grad, double* scalars, cudaStream_t s, int pc0, int pc1);
+void fused_march_launch(const FusedArgs<float>& a, cudaStream_t s);
+constexpr int kPostKZ = 4;  // deformation planes per k_post block
 template <typename T> int fused_prepare(int variant, size_t smem);
 template <typename T> size_t fused_smem(int variant, int wx, int wy);
 void fused_variant_geom(int variant, int* ty, int* nthreads);

@@ -32,6 +32,17 @@ struct LevelWork {
     double* dws = nullptr;  // 8
 };
 
+// ngf_level_eval_host's pipelined form (lean march, page-locked host buffers): the z chunks
+// are split into parts, each with its own stream; part i's march starts once its y planes
+// are up, its post kernel finalises the deformation planes no later chunk touches and their
+// gradient goes down while the later parts march.
+constexpr int kPipeMax = 8;
+struct PipeState {
+    cudaStream_t st[kPipeMax] = {};
+    cudaStream_t up = nullptr, down = nullptr;
+    cudaEvent_t start = nullptr, fin = nullptr, evH[kPipeMax] = {}, evM[kPipeMax] = {}, evP[kPipeMax] = {};
+};
+
 }  // namespace ngf
 
 struct ngf_level {
@@ -64,6 +75,8 @@ struct ngf_level {
     double* hsc;
     double* hsc_pin;
     cudaEvent_t done;  // completion of the last launch: destroy waits for it, not the device
+    ngf::PipeState* pipe;  // ngf_level_eval_host's streams and events (created on first use)
+    int pipe_req;          // parts of the pipelined host evaluation (0: default, 1: serial)
 };
 
 namespace ngf {
@@ -747,6 +760,20 @@ void ngf_level_destroy(ngf_level_t* L) {
                     L->ex.cws, L->ex.dws, L->hx, L->hg, L->hsc};
     for (void* b : bufs) dev_free(b);
     if (L->hsc_pin) cudaFreeHost(L->hsc_pin);
+    if (L->pipe) {
+        PipeState& ps = *L->pipe;
+        for (int i = 0; i < kPipeMax; ++i) {
+            if (ps.st[i]) cudaStreamDestroy(ps.st[i]);
+            if (ps.evH[i]) cudaEventDestroy(ps.evH[i]);
+            if (ps.evP[i]) cudaEventDestroy(ps.evP[i]);
+            if (ps.evM[i]) cudaEventDestroy(ps.evM[i]);
+        }
+        if (ps.up) cudaStreamDestroy(ps.up);
+        if (ps.down) cudaStreamDestroy(ps.down);
+        if (ps.start) cudaEventDestroy(ps.start);
+        if (ps.fin) cudaEventDestroy(ps.fin);
+        delete L->pipe;
+    }
     delete L->ctl;
     for (int k = 0; k < 2; ++k)
         if (L->ev[k]) cudaEventDestroy(L->ev[k]);
@@ -772,6 +799,180 @@ int ngf_level_eval(ngf_level_t* L, const void* y, void* grad, double* scalars_de
     return rc;
 }
 
+}  // extern "C"
+
+namespace ngf {
+
+static int pipe_parts() {
+    static const int n = [] {
+        const char* e = std::getenv("NGF_PIPE_PARTS");
+        return e ? std::max(0, std::min(kPipeMax, std::atoi(e))) : 4;
+    }();
+    return n;
+}
+
+static int pipe_init(ngf_level* L) {
+    if (L->pipe) return 0;
+    PipeState* ps = new PipeState();
+    L->pipe = ps;
+    int lo = 0, hi = 0;  // numerically: lo = least, hi = greatest priority
+    NGF_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    for (int i = 0; i < kPipeMax; ++i) {
+        // earlier parts first: their CTAs are dispatched ahead of a later part's
+        const int pr = std::min(lo, hi + i);
+        NGF_CUDA(cudaStreamCreateWithPriority(&ps->st[i], cudaStreamNonBlocking, pr));
+        NGF_CUDA(cudaEventCreateWithFlags(&ps->evH[i], cudaEventDisableTiming));
+        NGF_CUDA(cudaEventCreateWithFlags(&ps->evP[i], cudaEventDisableTiming));
+        NGF_CUDA(cudaEventCreateWithFlags(&ps->evM[i], cudaEventDisableTiming));
+    }
+    NGF_CUDA(cudaStreamCreateWithPriority(&ps->up, cudaStreamNonBlocking, hi));
+    NGF_CUDA(cudaStreamCreateWithPriority(&ps->down, cudaStreamNonBlocking, hi));
+    NGF_CUDA(cudaEventCreateWithFlags(&ps->start, cudaEventDisableTiming));
+    NGF_CUDA(cudaEventCreateWithFlags(&ps->fin, cudaEventDisableTiming));
+    return 0;
+}
+
+// deformation planes [a, b) of the three components between the (3, ndz, ndy, ndx) host and
+// device arrays: one strided copy
+static cudaError_t copy_planes(void* dst, const void* src, int64_t a, int64_t b, int64_t plane, int64_t m,
+                               cudaMemcpyKind kind, cudaStream_t s) {
+    if (b <= a) return cudaSuccess;
+    const size_t es = sizeof(float), o = (size_t)(a * plane) * es;
+    return cudaMemcpy2DAsync((char*)dst + o, (size_t)m * es, (const char*)src + o, (size_t)m * es,
+                             (size_t)((b - a) * plane) * es, 3, kind, s);
+}
+
+// Returns kNotPiped when the level does not take the pipelined path (the caller runs the
+// serial one); else 0 or an error.
+constexpr int kNotPiped = -1000;
+static int eval_host_pipelined(ngf_level* L, const void* y_host, void* grad_host, double* scalars_host,
+                               cudaStream_t s) {
+    if (L->dtype != NGF_F32 || L->fp.variant != kLeanVariant || !L->ctl || L->slab_terms || L->timing)
+        return kNotPiped;
+    const lean::Ctl& c = *L->ctl;
+    const int nc = c.nchunk;
+    const int P = std::min(L->pipe_req > 0 ? L->pipe_req : pipe_parts(), nc);
+    if (P < 2 || !host_is_pinned(y_host) || !host_is_pinned(grad_host)) return kNotPiped;
+    if (int rc = pipe_init(L)) return rc;
+    PipeState& ps = *L->pipe;
+    // The totals go straight into the page-locked scalars (mapped); the gradient planes of
+    // the last part too (its post kernel's stores cross PCIe, no copy after it), the other
+    // parts' planes by copies as they complete.  NGF_PIPE_MAPPED: 0 copies only, 1 every
+    // part mapped, 2 (default) the last part mapped.
+    static const int map_mode = std::getenv("NGF_PIPE_MAPPED") ? std::atoi(std::getenv("NGF_PIPE_MAPPED")) : 2;
+    const bool mapped_ok = map_mode != 0;
+    void* g_map = nullptr;
+    void* sc_map = nullptr;
+    if (mapped_ok && (cudaHostGetDevicePointer(&g_map, grad_host, 0) != cudaSuccess ||
+                      cudaHostGetDevicePointer(&sc_map, L->hsc_pin, 0) != cudaSuccess)) {
+        cudaGetLastError();
+        g_map = sc_map = nullptr;
+    }
+    const bool mapped = g_map && sc_map;
+    const int64_t ndz = L->def.dims[2], plane = L->def.dims[0] * L->def.dims[1], m = plane * ndz;
+    const int npc = (int)((ndz + kPostKZ - 1) / kPostKZ);
+    const int wz = L->fp.wz;
+    // parts: chunks [gb[i], gb[i+1]); deformation planes final after part i: those below the
+    // next part's lowest window plane (post chunks [pc[i], pc[i+1])); y planes part i needs:
+    // its chunks' windows and the post kernel's +-2 plane neighbourhood ([0, yz[i+1]))
+    int gb[kPipeMax + 1], pc[kPipeMax + 1], yz[kPipeMax + 1];
+    for (int i = 0; i <= P; ++i) gb[i] = (int)((int64_t)nc * i / P);
+    pc[0] = 0;
+    yz[0] = 0;
+    for (int i = 0; i < P; ++i) {
+        const bool last = i == P - 1;
+        pc[i + 1] = last ? npc : std::max(pc[i], c.wzlo[gb[i + 1]] / kPostKZ);
+        const int64_t need = std::max<int64_t>(c.wzlo[gb[i + 1] - 1] + wz, (int64_t)kPostKZ * pc[i + 1] + 2);
+        yz[i + 1] = last ? (int)ndz : (int)std::max<int64_t>(yz[i], std::min<int64_t>(ndz, need));
+    }
+    static const bool trace = std::getenv("NGF_PIPE_TRACE") != nullptr;
+    cudaEvent_t tev[4 * kPipeMax + 2] = {};
+    int ntev = 0;
+    auto mark = [&](cudaStream_t st) {
+        if (!trace) return;
+        cudaEventCreate(&tev[ntev]);
+        cudaEventRecord(tev[ntev++], st);
+    };
+    mark(s);
+    NGF_CUDA(cudaEventRecord(ps.start, s));
+    NGF_CUDA(cudaStreamWaitEvent(ps.up, ps.start, 0));
+    NGF_CUDA(cudaStreamWaitEvent(ps.down, ps.start, 0));
+    for (int i = 0; i < P; ++i) {
+        NGF_CUDA(cudaStreamWaitEvent(ps.st[i], ps.start, 0));
+        NGF_CUDA(copy_planes(L->hx, y_host, yz[i], yz[i + 1], plane, m, cudaMemcpyHostToDevice, ps.up));
+        NGF_CUDA(cudaEventRecord(ps.evH[i], ps.up));
+        mark(ps.up);
+    }
+    FusedArgs<float> a = fused_args<float>(L, L->hx);
+    double* sout = mapped ? (double*)sc_map : L->hsc;
+    for (int i = 0; i < P; ++i) {
+        cudaStream_t si = ps.st[i];
+        NGF_CUDA(cudaStreamWaitEvent(si, ps.evH[i], 0));
+        a.chunk0 = gb[i];
+        a.nchunks = gb[i + 1] - gb[i];
+        fused_march_launch(a, si);
+        NGF_CHECK_LAUNCH();
+        mark(si);
+        NGF_CUDA(cudaEventRecord(ps.evM[i], si));
+        // part i's post kernel also needs the earlier parts' marches (windows overlap across
+        // a part boundary; parts may finish out of order).  The totals are formed by the
+        // last post block to finish over all parts: every post block counts, and each runs
+        // after the marches its part waited for, so the last one runs after all of them.
+        for (int j = 0; j < i; ++j) NGF_CUDA(cudaStreamWaitEvent(si, ps.evM[j], 0));
+        const bool gmap = mapped && (map_mode == 1 || i == P - 1);
+        float* gout = gmap ? (float*)g_map : (float*)L->hg;
+        if (pc[i + 1] > pc[i])
+            if (int rc = fused_post_range<float>(a, L->def, L->alpha, L->spart, L->ns, L->flag, gout, sout, si, pc[i],
+                                                 pc[i + 1]))
+                return rc;
+        NGF_CUDA(cudaEventRecord(ps.evP[i], si));
+        mark(si);
+        if (!gmap) {
+            NGF_CUDA(cudaStreamWaitEvent(ps.down, ps.evP[i], 0));
+            NGF_CUDA(copy_planes(grad_host, L->hg, (int64_t)kPostKZ * pc[i],
+                                 std::min<int64_t>(ndz, (int64_t)kPostKZ * pc[i + 1]), plane, m,
+                                 cudaMemcpyDeviceToHost, ps.down));
+        }
+    }
+    if (!mapped) {
+        for (int i = 0; i < P; ++i) NGF_CUDA(cudaStreamWaitEvent(ps.down, ps.evP[i], 0));
+        NGF_CUDA(cudaMemcpyAsync(L->hsc_pin, L->hsc, 3 * sizeof(double), cudaMemcpyDeviceToHost, ps.down));
+        NGF_CUDA(cudaEventRecord(ps.fin, ps.down));
+        NGF_CUDA(cudaStreamWaitEvent(s, ps.fin, 0));
+    } else {
+        for (int i = 0; i < P; ++i) NGF_CUDA(cudaStreamWaitEvent(s, ps.evP[i], 0));
+        NGF_CUDA(cudaEventRecord(ps.fin, ps.down));  // the copied planes
+        NGF_CUDA(cudaStreamWaitEvent(s, ps.fin, 0));
+    }
+    mark(s);
+    NGF_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(scalars_host, L->hsc_pin, 3 * sizeof(double));
+    if (trace) {
+        // per part: H2D done (all parts first), then march end, post end; then the join
+        // (microseconds after start)
+        std::fprintf(stderr, "pipe P=%d mapped=%d chunks", P, (int)mapped);
+        for (int i = 0; i <= P; ++i) std::fprintf(stderr, " %d", gb[i]);
+        std::fprintf(stderr, " | y planes");
+        for (int i = 0; i <= P; ++i) std::fprintf(stderr, " %d", yz[i]);
+        std::fprintf(stderr, " | post chunks");
+        for (int i = 0; i <= P; ++i) std::fprintf(stderr, " %d", pc[i]);
+        std::fprintf(stderr, "\n  h2d:");
+        for (int k = 1; k < ntev; ++k) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, tev[0], tev[k]);
+            if (k == P + 1) std::fprintf(stderr, "\n  march/post:");
+            std::fprintf(stderr, " %.1f", ms * 1e3f);
+        }
+        std::fprintf(stderr, "\n");
+        for (int k = 0; k < ntev; ++k) cudaEventDestroy(tev[k]);
+    }
+    return 0;
+}
+
+}  // namespace ngf
+
+extern "C" {
+
 int ngf_level_eval_host(ngf_level_t* L, const void* y_host, void* grad_host, double* scalars_host,
                         int mode, void* stream) {
     if (!L || !y_host || !grad_host || !scalars_host || (mode != 0 && mode != 1)) return NGF_EARG;
@@ -782,6 +983,13 @@ int ngf_level_eval_host(ngf_level_t* L, const void* y_host, void* grad_host, dou
         if (dev_alloc(&L->hx, vb) || dev_alloc(&L->hg, vb) || dev_alloc((void**)&L->hsc, 4 * sizeof(double)))
             return NGF_ENOMEM;
         NGF_CUDA(cudaHostAlloc((void**)&L->hsc_pin, 4 * sizeof(double), cudaHostAllocDefault));
+    }
+    if (mode == 0) {
+        const int rc = eval_host_pipelined(L, y_host, grad_host, scalars_host, s);
+        if (rc != kNotPiped) {
+            record_done(L->done, s);
+            return rc;
+        }
     }
     if (int rc = host_upload(L->hx, y_host, vb, s)) return rc;
     if (int rc = ngf_level_eval(L, L->hx, L->hg, L->hsc, mode, stream)) return rc;
@@ -798,6 +1006,12 @@ int ngf_level_add_curvature(ngf_level_t* L, const void* y, void* grad, double* s
     const int rc = fused_part(L, y, grad, scalars_dev, as_stream(stream), 2);
     record_done(L->done, as_stream(stream));
     return rc;
+}
+
+int ngf_level_set_host_pipeline(ngf_level_t* L, int parts) {
+    if (!L || parts < 0 || parts > kPipeMax) return NGF_EARG;
+    L->pipe_req = parts;
+    return 0;
 }
 
 int ngf_level_set_zrange(ngf_level_t* L, int64_t zlo, int64_t zhi) {

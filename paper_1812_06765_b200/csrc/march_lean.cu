@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
     // ---- CTA geometry (uniform): grid (x tiles, y tiles, z chunks), dispatched chunk-major
-    const int tx = blockIdx.x, ty = blockIdx.y, tzc = blockIdx.z;
+    const int tx = blockIdx.x, ty = blockIdx.y, tzc = blockIdx.z + a.chunk0;
     m.cta = (tzc * fp.nty + ty) * fp.ntx + tx;
     const int x0 = tx * 32, y0 = ty * kTYI;
     m.z0 = c.zb[tzc];
@@ -662,7 +662,7 @@ int lean_prepare(size_t smem) {
 
 void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) {
     const FusedPlan& fp = a.fp;
-    const dim3 grid(fp.ntx, fp.nty, fp.ntz);
+    const dim3 grid(fp.ntx, fp.nty, a.nchunks ? a.nchunks : fp.ntz);
     const int k = (fp.kx <= 4 && fp.ky <= 4) ? 4 : 8;
     if (c.ratio == 4 && k == 8)
         lean::launch_sized<4, 8>(a, c, grid, fp.smem_bytes, s);

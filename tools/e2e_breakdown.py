@@ -12,7 +12,7 @@ import bench  # noqa: E402
 import paper_1812_06765_b200 as ngf  # noqa: E402
 from paper_1812_06765_b200._lib import lib  # noqa: E402
 
-R, T, gd, y = bench.make_inputs(256, 4, seed=0)
+R, T, gd, y, _ = bench.make_inputs(256, 4, seed=0)
 obj = ngf.LevelObjective.from_device(torch.from_numpy(T.values).cuda(), torch.from_numpy(R.values).cuda(),
                                      ngf.build_gather_plan(gd, R.grid), ngf.NgfParams(10.0, 10.0), 1.0)
 xh = y.ravel().copy()

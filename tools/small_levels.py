@@ -23,7 +23,7 @@ a = ap.parse_args()
 reps = 1 if a.once else 200
 s = torch.cuda.current_stream()
 for n in (32, 64, 128, 256):
-    R, T, gd, y = bench.make_inputs(n, 4, seed=0)
+    R, T, gd, y, _ = bench.make_inputs(n, 4, seed=0)
     obj = ngf.LevelObjective.from_device(torch.from_numpy(T.values).cuda(), torch.from_numpy(R.values).cuda(),
                                          ngf.build_gather_plan(gd, R.grid), ngf.NgfParams(10.0, 10.0), 1.0)
     x = torch.from_numpy(y.ravel().copy()).cuda()
