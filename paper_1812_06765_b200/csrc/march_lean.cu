@@ -40,6 +40,9 @@ namespace lean {
 constexpr int kPlane = kE1Y * kE1X;  // positions, row stride 34 for every per-position plane
 constexpr int kSink = kPlane;        // the position of ring-column lanes beyond 2 * kE1Y
 constexpr int kPl = kPlane + kE1X + 2;  // per-position plane incl. the sink and its neighbours
+constexpr int kFbPitch = kE1X + 1;   // Fb row pitch: 3 row + 16 column offset banks apart
+constexpr int kWXP = kWXM + 1;       // Xr row pitch (odd)
+static_assert(kE1Y * kFbPitch + 2 <= kPl, "Fb rows fit the per-position plane");
 constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4, aligned with the
                                      // deformation cells at grid ratio 2 and 4 (steady blocks)
 
@@ -51,9 +54,10 @@ struct Smem {
     float dT[kRing][3][kPl];              // interpolant derivative (times h), same ring
     float Qx[2][kPl + 2];                 // q_x at [P + 1] (ring columns, q = 0, pad the rows), by plane parity
     float Qy[2][kPl + 2 * kE1X];          // q_y at [P + 34]: one zero row each side
-    float Fb[3][kPl];                     // completed deformation plane (z-reduced ghat / h)
-    float Xr[3][kE1Y][kWXM];           // x-reduced
-    int2 xl[kWXM][kKMax];              // x pass: (E1 column, weight bits) per window output
+    float Fb[3][kPl];                     // completed deformation plane (z-reduced ghat / h), rows
+                                          // of kFbPitch (bank-conflict-free x pass)
+    float Xr[3][kE1Y][kWXP];           // x-reduced (odd pitch)
+    int2 xl[kKMax][kWXM];              // x pass: (E1 column, weight bits) per entry, window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
     float colG[kE1X][3], colGt[kE1X][3], rowG[kE1Y][3], rowGt[kE1Y][3];
     int colP0[kE1X], colP1[kE1X], rowP0[kE1Y], rowP1[kE1Y];
@@ -137,10 +141,10 @@ struct Lean {
         const int xr_r = f & 0xff, xr_d = (f >> 8) & 0xff;
         if (xr_r != 0xff) {
             float s0 = 0.f, s1 = 0.f, s2 = 0.f;
-            const float* fb = &sm.Fb[0][0] + xr_r * kE1X;
+            const float* fb = &sm.Fb[0][0] + xr_r * kFbPitch;
 #pragma unroll
             for (int k = 0; k < KX; ++k) {
-                const int2 e = sm.xl[xr_d][k];
+                const int2 e = sm.xl[k][xr_d];
                 const float w = __int_as_float(e.y);
                 s0 = fmaf(w, fb[e.x], s0);
                 s1 = fmaf(w, fb[kPl + e.x], s1);
@@ -176,9 +180,10 @@ struct Lean {
     }
 
     __device__ __forceinline__ void put_flush(const float (&acc)[3]) {
-        sm.Fb[0][P] = acc[0];
-        sm.Fb[1][P] = acc[1];
-        sm.Fb[2][P] = acc[2];
+        const int f = P + P / kE1X;  // row pitch kFbPitch (the sink lands past the last row)
+        sm.Fb[0][f] = acc[0];
+        sm.Fb[1][f] = acc[1];
+        sm.Fb[2][f] = acc[2];
     }
 
     __device__ __forceinline__ bool flushes(int j) const {
@@ -500,13 +505,24 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     {
         const int2* gx = reinterpret_cast<const int2*>(fp.lx) + (size_t)tx * fp.wx * KX;
         const int2* gy = reinterpret_cast<const int2*>(fp.ly) + (size_t)ty * fp.wy * KY;
-        for (int t = tid; t < fp.wx * KX; t += kNT) sm.xl[t / KX][t % KX] = gx[t];
+        for (int t = tid; t < fp.wx * KX; t += kNT) sm.xl[t % KX][t / KX] = gx[t];
         for (int t = tid; t < fp.wy * KY; t += kNT) sm.yl[t / KY][t % KY] = gy[t];
-        // flush pass assignment: x pass (row, window column), y pass (window row, column)
+        // flush pass assignment: x pass (row, window column), y pass (window row, column).
+        // x pass: half-warps hold the 16 rows of one window column, the two halves of a
+        // warp columns d and d + o whose image columns lie 16 banks apart (o = 16 / ratio):
+        // with the Fb row pitch of 35 the reads of a warp are conflict-free and its entry
+        // list reads are two broadcasts
+        static_assert(kE1Y == 16, "x pass: a half-warp per window column");
         unsigned xa = 0xffffu, ya = 0xffffu;
-        if (tid < kE1Y * fp.wx) {
-            const int r = tid / fp.wx;
-            xa = (unsigned)r | (unsigned)(tid - r * fp.wx) << 8;
+        {
+            constexpr int o = RATIO == 2 ? 8 : 4;
+            const int idx = 2 * warp + (lane >> 4);  // window column slot
+            int d = idx;
+            if ((idx / (2 * o) + 1) * (2 * o) <= fp.wx) {
+                const int j = idx % (2 * o);
+                d = (idx - j) + (j >> 1) + (j & 1) * o;
+            }
+            if (d < fp.wx) xa = (unsigned)(lane & 15) | (unsigned)d << 8;
         }
         if (tid < fp.wy * fp.wx) {
             const int r = tid / fp.wx;
