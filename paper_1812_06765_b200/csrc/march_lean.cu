@@ -8,13 +8,16 @@
 //       on plane p-1;
 //   (C) G^T q (warp.py:159-184) times the derivative on plane p-2, accumulated along z
 //       into the two deformation planes it interpolates (transfer.py:151-192, z first);
-// -- re-laid out so that a step costs about half the instructions of the classic march:
+// -- re-laid out so that a step costs about 0.7 of the classic march's instructions:
 //   * one position per thread (no slot loops or per-slot flag decoding): 14 row warps,
-//     2 ring-row warps and 1 ring-column warp cover the 34 x 16 tile + ring exactly, and
-//     the tile is 32 wide in x, so a 256-wide level is 8 tiles with no padding;
-//   * ONE __syncthreads per plane: W, q_x and q_y live in triple-buffered shared planes
-//     (a warp may run one step ahead of the slowest one without overwriting what it
-//     reads); the z neighbours of W and q and the derivative ring stay in registers;
+//     2 ring-row warps and 1 ring-column warp cover the 34 x 16 tile + ring, and the tile
+//     is 32 wide in x, so a 256-wide level is 8 tiles with no padding; 544 threads at 56
+//     registers, two CTAs per SM;
+//   * ONE __syncthreads per plane: W and the interpolant derivative live in 4-plane
+//     shared rings aligned with the deformation cells, q_x and q_y in shared planes
+//     double-buffered by parity; the z neighbours of q stay in registers;
+//   * the trilinear value and derivative as f32x2 pairs (FFMA2) over the z corner pairs
+//     (grid ratio 4);
 //   * template reads outside the image hull are redirected to a zero pad after the
 //     volume (one select instead of masking W and three derivatives), and the inside
 //     test compares the float bit patterns of t and n-1 (0 <= t <= n-1 for t >= +0);
@@ -76,7 +79,9 @@ __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
 constexpr unsigned kAdv = 1u << 16;    // i0z(z + 1) == i0z(z) + 1
 constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: central z rows)
 
-template <int RATIO, int K, int NXY = 0, bool PACK = false, bool PIPE = false>
+// PACK (f32x2 trilinear) by default at grid ratio 4; the ratio-2 instances are at the
+// register limit already (PACK spills there)
+template <int RATIO, int K, int NXY = 0, bool PACK = (RATIO == 4), bool PIPE = false>
 struct Lean {
     static constexpr int KX = K, KY = K;
     // NXY > 0: a square NXY x NXY image plane known at compile time, so the 8 template
@@ -422,7 +427,7 @@ struct Lean {
     }
 };
 
-template <int RATIO, int K, int NXY, bool PACK = false, bool PIPE = false>
+template <int RATIO, int K, int NXY, bool PACK = (RATIO == 4), bool PIPE = false>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -512,7 +517,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
         // warp columns d and d + o whose image columns lie 16 banks apart (o = 16 / ratio):
         // with the Fb row pitch of 35 the reads of a warp are conflict-free and its entry
         // list reads are two broadcasts
-        static_assert(kE1Y == 16, "x pass: a half-warp per window column");
+        static_assert(kE1Y <= 16, "x pass: a half-warp per window column");
         unsigned xa = 0xffffu, ya = 0xffffu;
         {
             constexpr int o = RATIO == 2 ? 8 : 4;
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
                 const int j = idx % (2 * o);
                 d = (idx - j) + (j >> 1) + (j & 1) * o;
             }
-            if (d < fp.wx) xa = (unsigned)(lane & 15) | (unsigned)d << 8;
+            if (d < fp.wx && (lane & 15) < kE1Y) xa = (unsigned)(lane & 15) | (unsigned)d << 8;
         }
         if (tid < fp.wy * fp.wx) {
             const int r = tid / fp.wx;
@@ -595,13 +600,15 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 }
 
-template <int RATIO, int K, int NXY>
+template <int RATIO, int K, int NXY, bool PACK = (RATIO == 4), bool PIPE = false>
 static cudaError_t set_smem(size_t smem) {
-    return cudaFuncSetAttribute(k_march_lean<RATIO, K, NXY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    return cudaFuncSetAttribute(k_march_lean<RATIO, K, NXY, PACK, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)smem);
 }
 
 // square power-of-two image planes with a compile-time size (the pyramid levels of the
-// configurations: 32 .. 512); any other plane runs the runtime-size instance
+// configurations: 32 .. 512); any other plane runs the runtime-size instance.  The A/B
+// instances (scalar trilinear, gathers across the barrier) exist for 128 and 256.
 template <int RATIO, int K>
 static cudaError_t set_smem_all(size_t smem) {
     cudaError_t e = set_smem<RATIO, K, 0>(smem);
@@ -610,19 +617,15 @@ static cudaError_t set_smem_all(size_t smem) {
     if (e == cudaSuccess) e = set_smem<RATIO, K, 128>(smem);
     if (e == cudaSuccess) e = set_smem<RATIO, K, 256>(smem);
     if (e == cudaSuccess) e = set_smem<RATIO, K, 512>(smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 256, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e == cudaSuccess)
-        e = cudaFuncSetAttribute(k_march_lean<RATIO, K, 128, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 256, false>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 128, false>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 256, false, true>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 128, false, true>(smem);
     return e;
 }
 
-static bool packed() {
-    static const bool on = std::getenv("NGF_LEAN_PACK") && std::atoi(std::getenv("NGF_LEAN_PACK")) != 0;
+static bool scalar_trilinear() {
+    static const bool on = std::getenv("NGF_LEAN_PACK") && std::atoi(std::getenv("NGF_LEAN_PACK")) == 0;
     return on;
 }
 static bool piped() {
@@ -641,12 +644,12 @@ static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, siz
         NGF_LAUNCH((k_march_lean<RATIO, K, 128, false, true>), grid, kNT, sb, s, a, c);
         return;
     }
-    if (packed() && n == 256) {
-        NGF_LAUNCH((k_march_lean<RATIO, K, 256, true>), grid, kNT, sb, s, a, c);
+    if (scalar_trilinear() && n == 256) {
+        NGF_LAUNCH((k_march_lean<RATIO, K, 256, false>), grid, kNT, sb, s, a, c);
         return;
     }
-    if (packed() && n == 128) {
-        NGF_LAUNCH((k_march_lean<RATIO, K, 128, true>), grid, kNT, sb, s, a, c);
+    if (scalar_trilinear() && n == 128) {
+        NGF_LAUNCH((k_march_lean<RATIO, K, 128, false>), grid, kNT, sb, s, a, c);
         return;
     }
     switch (n) {

@@ -10,8 +10,11 @@ namespace lean {
 
 // Tile: 32 x TYI interior image columns x rows, a one-voxel ring around it (34 x (TYI+2)
 // positions).  Row warps 0..TYI+1 own the 32 columns x0..x0+31 of one E1 row each; one
-// ring-column warp owns columns x0-1 and x0+32 of all TYI+2 rows (16 + 16 lanes), so
-// every lane of every warp holds a position and the tile is exactly 32 wide in x.
+// ring-column warp owns columns x0-1 (lanes 0..TYI+1) and x0+32 (lanes TYI+2..2 TYI+3) of
+// all rows, its other lanes sink, and the tile is exactly 32 wide in x.  TYI 14: 544
+// threads, two CTAs per SM at 56 registers (TYI 13: 512 threads at 64 registers, 2 % faster
+// at 256^3, 5 % at 128^3, but a different f32 summation order of the gradient partials;
+// kept at 14 so that the long registration runs stay comparable to the recorded ones).
 #ifndef NGF_LEAN_TYI
 #define NGF_LEAN_TYI 14
 #endif
