@@ -586,6 +586,24 @@ def run_ours(args):
             batch_info = run_pairs(args, n_pairs, ws, rank, n, ratio, npdt, cfg, barrier,
                                    max_over_ranks)
 
+    if not args.no_register and strong:
+        # config 5: one registration with every level z-slab decomposed over the ranks
+        # (distributed.register_slab; at N = 1 the single slab is the whole volume)
+        from paper_1812_06765_b200.distributed import register_slab
+        cfg = ngf.MultilevelConfig(num_levels=levels, grid_ratio=ratio, precision=args.precision)
+        register_slab(R, T, cfg)  # warm-up
+        barrier()
+        t0 = time.perf_counter()
+        yr, rep = register_slab(R, T, cfg)
+        barrier()
+        reg_s = max_over_ranks(time.perf_counter() - t0)
+        reg = {"seconds": reg_s, "levels": levels, "inputs": f"host numpy {args.precision} (H2D inside)",
+               "decomposition": f"z-slabs x{ws} (distributed.register_slab)",
+               "per_level": [{"image": lv.image_dims[0], "def": lv.def_dims[0],
+                              "iterations": lv.iterations, "evals": lv.evaluations,
+                              "stop": lv.stop_reason} for lv in rep.levels],
+               "probe_error": registration_probe(yr, gi, mapping)}
+
     # ---------------- CPU legs (rank 0, N = 1): parity, baselines, same-box registrations ----
     cpu = parity = cpu_matrix = regs = None
     if rank == 0 and not strong:
