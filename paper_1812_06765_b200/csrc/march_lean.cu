@@ -437,6 +437,10 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
+    // the post kernel (programmatic dependent launch) may be scheduled once every CTA of
+    // this grid has started: its prologue then runs on the SMs the last wave leaves idle,
+    // and it waits (griddepcontrol.wait) for this grid's completion before reading partials
+    asm volatile("griddepcontrol.launch_dependents;");
     // ---- CTA geometry (uniform): grid (x tiles, y tiles, z chunks), dispatched chunk-major
     const int tx = blockIdx.x, ty = blockIdx.y, tzc = blockIdx.z + a.chunk0;
     m.cta = (tzc * fp.nty + ty) * fp.ntx + tx;
