@@ -1,5 +1,6 @@
 // Shared definitions for libngfb200 (sm_100a).  See include/ngf_b200.h for the ABI.
 #pragma once
+#include <utility>
 
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -31,6 +32,31 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
         ::ngf::g_launches.fetch_add(1, std::memory_order_relaxed);                  \
         kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);                 \
     } while (0)
+
+// Launch with programmatic dependent launch (the kernel may start while the previous
+// kernel in the stream drains; it must execute griddepcontrol.wait before touching what
+// that kernel writes or reads).  Plain launch while the stream is being captured.
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
+    ::ngf::g_launches.fetch_add(1, std::memory_order_relaxed);
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cap);
+    if (cap != cudaStreamCaptureStatusNone) {
+        k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
+        return;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, k, std::forward<Args>(args)...);
+}
 
 #define NGF_CHECK_LAUNCH()                                                          \
     do {                                                                            \

@@ -548,6 +548,10 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     for (int r = 0; r < kRing; ++r) m.qz[r] = 0.f;
     m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
     __syncthreads();
+    // launched as a programmatic dependent of the previous kernel in the stream: the
+    // prologue above reads only the plan tables; y, the reference terms, the partials and
+    // dpart wait for that kernel's completion here
+    asm volatile("griddepcontrol.wait;" ::: "memory");
     if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
@@ -641,28 +645,28 @@ template <int RATIO, int K>
 static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, size_t sb, cudaStream_t s) {
     const int n = a.nx == a.ny ? a.nx : 0;
     if (piped() && n == 256) {
-        NGF_LAUNCH((k_march_lean<RATIO, K, 256, false, true>), grid, kNT, sb, s, a, c);
+        launch_pdl(k_march_lean<RATIO, K, 256, false, true>, grid, dim3(kNT), sb, s, a, c);
         return;
     }
     if (piped() && n == 128) {
-        NGF_LAUNCH((k_march_lean<RATIO, K, 128, false, true>), grid, kNT, sb, s, a, c);
+        launch_pdl(k_march_lean<RATIO, K, 128, false, true>, grid, dim3(kNT), sb, s, a, c);
         return;
     }
     if (scalar_trilinear() && n == 256) {
-        NGF_LAUNCH((k_march_lean<RATIO, K, 256, false>), grid, kNT, sb, s, a, c);
+        launch_pdl(k_march_lean<RATIO, K, 256, false>, grid, dim3(kNT), sb, s, a, c);
         return;
     }
     if (scalar_trilinear() && n == 128) {
-        NGF_LAUNCH((k_march_lean<RATIO, K, 128, false>), grid, kNT, sb, s, a, c);
+        launch_pdl(k_march_lean<RATIO, K, 128, false>, grid, dim3(kNT), sb, s, a, c);
         return;
     }
     switch (n) {
-        case 32: NGF_LAUNCH((k_march_lean<RATIO, K, 32>), grid, kNT, sb, s, a, c); break;
-        case 64: NGF_LAUNCH((k_march_lean<RATIO, K, 64>), grid, kNT, sb, s, a, c); break;
-        case 128: NGF_LAUNCH((k_march_lean<RATIO, K, 128>), grid, kNT, sb, s, a, c); break;
-        case 256: NGF_LAUNCH((k_march_lean<RATIO, K, 256>), grid, kNT, sb, s, a, c); break;
-        case 512: NGF_LAUNCH((k_march_lean<RATIO, K, 512>), grid, kNT, sb, s, a, c); break;
-        default: NGF_LAUNCH((k_march_lean<RATIO, K, 0>), grid, kNT, sb, s, a, c); break;
+        case 32: launch_pdl(k_march_lean<RATIO, K, 32>, grid, dim3(kNT), sb, s, a, c); break;
+        case 64: launch_pdl(k_march_lean<RATIO, K, 64>, grid, dim3(kNT), sb, s, a, c); break;
+        case 128: launch_pdl(k_march_lean<RATIO, K, 128>, grid, dim3(kNT), sb, s, a, c); break;
+        case 256: launch_pdl(k_march_lean<RATIO, K, 256>, grid, dim3(kNT), sb, s, a, c); break;
+        case 512: launch_pdl(k_march_lean<RATIO, K, 512>, grid, dim3(kNT), sb, s, a, c); break;
+        default: launch_pdl(k_march_lean<RATIO, K, 0>, grid, dim3(kNT), sb, s, a, c); break;
     }
 }
 
@@ -692,9 +696,9 @@ void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s) 
     else if (c.ratio == 2 && k == 4)
         lean::launch_sized<2, 4>(a, c, grid, fp.smem_bytes, s);
     else if (c.ratio == 2)
-        NGF_LAUNCH((lean::k_march_lean<2, 8, 0>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        launch_pdl((lean::k_march_lean<2, 8, 0>), grid, dim3(lean::kNT), fp.smem_bytes, s, a, c);
     else
-        NGF_LAUNCH((lean::k_march_lean<0, 8, 0>), grid, lean::kNT, fp.smem_bytes, s, a, c);
+        launch_pdl((lean::k_march_lean<0, 8, 0>), grid, dim3(lean::kNT), fp.smem_bytes, s, a, c);
 }
 
 // The per-level control block (kernel parameters) from the host plan.
