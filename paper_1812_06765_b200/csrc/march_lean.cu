@@ -201,7 +201,7 @@ struct Lean {
     // reloaded when q starts a deformation cell), the cell lookup and the 8 template corner
     // reads (outside the hull: the zero pad), left in g[] / f*; q outside the chunk's A
     // range gives zeros (W = 0, derivative 0)
-    template <bool GEN, bool NEWCELL>
+    template <bool GEN, bool NEWCELL, int RS = 0>
     __device__ __forceinline__ void a1(int q) {
         if (GEN && (q < pa0 || q > pa1)) {
 #pragma unroll
@@ -220,7 +220,7 @@ struct Lean {
             }
             load_yplane(min(zd + 1, a.ndz - 1), yhi);
         }
-        const float wz = c.w1[q], wz0 = __fsub_rn(1.0f, wz);
+        const float wz = GEN ? c.w1[q] : c.w1pat[RS], wz0 = __fsub_rn(1.0f, wz);
         const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
         const float yh1 = __fadd_rn(__fmul_rn(ylo[1], wz0), __fmul_rn(yhi[1], wz));
         const float yh2 = __fadd_rn(__fmul_rn(ylo[2], wz0), __fmul_rn(yhi[2], wz));
@@ -290,7 +290,7 @@ struct Lean {
 
         // ------------------------------------------------------------- (A) plane p
         // PIPE: its gathers were issued by the previous step's (A1); else issue them now
-        if constexpr (!PIPE) a1<GEN, (EV & kEvA) != 0>(p);
+        if constexpr (!PIPE) a1<GEN, (EV & kEvA) != 0, R>(p);
         float W, d0, d1, d2;
         a2(W, d0, d1, d2);
         sm.W[R][P] = W;
@@ -298,7 +298,7 @@ struct Lean {
         sm.dT[R][1][P] = d1;
         sm.dT[R][2][P] = d2;
         __syncthreads();
-        if constexpr (PIPE) a1<GEN, (EV & kEvA1) != 0>(p + 1);  // plane p+1's gathers in flight during (B), (C)
+        if constexpr (PIPE) a1<GEN, (EV & kEvA1) != 0, (R + 1) & 3>(p + 1);  // plane p+1's gathers in flight during (B), (C)
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
@@ -381,7 +381,7 @@ struct Lean {
             }
         }
         const float sv = sx + sy + sz;
-        const float w1 = c.w1[j], w0 = __fsub_rn(1.0f, w1);
+        const float w1 = GEN ? c.w1[j] : c.w1pat[RC], w0 = __fsub_rn(1.0f, w1);
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const float g = sv * sm.dT[RC][q][P];
@@ -759,6 +759,11 @@ int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double
             break;
         }
     }
+    if (c->ratio) {
+        // the w1 pattern: four consecutive planes away from the faces, by (plane - phase) mod 4
+        const int z0 = std::min(std::max(4, nz / 2), std::max(nz - 4, 0));
+        for (int k = 0; k < 4 && z0 + k < nz; ++k) c->w1pat[((z0 + k - c->phase) % 4 + 4) % 4] = c->w1[z0 + k];
+    }
     for (int t = 0; t < c->nchunk; ++t) {
         c->s0[t] = c->s1[t] = 0;
         if (!c->ratio) continue;
@@ -774,6 +779,10 @@ int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double
                 const bool want = ((p - c->phase) % c->ratio + c->ratio) % c->ratio == 0;
                 if (adv(p - 1) != want) return false;
             }
+            // the steady steps take w1 of planes s-2 .. s+3 from the 4-plane pattern
+            for (int p = s - 2; p <= s + 3; ++p)
+                if (std::memcmp(&c->w1[p], &c->w1pat[((p - c->phase) % 4 + 4) % 4], sizeof(float)) != 0)
+                    return false;
             for (int p = s; p < s + 4; ++p)
                 if (c->zw[p - 1] >> kFaceShift || c->zw[p - 2] >> kFaceShift) return false;
             return true;

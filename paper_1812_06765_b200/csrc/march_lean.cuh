@@ -48,6 +48,8 @@ struct Ctl {
     int wzlo[kMaxChunks];     // lowest deformation plane of each chunk's P^T window
     unsigned zw[kMaxZ];       // per image plane: i0z (bits 0-15), advance flag, z-face slot
     float w1[kMaxZ];          // f32(w1z)
+    float w1pat[4];           // w1 of a plane in the steady ranges, by (plane - phase) mod 4:
+                              // compile-time constant-bank operands there (no indexed load)
     float faceG[4][8];        // z = 0, 1, nz-2, nz-1: G (cm, c0, cp), G^T (gm, g0, gp)
     float hx2, hy2, hz2;      // 1 / (2 h): central differences
 };
