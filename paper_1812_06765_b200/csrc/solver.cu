@@ -25,21 +25,38 @@ int run_level_graph(ngf_level_t* level, int exact, T* x, T* g, T* d, T* xn, T* g
 
 namespace {
 
-struct PinnedScalars {
+
+// The host-driven loop's scalars (J, D, S, slope at [0..3], the vector statistics at
+// [8..12]) live in mapped page-locked memory: the kernels that produce them store straight
+// to the host, so a round trip is one stream synchronisation with no copy behind it.
+struct MappedScalars {
     double* host = nullptr;
-    ~PinnedScalars() {
+    double* dev = nullptr;
+    ~MappedScalars() {
         if (host) cudaFreeHost(host);
     }
 };
+thread_local MappedScalars t_map;
 
-thread_local PinnedScalars t_pin;
+int mapped_scalars(double** host, double** dev) {
+    if (!t_map.host) {
+        if (cudaHostAlloc((void**)&t_map.host, 16 * sizeof(double), cudaHostAllocMapped) != cudaSuccess)
+            return NGF_ENOMEM;
+        if (cudaHostGetDevicePointer((void**)&t_map.dev, t_map.host, 0) != cudaSuccess) {
+            cudaFreeHost(t_map.host);
+            t_map.host = nullptr;
+            return NGF_ENOMEM;
+        }
+    }
+    *host = t_map.host;
+    *dev = t_map.dev;
+    return 0;
+}
 
-int read_scalars(const double* dev_src, int k, double* out, cudaStream_t s) {
-    if (!t_pin.host && cudaMallocHost((void**)&t_pin.host, 16 * sizeof(double)) != cudaSuccess)
-        return NGF_ENOMEM;
-    NGF_CUDA(cudaMemcpyAsync(t_pin.host, dev_src, k * sizeof(double), cudaMemcpyDeviceToHost, s));
+// scalars stored by the kernels into mapped memory: wait for the stream, then read
+int read_mapped(const double* host_src, int k, double* out, cudaStream_t s) {
     NGF_CUDA(cudaStreamSynchronize(s));
-    std::memcpy(out, t_pin.host, k * sizeof(double));
+    std::memcpy(out, host_src, k * sizeof(double));
     return 0;
 }
 
@@ -98,10 +115,14 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
     };
     void *x = alloc(vb), *g = alloc(vb), *d = alloc(vb), *xn = alloc(vb), *gn = alloc(vb), *xt = alloc(vb),
          *gt = alloc(vb);
-    double* scal = (double*)alloc(4 * sizeof(double));   // J, D, S, slope
+    double* scal = (double*)alloc(4 * sizeof(double));   // J, D, S, slope (graph-driven loop)
     double* stats = (double*)alloc(5 * sizeof(double));  // see ngf_vec_stats / ngf_lbfgs_pair
     std::vector<Pair> free_pairs;
     int rc = (x && g && d && xn && gn && xt && gt && scal && stats) ? 0 : NGF_ENOMEM;
+    double *hm = nullptr, *dm = nullptr;  // host-driven loop: mapped scalars
+    if (!rc) rc = mapped_scalars(&hm, &dm);
+    double* const mscal = dm;      // J, D, S, slope
+    double* const mstats = dm + 8;  // vector statistics
     auto cleanup = [&]() {
         cudaStreamSynchronize(s);
         for (void* p : owned) dev_free(p);
@@ -130,14 +151,14 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
 
     {
         int evals = 0;
-        RUN(ngf_level_eval(level, x, g, scal, exact, s));
+        RUN(ngf_level_eval(level, x, g, mscal, exact, s));
         ++evals;
-        RUN(read_scalars(scal, 3, sc, s));
+        RUN(read_mapped(hm, 3, sc, s));
         double J = sc[0];
         row(sc);
-        RUN(ngf_vec_stats(dtype, g, nullptr, x, nullptr, n, stats, s));
+        RUN(ngf_vec_stats(dtype, g, nullptr, x, nullptr, n, mstats, s));
         double st[5];
-        RUN(read_scalars(stats, 5, st, s));
+        RUN(read_mapped(hm + 8, 5, st, s));
         const double g0_inf = st[4];
         if (g0_inf <= 0.0) {
             res->stop = NGF_STOP_STATIONARY;  // (the reference reports no evaluations here)
@@ -187,17 +208,17 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                 rho[k] = 1.0 / history[k].sy;
             }
             const double gamma = m ? history[m - 1].sy / history[m - 1].yy : 1.0;
-            return ngf_lbfgs_two_loop(dtype, S.data(), Y.data(), rho.data(), gamma, m, g, d, n, scal + 3, s);
+            return ngf_lbfgs_two_loop(dtype, S.data(), Y.data(), rho.data(), gamma, m, g, d, n, mscal + 3, s);
         };
         for (int it = 0; it < cfg->max_iterations; ++it) {
             // direction and (optimistically) the first trial point, one host round trip
             RUN(two_loop());
             double t = cfg->initial_step;
             RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
-            RUN(ngf_level_eval(level, xn, gn, scal, exact, s));
+            RUN(ngf_level_eval(level, xn, gn, mscal, exact, s));
             ++evals;
             double v[4];
-            RUN(read_scalars(scal, 4, v, s));
+            RUN(read_mapped(hm, 4, v, s));
             double Jn = v[0], slope = v[3];
             int ls_evals = 1;
             if (slope >= 0) {  // safeguard: steepest descent (lbfgs.py:113-116)
@@ -206,9 +227,9 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                 history.clear();
                 RUN(two_loop());
                 RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
-                RUN(ngf_level_eval(level, xn, gn, scal, exact, s));
+                RUN(ngf_level_eval(level, xn, gn, mscal, exact, s));
                 ++evals;
-                RUN(read_scalars(scal, 4, v, s));
+                RUN(read_mapped(hm, 4, v, s));
                 Jn = v[0];
                 slope = v[3];
             }
@@ -222,9 +243,9 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                 if (ls_evals >= cfg->max_ls_steps) break;
                 t *= cfg->step_shrink;
                 RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
-                RUN(ngf_level_eval(level, xn, gn, scal, exact, s));
+                RUN(ngf_level_eval(level, xn, gn, mscal, exact, s));
                 ++evals;
-                RUN(read_scalars(scal, 3, v, s));
+                RUN(read_mapped(hm, 3, v, s));
                 Jn = v[0];
                 row(v);
                 ++ls_evals;
@@ -240,9 +261,9 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                 while (ls_evals < cfg->max_ls_steps) {
                     const double t_try = t / cfg->step_shrink;
                     RUN(ngf_vec_axpy_step(dtype, x, t_try, d, xt, n, s));
-                    RUN(ngf_level_eval(level, xt, gt, scal, exact, s));
+                    RUN(ngf_level_eval(level, xt, gt, mscal, exact, s));
                     ++evals;
-                    RUN(read_scalars(scal, 3, v, s));
+                    RUN(read_mapped(hm, 3, v, s));
                     const double Jt = v[0];
                     row(v);
                     ++ls_evals;
@@ -269,8 +290,8 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                     goto done;
                 }
             }
-            RUN(ngf_lbfgs_pair(dtype, xn, x, gn, g, pair.s, pair.y, n, stats, s));
-            RUN(read_scalars(stats, 4, st, s));
+            RUN(ngf_lbfgs_pair(dtype, xn, x, gn, g, pair.s, pair.y, n, mstats, s));
+            RUN(read_mapped(hm + 8, 4, st, s));
             const double sy = st[0], ss = st[1], yy = st[2], g_inf = st[3];
             pair.sy = sy;
             pair.yy = yy;
