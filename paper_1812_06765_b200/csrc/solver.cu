@@ -210,6 +210,14 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
             const double gamma = m ? history[m - 1].sy / history[m - 1].yy : 1.0;
             return ngf_lbfgs_two_loop(dtype, S.data(), Y.data(), rho.data(), gamma, m, g, d, n, mscal + 3, s);
         };
+        // Speculation on small levels (an evaluation costs about as much as a host round
+        // trip there): the first forward-expansion trial (t = 2 t0 into xt / gt, its scalars
+        // in slots 4..6) is issued together with the first trial when the previous
+        // iteration accepted its first trial, and used only if the reference's control flow
+        // reaches it (Armijo holds at t0, no safeguard); otherwise it is dropped uncounted.
+        // The evaluations, their order and every decision are those of the serial loop.
+        const bool spec_level = n <= 3 * 32768 && cfg->max_ls_steps > 1;
+        bool t0_accepted = true;
         for (int it = 0; it < cfg->max_iterations; ++it) {
             // direction and (optimistically) the first trial point, one host round trip
             RUN(two_loop());
@@ -217,11 +225,17 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
             RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
             RUN(ngf_level_eval(level, xn, gn, mscal, exact, s));
             ++evals;
+            bool have_spec = spec_level && t0_accepted;
+            if (have_spec) {
+                RUN(ngf_vec_axpy_step(dtype, x, t / cfg->step_shrink, d, xt, n, s));
+                RUN(ngf_level_eval(level, xt, gt, mscal + 4, exact, s));
+            }
             double v[4];
             RUN(read_mapped(hm, 4, v, s));
             double Jn = v[0], slope = v[3];
             int ls_evals = 1;
             if (slope >= 0) {  // safeguard: steepest descent (lbfgs.py:113-116)
+                have_spec = false;
                 --evals;       // the optimistic trial above is discarded
                 for (const Pair& p : history) free_pairs.push_back(p);
                 history.clear();
@@ -240,6 +254,7 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                     accepted = true;
                     break;
                 }
+                have_spec = false;
                 if (ls_evals >= cfg->max_ls_steps) break;
                 t *= cfg->step_shrink;
                 RUN(ngf_vec_axpy_step(dtype, x, t, d, xn, n, s));
@@ -256,14 +271,20 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
                 res->evaluations = evals;
                 goto done;
             }
+            t0_accepted = t == cfg->initial_step;
             if (t == cfg->initial_step) {
                 // forward expansion while Armijo holds and J decreases (lbfgs.py:133-143)
                 while (ls_evals < cfg->max_ls_steps) {
                     const double t_try = t / cfg->step_shrink;
-                    RUN(ngf_vec_axpy_step(dtype, x, t_try, d, xt, n, s));
-                    RUN(ngf_level_eval(level, xt, gt, mscal, exact, s));
+                    if (have_spec) {  // already evaluated, issued with the first trial
+                        have_spec = false;
+                        std::memcpy(v, hm + 4, 3 * sizeof(double));
+                    } else {
+                        RUN(ngf_vec_axpy_step(dtype, x, t_try, d, xt, n, s));
+                        RUN(ngf_level_eval(level, xt, gt, mscal, exact, s));
+                        RUN(read_mapped(hm, 3, v, s));
+                    }
                     ++evals;
-                    RUN(read_mapped(hm, 3, v, s));
                     const double Jt = v[0];
                     row(v);
                     ++ls_evals;
