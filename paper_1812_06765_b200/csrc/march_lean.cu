@@ -307,8 +307,16 @@ struct Lean {
                 const float* Wk = &sm.W[RB][P];
                 const float wl = Wk[-1], wr = Wk[1], wu = Wk[-kE1X], wd = Wk[kE1X];
                 const float wzm = sm.W[RC][P], wzp = sm.W[R][P];
-                float gx = (wr - wl) * c.hx2;
-                float gy = (wd - wu) * c.hy2;
+                float gx, gy;
+                if constexpr (PACK) {  // the x and y central differences as one f32x2 pair
+                    const float2 gxy = __fmul2_rn(__fadd2_rn(make_float2(wr, wd), make_float2(-wl, -wu)),
+                                                  make_float2(c.hx2, c.hy2));
+                    gx = gxy.x;
+                    gy = gxy.y;
+                } else {
+                    gx = (wr - wl) * c.hx2;
+                    gy = (wd - wu) * c.hy2;
+                }
                 if (wface_b) {  // warp holds a position next to an x / y volume face
                     const int ey = P / kE1X, ex = P - ey * kE1X;
                     const float w0 = Wk[0];
@@ -339,8 +347,16 @@ struct Lean {
                 const float t1 = r * inv_nt;
                 const float cf = a.neg_hbar * t1;
                 qz[RB] = cf * fmaf(-t1, gz, rt.z);
-                sm.Qx[RB & 1][P + 1] = cf * fmaf(-t1, gx, rt.x);
-                sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
+                if constexpr (PACK) {
+                    const float2 qxy = __fmul2_rn(make_float2(cf, cf),
+                                                  __ffma2_rn(make_float2(-t1, -t1), make_float2(gx, gy),
+                                                             make_float2(rt.x, rt.y)));
+                    sm.Qx[RB & 1][P + 1] = qxy.x;
+                    sm.Qy[RB & 1][P + kE1X] = qxy.y;
+                } else {
+                    sm.Qx[RB & 1][P + 1] = cf * fmaf(-t1, gx, rt.x);
+                    sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
+                }
                 // reference terms of plane p for the next step's (B)
                 if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * nxy_() + ij);
             }
@@ -359,8 +375,16 @@ struct Lean {
         const float* qxj = &sm.Qx[RC & 1][P + 1];
         const float* qyj = &sm.Qy[RC & 1][P + kE1X];
         const float ql = qxj[-1], qr = qxj[1], qu = qyj[-kE1X], qd = qyj[kE1X];
-        float sx = (ql - qr) * c.hx2;
-        float sy = (qu - qd) * c.hy2;
+        float sx, sy;
+        if constexpr (PACK) {
+            const float2 sxy = __fmul2_rn(__fadd2_rn(make_float2(ql, qu), make_float2(-qr, -qd)),
+                                          make_float2(c.hx2, c.hy2));
+            sx = sxy.x;
+            sy = sxy.y;
+        } else {
+            sx = (ql - qr) * c.hx2;
+            sy = (qu - qd) * c.hy2;
+        }
         if (wface_c) {
             const int ey = P / kE1X, ex = P - ey * kE1X;
             if (fl & 1u) {  // exact transposed face rows (warp.py:168-175)
@@ -385,8 +409,14 @@ struct Lean {
 #pragma unroll
         for (int q = 0; q < 3; ++q) {
             const float g = sv * sm.dT[RC][q][P];
-            A0[q] = fmaf(w0, g, A0[q]);
-            A1[q] = fmaf(w1, g, A1[q]);
+            if constexpr (PACK) {  // both deformation planes' accumulators in one FFMA2
+                const float2 acc = __ffma2_rn(make_float2(w0, w1), make_float2(g, g), make_float2(A0[q], A1[q]));
+                A0[q] = acc.x;
+                A1[q] = acc.y;
+            } else {
+                A0[q] = fmaf(w0, g, A0[q]);
+                A1[q] = fmaf(w1, g, A1[q]);
+            }
         }
         if (GEN ? flushes(j) : (EV & kEvF) != 0) {
             put_flush(A0);
