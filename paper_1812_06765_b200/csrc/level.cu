@@ -856,10 +856,11 @@ static int eval_host_pipelined(ngf_level* L, const void* y_host, void* grad_host
     if (int rc = pipe_init(L)) return rc;
     PipeState& ps = *L->pipe;
     // The totals go straight into the page-locked scalars (mapped); the gradient planes of
-    // the last part too (its post kernel's stores cross PCIe, no copy after it), the other
-    // parts' planes by copies as they complete.  NGF_PIPE_MAPPED: 0 copies only, 1 every
-    // part mapped, 2 (default) the last part mapped.
-    static const int map_mode = std::getenv("NGF_PIPE_MAPPED") ? std::atoi(std::getenv("NGF_PIPE_MAPPED")) : 2;
+    // the last two parts too (their post kernels' stores cross PCIe, no copy after them:
+    // both finish with the march's last wave), the other parts' planes by copies as they
+    // complete.  NGF_PIPE_MAPPED: 0 copies only, 1 every part mapped, 2 the last part
+    // mapped, 3 (default) the last two.
+    static const int map_mode = std::getenv("NGF_PIPE_MAPPED") ? std::atoi(std::getenv("NGF_PIPE_MAPPED")) : 3;
     const bool mapped_ok = map_mode != 0;
     void* g_map = nullptr;
     void* sc_map = nullptr;
@@ -919,7 +920,7 @@ static int eval_host_pipelined(ngf_level* L, const void* y_host, void* grad_host
         // last post block to finish over all parts: every post block counts, and each runs
         // after the marches its part waited for, so the last one runs after all of them.
         for (int j = 0; j < i; ++j) NGF_CUDA(cudaStreamWaitEvent(si, ps.evM[j], 0));
-        const bool gmap = mapped && (map_mode == 1 || i == P - 1);
+        const bool gmap = mapped && (map_mode == 1 || i == P - 1 || (map_mode == 3 && i == P - 2));
         float* gout = gmap ? (float*)g_map : (float*)L->hg;
         if (pc[i + 1] > pc[i])
             if (int rc = fused_post_range<float>(a, L->def, L->alpha, L->spart, L->ns, L->flag, gout, sout, si, pc[i],
