@@ -1,5 +1,6 @@
 // Shared definitions for libngfb200 (sm_100a).  See include/ngf_b200.h for the ABI.
 #pragma once
+#include <cstdlib>
 #include <utility>
 
 #include <cuda_runtime.h>
@@ -39,9 +40,10 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args&&... args) {
     ::ngf::g_launches.fetch_add(1, std::memory_order_relaxed);
+    static const bool pdl_off = std::getenv("NGF_NO_PDL") != nullptr;
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     cudaStreamIsCapturing(s, &cap);
-    if (cap != cudaStreamCaptureStatusNone) {
+    if (pdl_off || cap != cudaStreamCaptureStatusNone) {
         k<<<grid, block, smem, s>>>(std::forward<Args>(args)...);
         return;
     }

@@ -216,7 +216,8 @@ extern "C" int ngf_lbfgs_run_level(ngf_level_t* level, int dtype, int exact, voi
         // iteration accepted its first trial, and used only if the reference's control flow
         // reaches it (Armijo holds at t0, no safeguard); otherwise it is dropped uncounted.
         // The evaluations, their order and every decision are those of the serial loop.
-        const bool spec_level = n <= 3 * 32768 && cfg->max_ls_steps > 1;
+        static const bool spec_on = !(std::getenv("NGF_LBFGS_SPEC") && std::atoi(std::getenv("NGF_LBFGS_SPEC")) == 0);
+        const bool spec_level = spec_on && n <= 3 * 32768 && cfg->max_ls_steps > 1;
         bool t0_accepted = true;
         for (int it = 0; it < cfg->max_iterations; ++it) {
             // direction and (optimistically) the first trial point, one host round trip

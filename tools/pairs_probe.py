@@ -2,6 +2,7 @@
 and a bitwise comparison of every field with the sequential run.
 
     python tools/pairs_probe.py [--pairs 16] [--n 256]
+    SCHED=1|2|4 python tools/pairs_probe.py ...   # context scheduling: spin / yield / blocking sync
 """
 import argparse
 import os
@@ -10,6 +11,14 @@ import threading
 import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+if os.environ.get("SCHED"):  # cudaDeviceScheduleSpin 1 / Yield 2 / BlockingSync 4, before the context exists
+    import ctypes
+    import glob
+    import torch as _t  # noqa: F401  (loads torch's cudart)
+    import nvidia
+    _cr = glob.glob(os.path.join(nvidia.__path__[0], "cuda_runtime", "lib", "libcudart.so*"))
+    _rt = ctypes.CDLL(_cr[0] if _cr else "libcudart.so.12")
+    print("cudaSetDeviceFlags", int(os.environ["SCHED"]), "->", _rt.cudaSetDeviceFlags(int(os.environ["SCHED"])))
 import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
