@@ -984,6 +984,9 @@ int ngf_level_eval_host(ngf_level_t* L, const void* y_host, void* grad_host, dou
         if (dev_alloc(&L->hx, vb) || dev_alloc(&L->hg, vb) || dev_alloc((void**)&L->hsc, 4 * sizeof(double)))
             return NGF_ENOMEM;
         NGF_CUDA(cudaHostAlloc((void**)&L->hsc_pin, 4 * sizeof(double), cudaHostAllocDefault));
+        // the buffers come from the stream-ordered pool on the legacy stream: complete the
+        // allocations before any other stream (the caller's, the pipeline's) touches them
+        NGF_CUDA(cudaStreamSynchronize(0));
     }
     if (mode == 0) {
         const int rc = eval_host_pipelined(L, y_host, grad_host, scalars_host, s);
