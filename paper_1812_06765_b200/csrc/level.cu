@@ -458,6 +458,7 @@ static int fused_setup(ngf_level* L, int zlo, int zhi, cudaStream_t stream = 0) 
         if (int rc = lean_ctl_build(p->h_i0[2], w1z.data(), nz, ndz, L->img.spacing[2], bounds, wz,
                                     L->img.spacing[0], L->img.spacing[1], L->ctl))
             return rc;
+        lean_rt_map(L->ctl, L->RT, nx, ny, nz);
         fp.lean_ctl = L->ctl;
         build_list(0, kTX, fp.ntx, fp.wx, fp.kx, xl, lxv);
         build_list(1, fp.ty, fp.nty, fp.wy, fp.ky, yl, lyv);

@@ -69,6 +69,18 @@ struct Smem {
     double red[kWarps];
 };
 
+// TMA instances: the reference terms of the tile interior of a plane land here by one
+// tensor copy per plane, issued two steps ahead into a 4-slot ring (slot = ring slot of the
+// plane), one mbarrier per slot; appended to Smem (128-byte aligned) in their dynamic
+// shared memory only
+struct RtBuf {
+    float4 v[kRing][kTYI][32];
+    unsigned long long bar[kRing];
+};
+constexpr size_t kRtOff = (sizeof(Smem) + 127) / 128 * 128;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+
 __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
     // a0 * (1 - w) + a1 * w, each op correctly rounded (transfer.py:126)
     return __fadd_rn(__fmul_rn(a0, w0), __fmul_rn(a1, w));
@@ -81,7 +93,7 @@ constexpr int kFaceShift = 17;         // bits 17-19: z-face slot + 1 (0: centra
 
 // PACK (f32x2 trilinear) by default at grid ratio 4; the ratio-2 instances are at the
 // register limit already (PACK spills there)
-template <int RATIO, int K, int NXY = 0, bool PACK = (RATIO == 4), bool PIPE = false>
+template <int RATIO, int K, int NXY = 0, bool PACK = (RATIO == 4), bool PIPE = false, bool TMA = false>
 struct Lean {
     static constexpr int KX = K, KY = K;
     // NXY > 0: a square NXY x NXY image plane known at compile time, so the 8 template
@@ -94,6 +106,7 @@ struct Lean {
     const FusedArgs<float>& a;
     const Ctl& c;
     Smem& sm;
+    RtBuf* rb;  // TMA instances only
     int P;         // flat E1 index ey * 34 + ex of this thread's position
     unsigned ij;   // yy * nx + x (reference-term offset inside a plane)
     unsigned fl;   // bit 0: x face, bit 1: y face, bit 2: interior position
@@ -108,7 +121,33 @@ struct Lean {
     float4 rt;
     float dacc;
 
-    __device__ __forceinline__ Lean(const FusedArgs<float>& a_, const Ctl& c_, Smem& sm_) : a(a_), c(c_), sm(sm_) {}
+    __device__ __forceinline__ Lean(const FusedArgs<float>& a_, const Ctl& c_, Smem& sm_)
+        : a(a_), c(c_), sm(sm_), rb(reinterpret_cast<RtBuf*>(reinterpret_cast<unsigned char*>(&sm_) + kRtOff)) {}
+
+    // TMA: the tile interior's reference terms of plane q into ring slot `slot` (thread 0)
+    __device__ __forceinline__ void issue_rt(int q, int slot) const {
+        const unsigned b = smem_u32(&rb->bar[slot]), d = smem_u32(&rb->v[slot][0][0]);
+        constexpr unsigned kBytes = sizeof(rb->v[0]);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(kBytes) : "memory");
+        asm volatile(
+            "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], "
+            "[%6];" ::"r"(d),
+            "l"(reinterpret_cast<uint64_t>(&c.rt_map)), "r"(0), "r"((int)blockIdx.x * 32), "r"((int)blockIdx.y * kTYI),
+            "r"(q), "r"(b)
+            : "memory");
+    }
+    // wait for plane k's terms in slot `slot` (the n-th fill of the slot in this chunk has
+    // parity n & 1, n = (k - z0) / 4)
+    __device__ __forceinline__ void wait_rt(int k, int slot) const {
+        const unsigned b = smem_u32(&rb->bar[slot]), par = (unsigned)((k - z0) >> 2) & 1u;
+        asm volatile(
+            "{\n\t.reg .pred p;\n"
+            "WAIT_RT_%=:\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+            "@!p bra WAIT_RT_%=;\n}" ::"r"(b),
+            "r"(par)
+            : "memory");
+    }
 
     __device__ __forceinline__ void load_yplane(int zd, float (&out)[3]) const {
         // P_xy y on def plane zd at this position's image (x, y): x then y (transfer.py:136-142)
@@ -299,11 +338,20 @@ struct Lean {
         sm.dT[R][2][P] = d2;
         __syncthreads();
         if constexpr (PIPE) a1<GEN, (EV & kEvA1) != 0, (R + 1) & 3>(p + 1);  // plane p+1's gathers in flight during (B), (C)
+        // TMA: the reference terms of plane p+1 (used by (B) two steps later); its slot's
+        // previous plane (p-3) was read by (B) of step p-2, before this barrier
+        if constexpr (TMA) {
+            if (threadIdx.x == 0 && (!GEN || (p + 1 >= z0 && p + 1 < z1))) issue_rt(p + 1, (R + 1) & 3);
+        }
 
         // ------------------------------------------------------------- (B) q on plane k = p-1
         const int k = p - 1;
         if (!GEN || (k >= z0 && k < z1)) {
             if (bwarp) {
+                if constexpr (TMA) {
+                    wait_rt(k, RB);
+                    rt = rb->v[RB][(threadIdx.x >> 5) - 1][threadIdx.x & 31];
+                }
                 const float* Wk = &sm.W[RB][P];
                 const float wl = Wk[-1], wr = Wk[1], wu = Wk[-kE1X], wd = Wk[kE1X];
                 const float wzm = sm.W[RC][P], wzp = sm.W[R][P];
@@ -358,7 +406,8 @@ struct Lean {
                     sm.Qy[RB & 1][P + kE1X] = cf * fmaf(-t1, gy, rt.y);
                 }
                 // reference terms of plane p for the next step's (B)
-                if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * nxy_() + ij);
+                if constexpr (!TMA)
+                    if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * nxy_() + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
@@ -457,12 +506,12 @@ struct Lean {
     }
 };
 
-template <int RATIO, int K, int NXY, bool PACK = (RATIO == 4), bool PIPE = false>
+template <int RATIO, int K, int NXY, bool PACK = (RATIO == 4), bool PIPE = false, bool TMA = false>
 __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ FusedArgs<float> a,
                                                        const __grid_constant__ Ctl c) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
+    extern __shared__ __align__(128) unsigned char smem_raw[];
     Smem& sm = *reinterpret_cast<Smem*>(smem_raw);
-    Lean<RATIO, K, NXY, PACK, PIPE> m(a, c, sm);
+    Lean<RATIO, K, NXY, PACK, PIPE, TMA> m(a, c, sm);
     constexpr int KX = K, KY = K;
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -577,12 +626,22 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
 #pragma unroll
     for (int r = 0; r < kRing; ++r) m.qz[r] = 0.f;
     m.rt = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (TMA) {
+        if (tid == 0) {
+            for (int r = 0; r < kRing; ++r)
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&m.rb->bar[r])) : "memory");
+            asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        }
+    }
     __syncthreads();
     // launched as a programmatic dependent of the previous kernel in the stream: the
     // prologue above reads only the plan tables; y, the reference terms, the partials and
     // dpart wait for that kernel's completion here
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
+    if constexpr (!TMA) {
+        if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
+    }
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
     // aligned to the plane phase (ring slot = (p - phase) mod 4); groups inside the chunk's
@@ -638,10 +697,10 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     }
 }
 
-template <int RATIO, int K, int NXY, bool PACK = (RATIO == 4), bool PIPE = false>
+template <int RATIO, int K, int NXY, bool PACK = (RATIO == 4), bool PIPE = false, bool TMA = false>
 static cudaError_t set_smem(size_t smem) {
-    return cudaFuncSetAttribute(k_march_lean<RATIO, K, NXY, PACK, PIPE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)smem);
+    return cudaFuncSetAttribute(k_march_lean<RATIO, K, NXY, PACK, PIPE, TMA>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 // square power-of-two image planes with a compile-time size (the pyramid levels of the
@@ -659,6 +718,8 @@ static cudaError_t set_smem_all(size_t smem) {
     if (e == cudaSuccess) e = set_smem<RATIO, K, 128, false>(smem);
     if (e == cudaSuccess) e = set_smem<RATIO, K, 256, false, true>(smem);
     if (e == cudaSuccess) e = set_smem<RATIO, K, 128, false, true>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 256, (RATIO == 4), false, true>(smem);
+    if (e == cudaSuccess) e = set_smem<RATIO, K, 128, (RATIO == 4), false, true>(smem);
     return e;
 }
 
@@ -670,10 +731,22 @@ static bool piped() {
     static const bool on = std::getenv("NGF_LEAN_PIPE") && std::atoi(std::getenv("NGF_LEAN_PIPE")) != 0;
     return on;
 }
+static bool tma_rt() {
+    static const bool on = std::getenv("NGF_LEAN_TMA") && std::atoi(std::getenv("NGF_LEAN_TMA")) != 0;
+    return on;
+}
 
 template <int RATIO, int K>
 static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, size_t sb, cudaStream_t s) {
     const int n = a.nx == a.ny ? a.nx : 0;
+    if (tma_rt() && c.rt_map_ok && n == 256) {
+        launch_pdl(k_march_lean<RATIO, K, 256, (RATIO == 4), false, true>, grid, dim3(kNT), sb, s, a, c);
+        return;
+    }
+    if (tma_rt() && c.rt_map_ok && n == 128) {
+        launch_pdl(k_march_lean<RATIO, K, 128, (RATIO == 4), false, true>, grid, dim3(kNT), sb, s, a, c);
+        return;
+    }
     if (piped() && n == 256) {
         launch_pdl(k_march_lean<RATIO, K, 256, false, true>, grid, dim3(kNT), sb, s, a, c);
         return;
@@ -702,7 +775,36 @@ static void launch_sized(const FusedArgs<float>& a, const Ctl& c, dim3 grid, siz
 
 }  // namespace lean
 
-size_t lean_smem(int, int) { return sizeof(lean::Smem); }
+size_t lean_smem(int, int) {
+    return lean::tma_rt() ? lean::kRtOff + sizeof(lean::RtBuf) : sizeof(lean::Smem);
+}
+
+int lean_rt_map(lean::Ctl* c, const void* rt, int nx, int ny, int nz) {
+    using Encode = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+    static const Encode encode = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            cudaGetLastError();
+            return (Encode) nullptr;
+        }
+        return (Encode)f;
+    }();
+    c->rt_map_ok = 0;
+    if (!encode || !rt) return 0;
+    const cuuint64_t dims[4] = {4, (cuuint64_t)nx, (cuuint64_t)ny, (cuuint64_t)nz};
+    const cuuint64_t strides[3] = {16, 16ull * nx, 16ull * nx * ny};
+    const cuuint32_t box[4] = {4, 32, (cuuint32_t)lean::kTYI, 1};
+    const cuuint32_t es[4] = {1, 1, 1, 1};
+    const CUresult r = encode(&c->rt_map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, const_cast<void*>(rt), dims, strides, box,
+                              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    c->rt_map_ok = r == CUDA_SUCCESS ? 1 : 0;
+    return 0;
+}
 
 int lean_prepare(size_t smem) {
     static std::mutex mu;

@@ -1,6 +1,7 @@
 // Lean fused march (f32, sm_100a): declarations shared with the host planner (level.cu)
 // and the dispatcher (eval_fused.cu).  See march_lean.cu for the design.
 #pragma once
+#include <cuda.h>  // CUtensorMap (the encode entry point is fetched at run time)
 #include <vector>
 
 #include "fused_impl.cuh"
@@ -38,7 +39,9 @@ constexpr int kMaxChunks = 128;  // z chunks per level
 
 // Per-level control of the march, passed as a kernel parameter (constant bank) and indexed
 // by the CTA-uniform plane counter so that every branch of the march is uniform.
-struct Ctl {
+struct alignas(64) Ctl {
+    CUtensorMap rt_map;       // TMA descriptor of the packed reference terms (4, nx, ny, nz) f32
+    int rt_map_ok;            // rt_map was encoded (the TMA instances may run)
     int nchunk;
     int ratio;                // 2 or 4: deformation cells of `ratio` planes in the steady range; 0: none
     int phase;                // a deformation cell starts at every plane = phase (mod 4) in the steady range
@@ -64,6 +67,8 @@ int ws_prepare(size_t smem);
 void ws_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s);
 size_t lean_smem(int kx, int ky);
 void lean_launch(const FusedArgs<float>& a, const lean::Ctl& c, cudaStream_t s);
+// the reference-term tensor map of a level (box: one tile interior of one plane); 0 or an error
+int lean_rt_map(lean::Ctl* c, const void* rt, int nx, int ny, int nz);
 int lean_ctl_build(const int32_t* i0z, const float* w1z, int nz, int ndz, double hz, const std::vector<int>& bounds,
                    const std::vector<int>& wzlo, double hx, double hy, lean::Ctl* c);
 

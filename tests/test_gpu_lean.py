@@ -82,3 +82,23 @@ def test_lean_not_selected_when_ineligible():
     R = ngf.smooth_random_volume(gi, seed=1).values.astype(np.float32)
     obj = _obj(R, R, gd, gi)
     assert lib().ngf_level_variant(obj.level.handle) != 6
+
+
+@pytest.mark.parametrize("n,ratio", [(128, 2), (256, 4)])
+def test_tma_reference_terms_instance_is_bit_identical(n, ratio, tmp_path):
+    """The opt-in instance that brings the reference terms in by TMA tensor copies
+    (NGF_LEAN_TMA=1: one cp.async.bulk.tensor per plane into a 4-slot mbarrier ring) gives
+    the same J and gradient bits as the default instance (separate processes: the switch
+    is read once per process)."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = []
+    for env_tma in ("0", "1"):
+        out = tmp_path / f"lean_{env_tma}.npz"
+        env = dict(os.environ, NGF_LEAN_TMA=env_tma)
+        subprocess.run([sys.executable, os.path.join(root, "tools", "lean_dump.py"), str(n), str(ratio), str(out)],
+                       check=True, env=env, cwd=root)
+        outs.append(np.load(out))
+    assert float(outs[0]["J"]) == float(outs[1]["J"])
+    assert np.array_equal(outs[0]["g"], outs[1]["g"])
