@@ -83,6 +83,16 @@ constexpr size_t kRtOff = (sizeof(Smem) + 127) / 128 * 128;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
 
+// the reference terms are read once: keep them out of L1 (room for the template lines;
+// `profiles/r02_ab_rt_no_allocate.txt`: -0.3 % at 256^3, -0.6 % at 512^3 against ld.global.cs)
+__device__ __forceinline__ float4 ld_rt_na(const float4* p) {
+    float4 v;
+    asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+                 : "l"(p));
+    return v;
+}
+
 __device__ __forceinline__ float lerp_x(float a0, float a1, float w, float w0) {
     // a0 * (1 - w) + a1 * w, each op correctly rounded (transfer.py:126)
     return __fadd_rn(__fmul_rn(a0, w0), __fmul_rn(a1, w));
@@ -458,7 +468,7 @@ struct Lean {
                 }
                 // reference terms of plane p for the next step's (B)
                 if constexpr (!TMA)
-                    if ((!GEN || p < z1) && (fl & 4u)) rt = __ldcs(a.RT + (size_t)p * nxy_() + ij);
+                    if ((!GEN || p < z1) && (fl & 4u)) rt = ld_rt_na(a.RT + (size_t)p * nxy_() + ij);
             }
         } else if (GEN && bwarp) {  // no q on this plane (chunk edges)
             qz[RB] = 0.f;
@@ -692,7 +702,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // dpart wait for that kernel's completion here
     asm volatile("griddepcontrol.wait;" ::: "memory");
     if constexpr (!TMA) {
-        if (inter && m.z0 < m.z1) m.rt = __ldcs(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
+        if (inter && m.z0 < m.z1) m.rt = ld_rt_na(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
     }
 
     // planes p = z0-1 .. z1+2: (A) on p, (B) on p-1, (C) on p-2, in groups of four steps
