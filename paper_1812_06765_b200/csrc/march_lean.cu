@@ -533,10 +533,6 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     const FusedPlan& fp = a.fp;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
 
-    // the post kernel (programmatic dependent launch) may be scheduled once every CTA of
-    // this grid has started: its prologue then runs on the SMs the last wave leaves idle,
-    // and it waits (griddepcontrol.wait) for this grid's completion before reading partials
-    asm volatile("griddepcontrol.launch_dependents;");
     // ---- CTA geometry (uniform): grid (x tiles, y tiles, z chunks), dispatched chunk-major
     const int tx = blockIdx.x, ty = blockIdx.y, tzc = blockIdx.z + a.chunk0;
     m.cta = (tzc * fp.nty + ty) * fp.ntx + tx;
@@ -656,6 +652,12 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
     // prologue above reads only the plan tables; y, the reference terms, the partials and
     // dpart wait for that kernel's completion here
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    // the post kernel (programmatic dependent launch) may be scheduled once every CTA of this
+    // grid is here: its prologue (which reads y) then runs on the SMs the last wave leaves
+    // idle, and it waits (griddepcontrol.wait) for this grid's completion before reading the
+    // partials.  Not earlier: before this grid's own wait, the kernel that wrote y (this
+    // grid's predecessor) may still be running.
+    asm volatile("griddepcontrol.launch_dependents;");
     if constexpr (!TMA) {
         if (inter && m.z0 < m.z1) m.rt = ld_rt_na(a.RT + (size_t)m.z0 * ((size_t)a.nx * a.ny) + m.ij);
     }
