@@ -51,6 +51,7 @@ constexpr int kRing = 4;             // plane ring: slot = (plane - phase) mod 4
 
 // events of a steady-state step (compile-time schedule, see Lean::block)
 constexpr unsigned kEvA = 1, kEvF = 2, kEvX = 4, kEvY = 8, kEvA1 = 16;  // kEvA1: plane p+1 starts a cell
+constexpr unsigned kEvXN = 32;  // plane p+2 starts a cell: stage its x-interpolated deformation rows
 
 struct Smem {
     float W[kRing][kPl];                  // W of planes p-3 .. p (ring by (plane - phase) mod 4)
@@ -60,6 +61,7 @@ struct Smem {
     float Fb[3][kPl];                     // completed deformation plane (z-reduced ghat / h), rows
                                           // of kFbPitch (bank-conflict-free x pass)
     float Xr[3][kE1Y][kWXP];           // x-reduced (odd pitch)
+    float Xs[3][kWYM][kE1X];           // the next cell's deformation rows interpolated in x
     int2 xl[kKMax][kWXM];              // x pass: (E1 column, weight bits) per entry, window output
     int2 yl[kWYM][kKMax];              // y pass: (E1 row, weight bits)
     float colG[kE1X][3], colGt[kE1X][3], rowG[kE1Y][3], rowGt[kE1Y][3];
@@ -127,6 +129,7 @@ struct Lean {
     float ylo[3], yhi[3];
     float g[8], gfx, gfy, gfz;  // the template corners and cell fractions of the next (A2)
     float qz[kRing];
+    bool xok;   // Xs holds the rows of the next cell (staged by a steady step two planes ago)
     float A0[3], A1[3];
     float4 rt;
     float dacc;
@@ -177,6 +180,37 @@ struct Lean {
             const float X1 = lerp_x(__ldg(a.y + (o + dy)), __ldg(a.y + (o + dy + dx)), wx, wx0);
             out[k] = lerp_x(X0, X1, wy, wy0);
         }
+    }
+
+    // the x lerps of P_xy (transfer.py:136-142) for plane zd on the tile's deformation rows,
+    // shared by all positions: one (row, column) per thread over the three components, on
+    // the last warps (the ring-column and ring-row warps run no (B))
+    __device__ __forceinline__ void stage_x(int zd) const {
+        const int t = kNT - 1 - (int)threadIdx.x, wy = a.fp.wy;
+        if (t < wy * kE1X) {
+            const int r = t / kE1X, ex = t - r * kE1X;
+            const int j = min(sm.rowP0[0] + r, a.ndy - 1);
+            const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
+            const float wx = sm.colPw[ex], wx0 = __fsub_rn(1.0f, wx);
+            const unsigned mm = (unsigned)(a.ndx * a.ndy * a.ndz);
+            const unsigned o = (unsigned)zd * (unsigned)(a.ndx * a.ndy) + (unsigned)(j * a.ndx);
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                const unsigned ok = o + (unsigned)k * mm;
+                sm.Xs[k][r][ex] = lerp_x(__ldg(a.y + (ok + (unsigned)x0)), __ldg(a.y + (ok + (unsigned)x1)), wx, wx0);
+            }
+        }
+    }
+
+    // P_xy y of the staged plane at this position: the y lerp of two staged rows (the same
+    // operations as load_yplane)
+    __device__ __forceinline__ void yplane_from_x(float (&out)[3]) const {
+        const int ey = min(P / kE1X, kE1Y - 1), ex = P - (P / kE1X) * kE1X;
+        const int j0 = sm.rowP0[0];
+        const int r0 = sm.rowP0[ey] - j0, r1 = sm.rowP1[ey] - j0;
+        const float wy = sm.rowPw[ey], wy0 = __fsub_rn(1.0f, wy);
+#pragma unroll
+        for (int k = 0; k < 3; ++k) out[k] = lerp_x(sm.Xs[k][r0][ex], sm.Xs[k][r1][ex], wy, wy0);
     }
 
     // one axis of the cell lookup (warp.py:38-53): t = (p - o) / h (power-of-two h: an
@@ -267,7 +301,10 @@ struct Lean {
 #pragma unroll
                 for (int k = 0; k < 3; ++k) ylo[k] = yhi[k];
             }
-            load_yplane(min(zd + 1, a.ndz - 1), yhi);
+            if (!GEN && !PIPE && xok)
+                yplane_from_x(yhi);
+            else
+                load_yplane(min(zd + 1, a.ndz - 1), yhi);
         }
         const float wz = GEN ? c.w1[q] : c.w1pat[RS], wz0 = __fsub_rn(1.0f, wz);
         const float yh0 = __fadd_rn(__fmul_rn(ylo[0], wz0), __fmul_rn(yhi[0], wz));
@@ -355,6 +392,13 @@ struct Lean {
         sm.dT[R][2][P] = d2;
         __syncthreads();
         if constexpr (PIPE) a1<GEN, (EV & kEvA1) != 0, (R + 1) & 3>(p + 1);  // plane p+1's gathers in flight during (B), (C)
+        // the x lerps of the cell starting at plane p+2 (read by its (A) after the next barrier;
+        // the previous staging was read by (A) of plane p, before this barrier)
+        if constexpr (!GEN && !PIPE && (EV & kEvXN) != 0) {
+            stage_x(min((int)(c.zw[p + 2] & 0xffffu) + 1, a.ndz - 1));
+            xok = true;
+        }
+        if constexpr (GEN) xok = false;
         // TMA: the reference terms of plane p+1 (used by (B) two steps later); its slot's
         // previous plane (p-3) was read by (B) of step p-2, before this barrier
         if constexpr (TMA) {
@@ -510,12 +554,12 @@ struct Lean {
         if constexpr (RATIO == 4) {
             step<0, false, kEvA>(p);
             step<1, false, kEvF>(p + 1);
-            step<2, false, kEvX>(p + 2);
+            step<2, false, kEvX | kEvXN>(p + 2);
             step<3, false, kEvY | kEvA1>(p + 3);
         } else if constexpr (RATIO == 2) {
-            step<0, false, kEvA | kEvX>(p);
+            step<0, false, kEvA | kEvX | kEvXN>(p);
             step<1, false, kEvF | kEvY | kEvA1>(p + 1);
-            step<2, false, kEvA | kEvX>(p + 2);
+            step<2, false, kEvA | kEvX | kEvXN>(p + 2);
             step<3, false, kEvF | kEvY | kEvA1>(p + 3);
         } else {
             generic4(p);
@@ -634,6 +678,7 @@ __global__ void __launch_bounds__(kNT, 2) k_march_lean(const __grid_constant__ F
 
     // ---- march state
     m.dacc = 0.f;
+    m.xok = false;
 #pragma unroll
     for (int r = 0; r < 3; ++r) m.ylo[r] = m.yhi[r] = m.A0[r] = m.A1[r] = 0.f;
 #pragma unroll
