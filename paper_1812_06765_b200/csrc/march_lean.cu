@@ -206,8 +206,10 @@ struct Lean {
     // operations as load_yplane)
     __device__ __forceinline__ void yplane_from_x(float (&out)[3]) const {
         const int ey = min(P / kE1X, kE1Y - 1), ex = P - (P / kE1X) * kE1X;
-        const int j0 = sm.rowP0[0];
-        const int r0 = sm.rowP0[ey] - j0, r1 = sm.rowP1[ey] - j0;
+        const int j0 = sm.rowP0[0], top = a.fp.wy - 1;
+        // rows outside the volume carry index 0 in the tables (their samples go to the zero
+        // pad whatever yhat is): clamp them onto staged rows, never read outside Xs
+        const int r0 = min(max(sm.rowP0[ey] - j0, 0), top), r1 = min(max(sm.rowP1[ey] - j0, 0), top);
         const float wy = sm.rowPw[ey], wy0 = __fsub_rn(1.0f, wy);
 #pragma unroll
         for (int k = 0; k < 3; ++k) out[k] = lerp_x(sm.Xs[k][r0][ex], sm.Xs[k][r1][ex], wy, wy0);
