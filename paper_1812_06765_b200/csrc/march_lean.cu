@@ -40,6 +40,18 @@
 namespace ngf {
 namespace lean {
 
+// NGF_LEAN_CHECKS: trap on any shared-memory index outside its array (debug builds)
+#ifdef NGF_LEAN_CHECKS
+#define LEAN_CHECK(c) \
+    do {              \
+        if (!(c)) __trap(); \
+    } while (0)
+#else
+#define LEAN_CHECK(c) \
+    do {              \
+    } while (0)
+#endif
+
 constexpr int kPlane = kE1Y * kE1X;  // positions, row stride 34 for every per-position plane
 constexpr int kSink = kPlane;        // the position of ring-column lanes beyond 2 * kE1Y
 constexpr int kPl = kPlane + kE1X + 2;  // per-position plane incl. the sink and its neighbours
@@ -166,6 +178,7 @@ struct Lean {
         // P_xy y on def plane zd at this position's image (x, y): x then y (transfer.py:136-142)
         // (the sink lanes read a valid table entry; their samples are redirected to the pad)
         const int ey = min(P / kE1X, kE1Y - 1), ex = P - (P / kE1X) * kE1X;
+        LEAN_CHECK(ex >= 0 && ex < kE1X && ey >= 0 && ey < kE1Y);
         const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
         const int y0 = sm.rowP0[ey], y1 = sm.rowP1[ey];
         const float wx = sm.colPw[ex], wy = sm.rowPw[ey];
@@ -189,6 +202,7 @@ struct Lean {
         const int t = kNT - 1 - (int)threadIdx.x, wy = a.fp.wy;
         if (t < wy * kE1X) {
             const int r = t / kE1X, ex = t - r * kE1X;
+            LEAN_CHECK(r >= 0 && r < kWYM && ex >= 0 && ex < kE1X);
             const int j = min(sm.rowP0[0] + r, a.ndy - 1);
             const int x0 = sm.colP0[ex], x1 = sm.colP1[ex];
             const float wx = sm.colPw[ex], wx0 = __fsub_rn(1.0f, wx);
@@ -210,6 +224,7 @@ struct Lean {
         // rows outside the volume carry index 0 in the tables (their samples go to the zero
         // pad whatever yhat is): clamp them onto staged rows, never read outside Xs
         const int r0 = min(max(sm.rowP0[ey] - j0, 0), top), r1 = min(max(sm.rowP1[ey] - j0, 0), top);
+        LEAN_CHECK(ex >= 0 && ex < kE1X && ey >= 0 && ey < kE1Y && r0 >= 0 && r1 < kWYM && top < kWYM);
         const float wy = sm.rowPw[ey], wy0 = __fsub_rn(1.0f, wy);
 #pragma unroll
         for (int k = 0; k < 3; ++k) out[k] = lerp_x(sm.Xs[k][r0][ex], sm.Xs[k][r1][ex], wy, wy0);
@@ -229,6 +244,7 @@ struct Lean {
     __device__ __forceinline__ void xpass() const {
         const unsigned f = sm.fa[threadIdx.x];
         const int xr_r = f & 0xff, xr_d = (f >> 8) & 0xff;
+        LEAN_CHECK(xr_r == 0xff || (xr_r < kE1Y && xr_d < kWXM));
         if (xr_r != 0xff) {
             float s0 = 0.f, s1 = 0.f, s2 = 0.f;
             const float* fb = &sm.Fb[0][0] + xr_r * kFbPitch;
@@ -236,6 +252,7 @@ struct Lean {
             for (int k = 0; k < KX; ++k) {
                 const int2 e = sm.xl[k][xr_d];
                 const float w = __int_as_float(e.y);
+                LEAN_CHECK(e.x >= 0 && xr_r * kFbPitch + e.x < kPl);
                 s0 = fmaf(w, fb[e.x], s0);
                 s1 = fmaf(w, fb[kPl + e.x], s1);
                 s2 = fmaf(w, fb[2 * kPl + e.x], s2);
@@ -250,12 +267,14 @@ struct Lean {
     __device__ __forceinline__ void ypass(int zs) const {
         const unsigned f = sm.fa[threadIdx.x];
         const int yp_dy = (f >> 16) & 0xff, yp_d = f >> 24;
+        LEAN_CHECK(yp_dy == 0xff || (yp_dy < kWYM && yp_d < kWXM));
         if (yp_dy != 0xff) {
             float s0 = 0.f, s1 = 0.f, s2 = 0.f;
 #pragma unroll
             for (int k = 0; k < KY; ++k) {
                 const int2 e = sm.yl[yp_dy][k];
                 const float w = __int_as_float(e.y);
+                LEAN_CHECK(e.x >= 0 && e.x < kE1Y);
                 s0 = fmaf(w, sm.Xr[0][e.x][yp_d], s0);
                 s1 = fmaf(w, sm.Xr[1][e.x][yp_d], s1);
                 s2 = fmaf(w, sm.Xr[2][e.x][yp_d], s2);
@@ -271,6 +290,7 @@ struct Lean {
 
     __device__ __forceinline__ void put_flush(const float (&acc)[3]) {
         const int f = P + P / kE1X;  // row pitch kFbPitch (the sink lands past the last row)
+        LEAN_CHECK(f >= 0 && f < kPl);
         sm.Fb[0][f] = acc[0];
         sm.Fb[1][f] = acc[1];
         sm.Fb[2][f] = acc[2];
